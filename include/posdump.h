@@ -1,0 +1,244 @@
+/*
+ * posdump.h -- C ABI of the B200-native buffer-dump hot path of the POS
+ * checkpoint engine (libposdump.so).
+ *
+ * The reference (gpucrsim, /root/reference/proj) is a header-only C++20
+ * library with no FFI; its hot path is a set of CrEngine member functions.
+ * Each entry point below names the reference function it replaces
+ * (path:line relative to /root/reference/proj).  INTEGRATION.md shows the
+ * call site a maintainer would change and the ctypes / C++ bindings.
+ *
+ * Conventions
+ *  - plain pointers and sizes; device addresses are uint64_t; streams are
+ *    cudaStream_t passed as void* (NULL = legacy default stream);
+ *  - every function returns int: 0 (POS_OK) or a code that maps 1:1 onto the
+ *    reference's Errc (include/gpucrsim/errors.hpp:9-25) as POS_E_<Errc> =
+ *    1 + enum index, plus POS_E_CUDA / POS_E_NO_DEVICE for the runtime;
+ *  - no exceptions cross the ABI; pos_last_error() gives the message;
+ *  - not re-entrant per context (the reference is single-threaded,
+ *    SPEC.md:104-105); distinct contexts may be used from distinct threads.
+ */
+#ifndef POSDUMP_H
+#define POSDUMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POSDUMP_ABI_VERSION 1
+
+enum {
+  POS_OK = 0,
+  /* 1 + gpucrsim::Errc index (errors.hpp:9-25) */
+  POS_E_PAST_TIME = 1,
+  POS_E_LIVELOCK = 2,
+  POS_E_OUT_OF_DEVICE_MEMORY = 3,
+  POS_E_INVALID_LOCATOR = 4,
+  POS_E_USE_AFTER_FREE = 5,
+  POS_E_FREED_BUFFER = 6,
+  POS_E_BAD_STATE = 7,
+  POS_E_PENDING_KERNELS = 8,
+  POS_E_UNKNOWN_API = 9,
+  POS_E_INVALID_ARGUMENT = 10,
+  POS_E_CORRUPT_DAG = 11,
+  POS_E_CORRUPT_IMAGE = 12,
+  POS_E_INVARIANT_VIOLATION = 13,
+  POS_E_STAGING_EXHAUSTED = 14,
+  POS_E_ORACLE_MISMATCH = 15,
+  /* runtime */
+  POS_E_CUDA = 64,
+  POS_E_NO_DEVICE = 65
+};
+
+typedef struct pos_ctx pos_ctx;
+
+/* SimConfig keys of the path (include/gpucrsim/config.hpp:18-45). */
+typedef struct pos_config {
+  uint64_t chunk_size;       /* chunk_size (config.hpp:25); any value > 0 (config.hpp:70-71) */
+  uint64_t page_size;        /* page_size (config.hpp:26) */
+  uint64_t cache_capacity;   /* O3 on-device cache bytes; 0 => staging_capacity() */
+  double staging_fraction;   /* staging_fraction (config.hpp:35); 0 => 1/16 */
+  int32_t device;            /* CUDA ordinal */
+  int32_t dedup;             /* dedup (config.hpp:36) */
+} pos_config;
+
+/* One active allocation of the checkpointed process: the fields of
+ * GpuBuffer (buffer.hpp:27-41) and Upstream (buffer.hpp:20-25) the path reads. */
+typedef struct pos_buffer_desc {
+  uint64_t handle;             /* BufferHandle (buffer.hpp:14) */
+  uint64_t dev_ptr;            /* device address of the allocation */
+  uint64_t size;               /* GpuBuffer::size, > 0 (buffer.hpp:109) */
+  uint32_t has_upstream;       /* GpuBuffer::upstream.has_value() (buffer.hpp:37) */
+  uint32_t upstream_crc;       /* Upstream::crc (buffer.hpp:23) */
+  uint32_t host_untouched;     /* range_write_seq <= Upstream::host_write_seq (cr.hpp:420) */
+  uint32_t written_since_ckpt; /* GpuBuffer::written_since_ckpt (buffer.hpp:34) */
+} pos_buffer_desc;
+
+/* ---- errors --------------------------------------------------------- */
+const char* pos_strerror(int code);
+/* Message of the last failing call on this thread. */
+const char* pos_last_error(void);
+int pos_abi_version(void);
+
+/* ---- context ---------------------------------------------------------- */
+/* Replaces the CrEngine session state (cr.hpp:1271-1321): digest tables,
+ * dirty bitmap, O3 cache, CUDA events.  Fails with POS_E_NO_DEVICE when no
+ * CUDA device is present (there is no CPU fallback). */
+int pos_ctx_create(const pos_config* cfg, pos_ctx** out);
+int pos_ctx_destroy(pos_ctx* ctx);
+
+/* snapshot_buffers_ = active_handles() (cr.hpp:346): the buffer set of the
+ * dump, ascending handle.  Resets the epoch (next hash is "fresh"). */
+int pos_register_buffers(pos_ctx* ctx, const pos_buffer_desc* bufs, uint32_t n);
+/* Refresh provenance / written bits of one registered buffer, e.g. after
+ * note_h2d_provenance (process.hpp:505-522). */
+int pos_update_buffer(pos_ctx* ctx, const pos_buffer_desc* buf);
+int pos_num_chunks(pos_ctx* ctx, uint64_t* out);
+
+/* ---- O2: chunk digests + dirty bitmap ---------------------------------- */
+/* digest[g] = crc32(chunk g) for every chunk of every registered buffer
+ * (per-chunk form of crc32.hpp:26-34 as applied at cr.hpp:419);
+ * flag[g] = (no previous epoch) || digest[g] != previous digest[g]; sets the
+ * dirty bitmap.  Replaces the O2 branch of plan_precopy (cr.hpp:396-401),
+ * refined from buffer to chunk granularity. */
+int pos_hash_chunks(pos_ctx* ctx, void* stream);
+/* The current digest table becomes the comparison base of the next epoch
+ * (finalize_image clearing written_since_ckpt, cr.hpp:745). */
+int pos_commit_epoch(pos_ctx* ctx);
+int pos_read_digests(pos_ctx* ctx, uint32_t* host, uint64_t n, void* stream);
+int pos_read_flags(pos_ctx* ctx, uint8_t* host, uint64_t n, void* stream);
+int pos_read_bitmap(pos_ctx* ctx, uint32_t* host, uint64_t nwords, void* stream);
+
+/* ---- O1: whole-buffer CRC + dedup verdicts ----------------------------- */
+/* crc[b] = crc32(buffer b) folded from the chunk digests (the value
+ * scan_dedup computes, cr.hpp:419, and note_h2d_provenance records,
+ * process.hpp:518); verdict[b] = has_upstream && crc == upstream_crc &&
+ * host_untouched && !dag_dirty (cr.hpp:420-421, 720). Requires
+ * pos_hash_chunks on the same stream first. */
+int pos_buffer_crc(pos_ctx* ctx, void* stream);
+int pos_read_buffer_crcs(pos_ctx* ctx, uint32_t* crcs, uint8_t* verdicts, uint32_t n,
+                         void* stream);
+
+/* ---- DAG write sets ------------------------------------------------------ */
+/* dirty_set_ |= spec_writes (record_dirty, cr.hpp:901-931).  Handles not in
+ * the snapshot are ignored, as in the reference. */
+int pos_record_dirty(pos_ctx* ctx, const uint64_t* handles, uint32_t n);
+int pos_clear_dirty(pos_ctx* ctx);
+
+/* ---- O3: compaction into the on-device cache ---------------------------- */
+/* Packs every flagged chunk of every non-dedup buffer (and, when
+ * exclude_dag_dirty, outside dirty_set_: chunk_copied abandons those,
+ * cr.hpp:487) into the cache as a POSD pack, in
+ * (handle, chunk) order, at cache offset 0.  Replaces enqueue_buffer_copy /
+ * chunk_copied (cr.hpp:447-504) and stage_buffers (cr.hpp:858-888).
+ * Synchronises `stream` once to learn the pack size; the copy itself is left
+ * running on `stream`.  POS_E_STAGING_EXHAUSTED if it does not fit. */
+int pos_compact(pos_ctx* ctx, int exclude_dag_dirty, void* stream, uint64_t* pack_bytes);
+
+/* ---- STW delta-copy --------------------------------------------------- */
+/* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is
+ * hashed and copied into the cache as a second POSD pack starting at
+ * *pack_offset (256-B aligned, after the pre-copy pack), refreshing their
+ * digests.  Asynchronous on `stream`. */
+int pos_delta_copy(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes);
+
+/* ---- host leg ------------------------------------------------------------- */
+/* Pinned D2H of cache[offset, offset+bytes) into host_dst, on `stream`, in
+ * slices of at most slice_bytes (0 => 8 MiB) so application copies queued on
+ * other streams interleave (engines.hpp:153-159). */
+int pos_d2h_async(pos_ctx* ctx, void* host_dst, uint64_t offset, uint64_t bytes,
+                  uint64_t slice_bytes, void* stream);
+int pos_cache_info(pos_ctx* ctx, uint64_t* dev_ptr, uint64_t* capacity);
+
+/* ---- restore scatter ------------------------------------------------------ */
+/* Apply a POSD pack resident in device memory onto the registered buffers
+ * (materialize/load_complete, cr.hpp:1026-1084).  POS_E_CORRUPT_IMAGE for a
+ * malformed pack, POS_E_INVALID_LOCATOR for an entry outside its buffer or
+ * an unknown handle.  Synchronises `stream` once to validate. */
+int pos_scatter(pos_ctx* ctx, uint64_t pack_dev_ptr, uint64_t pack_bytes, void* stream);
+
+/* Host side of the same scatter: apply a POSD pack held in host memory onto
+ * host copies of the buffers (the checkpoint target's image of captured_,
+ * cr.hpp:499-501).  hosts[i]/sizes[i] belong to handles[i] (ascending).
+ * Entries are applied with `threads` host threads (0 => 1). */
+int pos_pack_apply_host(const uint8_t* pack, uint64_t pack_bytes, const uint64_t* handles,
+                        uint8_t* const* hosts, const uint64_t* sizes, uint32_t n,
+                        uint32_t threads);
+
+/* ---- device crc32 (crc32.hpp:26-34 over device memory) ---------------- */
+int pos_crc32(uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream);
+int pos_crc32_update(uint32_t crc, uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream);
+
+/* ---- synthetic writes ------------------------------------------------- */
+/* dst[0..n) = fill_bytes(seed) (rng.hpp:43-54): the kernel effect of
+ * apply_kernel_effect (process.hpp:256-259).  Asynchronous. */
+int pos_fill(uint64_t dev_ptr, uint64_t n, uint64_t seed, void* stream);
+/* Batched form: ranges[i] = {dev_ptr, n, seed}. */
+int pos_fill_batch(const uint64_t* ranges, uint32_t count, void* stream);
+
+/* ---- timing ----------------------------------------------------------- */
+int pos_event_record(pos_ctx* ctx, uint32_t slot, void* stream);
+int pos_event_elapsed(pos_ctx* ctx, uint32_t a, uint32_t b, float* ms);
+/* `stream` waits for event `slot` (cross-stream drain: the STW delta-copy
+ * waits for the application stream, cr.hpp:591-597). */
+int pos_stream_wait_event(pos_ctx* ctx, uint32_t slot, void* stream);
+/* Kernels this context has launched (monotone counter). */
+int pos_launch_count(pos_ctx* ctx, uint64_t* out);
+/* Device time of the most recent hash kernel launch (ms). */
+int pos_last_kernel_ms(pos_ctx* ctx, const char* which, float* ms);
+
+/* ---- POSI image (image.hpp:136-207, canonical writer) ------------------ */
+typedef struct pos_image_rec {
+  uint64_t handle;
+  uint32_t kind;               /* 0 Inline, 1 DedupRef, 2 Recompute (image.hpp:42) */
+  uint32_t n_recompute;
+  const uint8_t* inline_bytes; /* host bytes of the buffer (kind 0) */
+  uint64_t inline_len;
+  uint64_t dedup_first_page;
+  uint32_t dedup_page_count, dedup_offset, dedup_crc, reserved;
+  const uint64_t* recompute;
+} pos_image_rec;
+typedef struct pos_image_alloc {
+  uint64_t handle, base, size;
+} pos_image_alloc;
+typedef struct pos_image_page {
+  uint64_t index;
+  const uint8_t* bytes; /* page_size bytes */
+} pos_image_page;
+typedef struct pos_image_desc {
+  uint64_t page_size;
+  const pos_image_page* pages; uint32_t n_pages;
+  const pos_image_rec* recs; uint32_t n_recs;
+  const pos_image_alloc* allocs; uint32_t n_allocs;
+  const uint64_t* stream_ids; uint32_t n_streams;
+  uint64_t cursor, next_handle, next_base;
+  const uint8_t* dag_bytes; uint64_t dag_len;
+} pos_image_desc;
+/* Byte-identical to gpucrsim::write_image.  *size always receives the image
+ * size; bytes are written when cap >= size. */
+int pos_image_write(const pos_image_desc* img, uint8_t* out, uint64_t cap, uint64_t* size);
+
+/* ---- plumbing (device memory / streams for hosts without their own) ---- */
+int pos_device_count(int* n);
+int pos_set_device(int device);
+int pos_dev_malloc(uint64_t bytes, uint64_t* dev_ptr);
+int pos_dev_free(uint64_t dev_ptr);
+int pos_host_malloc_pinned(uint64_t bytes, void** host);
+int pos_host_free_pinned(void* host);
+/* kind: 1 H2D, 2 D2H, 3 D2D (cudaMemcpyKind); asynchronous on `stream`. */
+int pos_memcpy(uint64_t dst, uint64_t src, uint64_t bytes, int kind, void* stream);
+int pos_memset(uint64_t dev_ptr, int value, uint64_t bytes, void* stream);
+int pos_stream_create(void** stream);
+int pos_stream_destroy(void* stream);
+int pos_stream_sync(void* stream);
+int pos_device_sync(void);
+/* Cross-stream ordering: `waiter` waits for work queued so far on `signaller`. */
+int pos_stream_wait(void* waiter, void* signaller);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POSDUMP_H */

@@ -1,0 +1,216 @@
+// ref_shim.cpp -- extern "C" wrappers over the UNMODIFIED reference headers
+// (/root/reference/proj/include/gpucrsim), compiled by oracle/Makefile into
+// oracle/_ref/libgpucrsim_ref.so.
+//
+// TEST INFRASTRUCTURE ONLY: used to pin the C restatement (posdump_oracle.c)
+// against the reference's own code, to generate tests/golden/, and as the
+// reference CPU arm of bench.py.  No reference source is copied here; the
+// headers are included from where they lie.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <thread>
+#include <vector>
+
+#include "gpucrsim/buffer.hpp"
+#include "gpucrsim/crc32.hpp"
+#include "gpucrsim/image.hpp"
+#include "gpucrsim/rng.hpp"
+#include "gpucrsim/workload.hpp"
+
+#include <sstream>
+
+using namespace gpucrsim;
+
+extern "C" {
+
+uint32_t ref_crc32(const void* p, uint64_t n) { return crc32(p, n); }
+uint32_t ref_crc32_update(uint32_t c, const void* p, uint64_t n) { return crc32_update(c, p, n); }
+uint64_t ref_mix64(uint64_t a, uint64_t b) { return mix64(a, b); }
+uint64_t ref_fnv1a(const void* p, uint64_t n, uint64_t h) { return fnv1a(p, n, h); }
+void ref_make_bytes(uint64_t seed, uint8_t* out, uint64_t n) {
+  std::vector<uint8_t> v = make_bytes(seed, n);
+  std::memcpy(out, v.data(), n);
+}
+
+// Chunk geometry through the reference's own allocator + GpuBuffer
+// (buffer.hpp:44-49, :101-124).  Returns chunk count; fills out[] if given.
+uint32_t ref_chunk_geometry(uint64_t size, uint64_t chunk_size, uint64_t* out) {
+  DeviceMemory dev(size + (1ull << 20), chunk_size);
+  BufferHandle h = dev.alloc(size);
+  const GpuBuffer& b = dev.at(h);
+  if (out)
+    for (uint32_t i = 0; i < b.chunk_count(); ++i) out[i] = b.chunk_bytes(i);
+  return b.chunk_count();
+}
+
+// ---- image encode/decode (image.hpp:136-361) -------------------------------
+
+struct ref_rec_t {
+  uint64_t handle;
+  uint32_t kind;
+  uint32_t n_recompute;
+  const uint8_t* inline_bytes;
+  uint64_t inline_len;
+  uint64_t dedup_first_page;
+  uint32_t dedup_page_count, dedup_offset, dedup_crc, pad;
+  const uint64_t* recompute;
+};
+struct ref_alloc_t {
+  uint64_t handle, base, size;
+};
+struct ref_page_t {
+  uint64_t index;
+  const uint8_t* bytes;
+};
+
+uint64_t ref_write_image(uint64_t page_size, const ref_page_t* pages, uint32_t npages,
+                         const ref_rec_t* recs, uint32_t nrecs, const ref_alloc_t* allocs,
+                         uint32_t nallocs, const uint64_t* streams, uint32_t nstreams,
+                         uint64_t cursor, uint64_t next_handle, uint64_t next_base,
+                         const uint8_t* dag, uint64_t dag_len, uint8_t* out, uint64_t cap) {
+  CheckpointImage img;
+  img.page_size = page_size;
+  for (uint32_t i = 0; i < npages; ++i)
+    img.host_pages.push_back({pages[i].index, {pages[i].bytes, pages[i].bytes + page_size}});
+  for (uint32_t i = 0; i < nrecs; ++i) {
+    GpuBufferRec r;
+    r.handle = recs[i].handle;
+    r.kind = static_cast<GpuRecordKind>(recs[i].kind);
+    if (r.kind == GpuRecordKind::Inline)
+      r.inline_bytes.assign(recs[i].inline_bytes, recs[i].inline_bytes + recs[i].inline_len);
+    r.dedup_first_page = recs[i].dedup_first_page;
+    r.dedup_page_count = recs[i].dedup_page_count;
+    r.dedup_offset = recs[i].dedup_offset;
+    r.dedup_crc = recs[i].dedup_crc;
+    for (uint32_t k = 0; k < recs[i].n_recompute; ++k) r.recompute_nodes.push_back(recs[i].recompute[k]);
+    img.gpu_records.push_back(std::move(r));
+  }
+  for (uint32_t i = 0; i < nallocs; ++i)
+    img.meta.allocs.push_back({allocs[i].handle, allocs[i].base, allocs[i].size});
+  for (uint32_t i = 0; i < nstreams; ++i) img.meta.stream_ids.push_back(streams[i]);
+  img.meta.cursor = cursor;
+  img.meta.next_handle = next_handle;
+  img.meta.next_base = next_base;
+  if (dag_len) img.dag_bytes.assign(dag, dag + dag_len);
+  std::vector<uint8_t> bytes = write_image(img);
+  if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+  return bytes.size();
+}
+
+// 0 = valid, else 1 + offset of the CorruptImageError (image.hpp:209-361).
+uint64_t ref_read_image_check(const uint8_t* p, uint64_t n) {
+  try {
+    std::vector<uint8_t> v(p, p + n);
+    (void)read_image(v);
+    return 0;
+  } catch (const CorruptImageError& e) {
+    return 1 + e.offset();
+  }
+}
+
+// ---- reference CPU dump path (the --impl reference arm) --------------------
+// One "process" worth of GpuBuffers (buffer.hpp:27-97) plus the captured_
+// map of CrEngine (cr.hpp:1300).  ref_state_dump runs, per chunk, the
+// reference's digest crc32 (crc32.hpp:26-34) and, for dirty chunks, the
+// chunk_copied() capture: read_content + std::copy into captured_[h]
+// (cr.hpp:488-501).  Buffers are split across `threads` std::threads
+// (parallel-for over buffers; the reference itself is single-threaded).
+struct RefState {
+  DeviceMemory dev;
+  std::vector<BufferHandle> handles;
+  std::map<BufferHandle, std::vector<uint8_t>> captured;
+  uint64_t chunk_size;
+  RefState(uint64_t cap, uint64_t cs) : dev(cap, cs), chunk_size(cs) {}
+};
+
+void* ref_state_create(uint32_t n, const uint64_t* sizes, const uint8_t* const* contents,
+                       uint64_t chunk_size) {
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) total += sizes[i];
+  auto* s = new RefState(total + (1ull << 20), chunk_size);
+  for (uint32_t i = 0; i < n; ++i) {
+    BufferHandle h = s->dev.alloc(sizes[i]);
+    s->dev.at(h).write_content(0, contents[i], sizes[i]);
+    s->handles.push_back(h);
+    s->captured[h].assign(sizes[i], 0);
+  }
+  return s;
+}
+
+void ref_state_destroy(void* p) { delete static_cast<RefState*>(p); }
+
+// prev/cur are digest tables over global chunk order; flags out.  Returns
+// number of dirty chunks.  prev_valid == 0 marks every chunk dirty (fresh).
+uint64_t ref_state_dump(void* p, const uint32_t* prev, int prev_valid, uint32_t* cur,
+                        uint8_t* flags, uint32_t threads) {
+  auto* s = static_cast<RefState*>(p);
+  std::vector<uint64_t> first(s->handles.size() + 1, 0);
+  for (size_t i = 0; i < s->handles.size(); ++i)
+    first[i + 1] = first[i] + s->dev.at(s->handles[i]).chunk_count();
+  // Pre-touch captured_ entries so worker threads never mutate the map.
+  std::vector<std::vector<uint8_t>*> dst;
+  for (BufferHandle h : s->handles) dst.push_back(&s->captured[h]);
+  std::vector<uint64_t> dirty(threads ? threads : 1, 0);
+  auto work = [&](uint32_t t, uint32_t nt) {
+    for (size_t i = t; i < s->handles.size(); i += nt) {
+      const GpuBuffer& b = s->dev.at(s->handles[i]);
+      for (uint32_t ci = 0; ci < b.chunk_count(); ++ci) {
+        uint64_t g = first[i] + ci, off = static_cast<uint64_t>(ci) * b.chunk_size;
+        uint64_t len = b.chunk_bytes(ci);
+        uint32_t d = crc32(b.content().data() + off, len);
+        cur[g] = d;
+        bool is_dirty = !prev_valid || prev[g] != d;
+        flags[g] = is_dirty;
+        if (!is_dirty) continue;
+        ++dirty[t];
+        std::vector<uint8_t> bytes = b.read_content(off, len);
+        std::copy(bytes.begin(), bytes.end(), dst[i]->begin() + static_cast<ptrdiff_t>(off));
+      }
+    }
+  };
+  uint32_t nt = threads ? threads : 1;
+  if (nt == 1) {
+    work(0, 1);
+  } else {
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < nt; ++t) pool.emplace_back(work, t, nt);
+    for (auto& th : pool) th.join();
+  }
+  uint64_t total = 0;
+  for (uint64_t d : dirty) total += d;
+  return total;
+}
+
+// Overwrite a byte range of buffer i (epoch writes for the baseline).
+void ref_state_write(void* p, uint32_t i, uint64_t off, const uint8_t* data, uint64_t len) {
+  auto* s = static_cast<RefState*>(p);
+  s->dev.at(s->handles[i]).write_content(off, data, len);
+}
+
+// Copy out captured_[h] of buffer i.
+void ref_state_captured(void* p, uint32_t i, uint8_t* out) {
+  auto* s = static_cast<RefState*>(p);
+  const auto& v = s->captured[s->handles[i]];
+  std::memcpy(out, v.data(), v.size());
+}
+
+// gen_workload (workload.hpp:162-410) for a named desk profile
+// (workload.hpp:461-529) with total_bytes / kernel durations overridden; the
+// trace as JSON lines (api.hpp:125-160).  Returns the byte length.
+uint64_t ref_gen_workload(const char* profile, uint64_t total_bytes, uint64_t p50_ns,
+                          uint64_t p99_ns, uint64_t seed, char* out, uint64_t cap) {
+  WorkloadProfile p = profile_by_name(profile, seed);
+  if (total_bytes) p.total_bytes = total_bytes;
+  if (p50_ns) p.p50_ns = p50_ns;
+  if (p99_ns) p.p99_ns = p99_ns;
+  std::ostringstream os;
+  write_trace(os, gen_workload(p));
+  std::string s = os.str();
+  if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+  return s.size();
+}
+
+}  // extern "C"

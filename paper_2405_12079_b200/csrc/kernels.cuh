@@ -1,0 +1,642 @@
+// kernels.cuh -- sm_100a kernels of the buffer-dump hot path.
+//
+//   k_hash_chunks<COPY>  O2 digest + dirty bitmap (COPY=false), or the STW
+//                        delta-copy: digest + gather into a POSD pack (COPY=true)
+//   k_buffer_crc         O1: whole-buffer CRC folded from chunk digests + verdict
+//   k_pack_scan          deterministic (handle, chunk)-ordered pack layout
+//   k_copy_bulk          TMA bulk copies (cp.async.bulk) staged through smem
+//   k_copy_simt          16-B vector / byte copy for unaligned items
+//   k_pack_items         restore: POSD entries -> scatter copy items
+//   k_fill               fill_bytes(seed) (rng.hpp:43-54) into device memory
+//
+// See DESIGN.md for the data layout and the roofline of each kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "crc_math.h"
+
+namespace posdump {
+
+// ---------------------------------------------------------------------------
+// Shared device structures (mirrored on the host in posdump.cu).
+
+struct DevBuf {              // one registered allocation (GpuBuffer, buffer.hpp:27-41)
+  uint64_t ptr;              // device address
+  uint64_t size;             // bytes
+  uint64_t handle;           // BufferHandle
+  uint64_t chunk_base;       // global index of chunk 0
+  uint32_t nchunks;          // ceil(size / chunk_size) (buffer.hpp:119)
+  uint32_t k_tail;           // zeros_crc(last chunk length)
+  uint32_t x8_tail;          // x^(8 * last chunk length) mod P
+  uint32_t flags;            // kBuf* bits
+  uint32_t upstream_crc;     // Upstream::crc
+  uint32_t pad[3];
+};
+static_assert(sizeof(DevBuf) == 64, "DevBuf layout");
+
+enum : uint32_t {
+  kBufHasUpstream = 1u,
+  kBufHostUntouched = 2u,
+  kBufWrittenSinceCkpt = 8u,
+};
+
+struct CopyItem {            // one contiguous copy: chunk -> pack, or pack -> chunk
+  uint64_t src;
+  uint64_t dst;
+  uint64_t len;              // payload bytes
+  uint64_t padded;           // bytes to write at dst (len rounded up to 16, zero-filled)
+};
+
+// POSD pack layout.
+constexpr uint32_t kPackHeader = 64;
+constexpr uint32_t kPackEntry = 32;
+constexpr uint32_t kPackAlign = 256;
+constexpr uint32_t kPackMagic = 0x44534F50u;  // "POSD"
+
+struct HashParams {
+  const DevBuf* bufs;
+  const uint2* chunk_map;    // [n_chunks] {buffer index, chunk index}
+  uint64_t n_items;          // chunks (hash mode) or work items (COPY mode)
+  uint64_t chunk_size;
+  uint32_t k_full;           // zeros_crc(chunk_size)
+  uint32_t pad0;
+  const uint32_t* tables;    // [7][1024]: Z^512, Z^4, Z^16, Z^32, Z^64, Z^128, Z^256
+  const uint32_t* xinv;      // [512]: x^(-8n) mod P
+  uint32_t* digest_cur;
+  const uint32_t* digest_prev;
+  uint8_t* flags;
+  uint32_t* bitmap;
+  int prev_valid;
+  int pad1;
+  // COPY mode
+  const uint4* work;         // {g, entry, dst_off lo, dst_off hi}
+  uint8_t* pack;             // pack base
+  uint64_t payload_off;      // payload offset within the pack
+};
+
+// Hash kernel geometry.
+constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
+constexpr int kStepBytes = 512;              // one warp step: 32 lanes x 16 B
+constexpr int kUnroll = 8;                   // warp steps per batch (4 KiB per warp)
+constexpr uint32_t kRepTableBytes = 131072;  // lane-replicated Z^512: 4 x 256 x 32 lanes x 4 B
+constexpr uint32_t kSmallTablesBytes = 6 * 4096;
+constexpr uint32_t kHashSmem = kRepTableBytes + kSmallTablesBytes;
+
+// ---------------------------------------------------------------------------
+// Load helpers.
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_stream(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Lane's 16 bytes of warp step `blk` of a region that starts at the 16-B
+// aligned address a0, keeping only bytes in [lead, end) (others read as 0).
+__device__ __forceinline__ uint4 load_masked(uint64_t a0, uint64_t blk, int lane, uint64_t lead,
+                                             uint64_t end) {
+  uint64_t off = blk * kStepBytes + (uint64_t)lane * 16;
+  if (off >= lead && off + 16 <= end) return ldg_stream((const void*)(a0 + off));
+  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+  if (off + 16 > lead && off < end) {
+    const uint8_t* p = (const uint8_t*)(a0 + off);
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      uint64_t o = off + b;
+      uint32_t byte = (o >= lead && o < end) ? (uint32_t)p[b] : 0u;
+      uint32_t sh = 8 * (b & 3);
+      if (b < 4) w0 |= byte << sh;
+      else if (b < 8) w1 |= byte << sh;
+      else if (b < 12) w2 |= byte << sh;
+      else w3 |= byte << sh;
+    }
+  }
+  return make_uint4(w0, w1, w2, w3);
+}
+
+// ---------------------------------------------------------------------------
+// CRC advance operators.
+//
+// Z^512 runs out of a lane-replicated table: entry e of slice k for lane l
+// lives at byte (k>>1)*65536 + e*256 + (k&1)*128 + l*4, so every lane hits its
+// own bank (conflict-free LDS) and one PRMT builds the address:
+// __byte_perm(x, lane*4, 0x55k4) = lane*4 + byte_k(x)*256.
+
+__device__ __forceinline__ uint32_t lds_u32(const uint8_t* smem, uint32_t off) {
+  return *reinterpret_cast<const uint32_t*>(smem + off);
+}
+
+__device__ __forceinline__ uint32_t adv512(const uint8_t* rep, uint32_t lsel, uint32_t x) {
+  uint32_t o0 = __byte_perm(x, lsel, 0x5504);
+  uint32_t o1 = __byte_perm(x, lsel, 0x5514);
+  uint32_t o2 = __byte_perm(x, lsel, 0x5524);
+  uint32_t o3 = __byte_perm(x, lsel, 0x5534);
+  return lds_u32(rep, o0) ^ lds_u32(rep, o1 + 128) ^ lds_u32(rep, o2 + 65536) ^
+         lds_u32(rep, o3 + 65536 + 128);
+}
+
+__device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
+  return t[x & 255] ^ t[256 + ((x >> 8) & 255)] ^ t[512 + ((x >> 16) & 255)] ^ t[768 + (x >> 24)];
+}
+
+// ---------------------------------------------------------------------------
+// One warp computes crc32 of [src, src+len) (len > 0).  Lane l owns 4
+// streams: word j of its 16 B in every 512-B warp step.  A stream's register
+// r advances r <- Z^512(r ^ w) from step to step.  In the last step the lane
+// merges its 4 streams with Z^4, the warp folds lanes with Z^16..Z^256
+// (shuffle tree), and the zero padding up to the step boundary is undone
+// with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
+// which leaves a register that starts at 0 unchanged.  COPY: every loaded
+// vector is also stored at dst (only when src is 16-B aligned).
+template <bool COPY>
+__device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_t* small,
+                                               const uint32_t* xinv, uint32_t lsel, int lane,
+                                               uint64_t src, uint64_t len, uint32_t k_len,
+                                               uint8_t* dst) {
+  const uint64_t a0 = src & ~15ull;
+  const uint64_t lead = src - a0;
+  const uint64_t end = lead + len;
+  const uint64_t nblk = (end + kStepBytes - 1) / kStepBytes;
+  const bool vec_copy = COPY && lead == 0;
+  const uint4* base = reinterpret_cast<const uint4*>(a0) + lane;
+  uint4* dbase = reinterpret_cast<uint4*>(dst) + lane;
+
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  uint64_t blk = 0;
+  if (lead != 0 && nblk > 1) {  // first step straddles the aligned base
+    uint4 v = load_masked(a0, 0, lane, lead, end);
+    c0 = adv512(rep, lsel, c0 ^ v.x);
+    c1 = adv512(rep, lsel, c1 ^ v.y);
+    c2 = adv512(rep, lsel, c2 ^ v.z);
+    c3 = adv512(rep, lsel, c3 ^ v.w);
+    blk = 1;
+  }
+  const uint64_t full_end = nblk - 1;  // steps [blk, full_end) are fully inside
+  // Software-pipelined batches of kUnroll steps (4 KiB per warp in flight,
+  // plus the next batch's loads issued before this batch's lookups).
+  if (blk + kUnroll <= full_end) {
+    uint4 cur[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) cur[u] = ldg_stream(base + (blk + u) * 32);
+    for (;;) {
+      const uint64_t nxt_blk = blk + kUnroll;
+      const bool more = nxt_blk + kUnroll <= full_end;
+      uint4 nxt[kUnroll];
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) nxt[u] = ldg_stream(base + (nxt_blk + u) * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (vec_copy) stg_stream(dbase + (blk + u) * 32, cur[u]);
+        c0 = adv512(rep, lsel, c0 ^ cur[u].x);
+        c1 = adv512(rep, lsel, c1 ^ cur[u].y);
+        c2 = adv512(rep, lsel, c2 ^ cur[u].z);
+        c3 = adv512(rep, lsel, c3 ^ cur[u].w);
+      }
+      blk = nxt_blk;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) cur[u] = nxt[u];
+    }
+  }
+  for (; blk < full_end; ++blk) {
+    uint4 v = ldg_stream(base + blk * 32);
+    if (vec_copy) stg_stream(dbase + blk * 32, v);
+    c0 = adv512(rep, lsel, c0 ^ v.x);
+    c1 = adv512(rep, lsel, c1 ^ v.y);
+    c2 = adv512(rep, lsel, c2 ^ v.z);
+    c3 = adv512(rep, lsel, c3 ^ v.w);
+  }
+  // Last (partial) step: bytes past `end` read as zero.
+  uint4 v = load_masked(a0, full_end, lane, lead, end);
+  if (vec_copy) {
+    uint64_t off = full_end * kStepBytes + (uint64_t)lane * 16;
+    if (off < end) stg_stream(dbase + full_end * 32, v);  // zero tail == POSD padding
+  }
+  const uint32_t* t4 = small;
+  uint32_t r = c0;
+  r = adv_small(t4, r ^ v.x) ^ c1;
+  r = adv_small(t4, r ^ v.y) ^ c2;
+  r = adv_small(t4, r ^ v.z) ^ c3;
+  r = adv_small(t4, r ^ v.w);  // lane register at step offset 16(l+1)
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    uint32_t t = adv_small(small + 1024 * (k + 1), r);  // Z^(16 << k)
+    uint32_t u = __shfl_up_sync(0xffffffffu, t, 1 << k);
+    const int m = (2 << k) - 1;
+    if ((lane & m) == m) r ^= u;
+  }
+  // lane 31: register at nblk*512; undo the zero padding.
+  uint32_t pad = (uint32_t)(nblk * kStepBytes - end);
+  uint32_t raw = pad ? multmodp(__ldg(xinv + pad), r) : r;
+  uint32_t crc = raw ^ k_len;
+  crc = __shfl_sync(0xffffffffu, crc, 31);
+  if (COPY && !vec_copy) {  // unaligned source: plain byte copy, zero padding
+    uint64_t padded = (len + 15) & ~15ull;
+    for (uint64_t i = lane; i < padded; i += 32)
+      dst[i] = i < len ? *reinterpret_cast<const uint8_t*>(src + i) : 0;
+  }
+  return crc;
+}
+
+__device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* tables) {
+  uint32_t* s32 = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < 32768; i += blockDim.x) {
+    int t2 = (i >> 5) & 1, e = (i >> 6) & 255, pair = i >> 14;
+    s32[i] = __ldg(tables + (pair * 2 + t2) * 256 + e);
+  }
+  for (int i = threadIdx.x; i < 6 * 1024; i += blockDim.x) s32[32768 + i] = __ldg(tables + 1024 + i);
+  __syncthreads();
+}
+
+// O2 (COPY=false): every chunk -> digest, dirty flag, bitmap bit.
+// STW delta-copy (COPY=true): every work item -> digest + pack entry + payload.
+template <bool COPY>
+__global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  load_hash_tables(smem, p.tables);
+  const uint8_t* rep = smem;
+  const uint32_t* small = reinterpret_cast<const uint32_t*>(smem + kRepTableBytes);
+  const int lane = threadIdx.x & 31;
+  const uint32_t lsel = (uint32_t)lane * 4;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kHashThreads / 32);
+  for (uint64_t it = (uint64_t)blockIdx.x * (kHashThreads / 32) + (threadIdx.x >> 5);
+       it < p.n_items; it += nwarps) {
+    uint64_t g, dst_off = 0;
+    uint32_t entry = 0;
+    if (COPY) {
+      uint4 w = p.work[it];
+      g = w.x;
+      entry = w.y;
+      dst_off = (uint64_t)w.z | ((uint64_t)w.w << 32);
+    } else {
+      g = it;
+    }
+    const uint2 cm = p.chunk_map[g];
+    const DevBuf& b = p.bufs[cm.x];
+    const uint64_t start = (uint64_t)cm.y * p.chunk_size;
+    const bool last = cm.y + 1 == b.nchunks;
+    const uint64_t len = last ? b.size - start : p.chunk_size;
+    const uint32_t k_len = last ? b.k_tail : p.k_full;
+    uint8_t* dst = COPY ? p.pack + p.payload_off + dst_off : nullptr;
+    uint32_t crc = warp_crc32<COPY>(rep, small, p.xinv, lsel, lane, b.ptr + start, len, k_len, dst);
+    if (lane == 31) {
+      p.digest_cur[g] = crc;
+      if (COPY) {
+        uint4* e = reinterpret_cast<uint4*>(p.pack + kPackHeader + (uint64_t)entry * kPackEntry);
+        e[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)dst_off,
+                          (uint32_t)(dst_off >> 32));
+        e[1] = make_uint4(cm.y, (uint32_t)len, crc, 0u);
+      } else if (p.flags) {
+        const bool dirty = !p.prev_valid || p.digest_prev[g] != crc;
+        p.flags[g] = dirty;
+        if (dirty) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// O1: whole-buffer CRC = crc32_combine fold of the chunk digests, then the
+// scan_dedup verdict (cr.hpp:419-421) and the finalize_image gate
+// (!dirty_set_, cr.hpp:720).  One thread per buffer; Z^chunk_size from a table.
+__global__ void k_buffer_crc(const DevBuf* bufs, uint32_t nbufs, const uint32_t* digests,
+                             const uint32_t* tcs, const uint8_t* dag_dirty, int dedup,
+                             uint32_t* crc_out, uint8_t* verdict_out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbufs) return;
+  const DevBuf b = bufs[i];
+  const uint32_t* d = digests + b.chunk_base;
+  uint32_t crc = d[0];
+  for (uint32_t c = 1; c < b.nchunks; ++c) {
+    bool last = c + 1 == b.nchunks;
+    uint32_t adv = last ? multmodp(b.x8_tail, crc) : adv_small(tcs, crc);
+    crc = adv ^ d[c];
+  }
+  crc_out[i] = crc;
+  bool ok = dedup && (b.flags & kBufHasUpstream) && crc == b.upstream_crc &&
+            (b.flags & kBufHostUntouched) && !dag_dirty[i];
+  verdict_out[i] = ok;
+}
+
+// ---------------------------------------------------------------------------
+// Pack layout: one CTA scans the eligible-chunk flags in global chunk order
+// (= ascending (handle, chunk), since buffers are registered by ascending
+// handle), writes the POSD header + entries and one CopyItem per entry.
+// eligible = flag && !verdict_ok(buffer) && !(exclude_dag && dag_dirty(buffer)).
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads) k_pack_scan(
+    const DevBuf* bufs, const uint2* chunk_map, uint64_t n_chunks, uint64_t chunk_size,
+    const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty, int exclude_dag,
+    const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* pack,
+    uint64_t pack_capacity, CopyItem* items, uint64_t* result /* [n, total, overflow] */) {
+  __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
+  const int t = threadIdx.x;
+  const uint64_t per = (n_chunks + kScanThreads - 1) / kScanThreads;
+  const uint64_t lo = (uint64_t)t * per < n_chunks ? (uint64_t)t * per : n_chunks;
+  const uint64_t hi = lo + per < n_chunks ? lo + per : n_chunks;
+  auto chunk_len = [&](uint2 cm) -> uint64_t {
+    const DevBuf& b = bufs[cm.x];
+    uint64_t start = (uint64_t)cm.y * chunk_size;
+    return cm.y + 1 == b.nchunks ? b.size - start : chunk_size;
+  };
+  auto eligible = [&](uint64_t g, uint2 cm) -> bool {
+    return flags[g] && !verdict[cm.x] && !(exclude_dag && dag_dirty[cm.x]);
+  };
+  uint64_t n = 0, bytes = 0;
+  for (uint64_t g = lo; g < hi; ++g) {
+    uint2 cm = chunk_map[g];
+    if (eligible(g, cm)) {
+      ++n;
+      bytes += (chunk_len(cm) + 15) & ~15ull;
+    }
+  }
+  s_n[t] = n;
+  s_b[t] = bytes;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {  // inclusive Hillis-Steele
+    uint64_t an = t >= off ? s_n[t - off] : 0, ab = t >= off ? s_b[t - off] : 0;
+    __syncthreads();
+    s_n[t] += an;
+    s_b[t] += ab;
+    __syncthreads();
+  }
+  const uint64_t N = s_n[kScanThreads - 1], B = s_b[kScanThreads - 1];
+  const uint64_t payload_off =
+      (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
+  const uint64_t total = payload_off + B;
+  const bool overflow = total > pack_capacity;
+  if (t == 0) {
+    result[0] = N;
+    result[1] = total;
+    result[2] = overflow;
+  }
+  if (overflow) return;
+  if (t == 0) {
+    uint32_t* h = reinterpret_cast<uint32_t*>(pack);
+    h[0] = kPackMagic;
+    h[1] = 1;
+    *reinterpret_cast<uint64_t*>(pack + 8) = chunk_size;
+    h[4] = (uint32_t)N;
+    h[5] = pack_flags;
+    *reinterpret_cast<uint64_t*>(pack + 24) = payload_off;
+    *reinterpret_cast<uint64_t*>(pack + 32) = B;
+    *reinterpret_cast<uint64_t*>(pack + 40) = epoch;
+    *reinterpret_cast<uint64_t*>(pack + 48) = total;
+    *reinterpret_cast<uint64_t*>(pack + 56) = 0;
+  }
+  for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
+  uint64_t e = s_n[t] - n, off = s_b[t] - bytes;
+  for (uint64_t g = lo; g < hi; ++g) {
+    uint2 cm = chunk_map[g];
+    if (!eligible(g, cm)) continue;
+    const DevBuf& b = bufs[cm.x];
+    uint64_t len = chunk_len(cm);
+    uint4* ent = reinterpret_cast<uint4*>(pack + kPackHeader + e * kPackEntry);
+    ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)off,
+                        (uint32_t)(off >> 32));
+    ent[1] = make_uint4(cm.y, (uint32_t)len, digests[g], 0u);
+    CopyItem ci;
+    ci.src = b.ptr + (uint64_t)cm.y * chunk_size;
+    ci.dst = (uint64_t)pack + payload_off + off;
+    ci.len = len;
+    ci.padded = (len + 15) & ~15ull;
+    items[e] = ci;
+    ++e;
+    off += ci.padded;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bulk copy engine: each CTA streams its items (grid-stride) through a ring of
+// kCopyStages smem slots with cp.async.bulk (TMA bulk) G->S loads completing
+// on an mbarrier and S->G bulk stores tracked by bulk groups; one elected
+// thread drives the pipeline.  Requires 16-B aligned src/dst (checked by the
+// host; otherwise k_copy_simt runs).  The <16-B remainder of an item and its
+// zero padding go through one vector store.
+constexpr int kCopyStages = 4;
+constexpr uint32_t kCopyPiece = 16384;
+constexpr uint32_t kCopySmem = kCopyStages * kCopyPiece + 64;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+struct PieceIter {  // walks (item, offset) pieces of this CTA's grid-stride items
+  uint64_t item, off;
+};
+
+__global__ void __launch_bounds__(32) k_copy_bulk(const CopyItem* items, const uint64_t* n_items_dev,
+                                                  uint64_t n_items_host) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCopyStages * kCopyPiece);
+  const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kCopyStages; ++s) mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  // Piece = up to kCopyPiece bytes of the 16-B-aligned body of an item.
+  auto body = [&](uint64_t i) { return items[i].len & ~15ull; };
+  auto advance = [&](PieceIter& it) {
+    it.off += kCopyPiece;
+    while (it.item < n && it.off >= body(it.item)) {
+      it.item += gridDim.x;
+      it.off = 0;
+    }
+  };
+  auto first = [&]() {
+    PieceIter it{blockIdx.x, 0};
+    while (it.item < n && body(it.item) == 0) it.item += gridDim.x;
+    return it;
+  };
+  uint64_t slot_dst[kCopyStages];
+  uint32_t slot_bytes[kCopyStages];
+  uint32_t phase = 0;  // bit s = parity of slot s
+  PieceIter ld = first();
+  int issued = 0;
+  // Prologue: fill the ring.
+  for (; issued < kCopyStages && ld.item < n; ++issued) {
+    const CopyItem& c = items[ld.item];
+    uint32_t bytes = (uint32_t)umin64((uint64_t)kCopyPiece, body(ld.item) - ld.off);
+    slot_dst[issued] = c.dst + ld.off;
+    slot_bytes[issued] = bytes;
+    mbar_expect_tx(bars + issued, bytes);
+    bulk_g2s(smem + issued * kCopyPiece, (const void*)(c.src + ld.off), bytes, bars + issued);
+    advance(ld);
+  }
+  int slot = 0;
+  for (int done = 0; done < issued; ++done) {
+    mbar_wait(bars + slot, (phase >> slot) & 1);
+    phase ^= 1u << slot;
+    bulk_s2g((void*)slot_dst[slot], smem + slot * kCopyPiece, slot_bytes[slot]);
+    bulk_commit();
+    if (ld.item < n) {
+      // Reuse this slot once its store has read the smem.
+      bulk_wait_read<0>();
+      const CopyItem& c = items[ld.item];
+      uint32_t bytes = (uint32_t)umin64((uint64_t)kCopyPiece, body(ld.item) - ld.off);
+      slot_dst[slot] = c.dst + ld.off;
+      slot_bytes[slot] = bytes;
+      mbar_expect_tx(bars + slot, bytes);
+      bulk_g2s(smem + slot * kCopyPiece, (const void*)(c.src + ld.off), bytes, bars + slot);
+      advance(ld);
+      ++issued;
+    }
+    slot = (slot + 1) % kCopyStages;
+  }
+  bulk_wait_all();
+  // Remainders (< 16 B) + zero padding of this CTA's items, byte-exact.
+  for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const CopyItem c = items[i];
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
+    uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
+    for (uint64_t k = c.len & ~15ull; k < c.padded; ++k) d[k] = k < c.len ? s[k] : 0;
+  }
+}
+
+// Fallback for items whose src or dst is not 16-B aligned: one warp per item,
+// byte copy + zero padding to `padded`.
+__global__ void k_copy_simt(const CopyItem* items, const uint64_t* n_items_dev, uint64_t n_items_host) {
+  const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+    const CopyItem c = items[i];
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
+    uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
+    for (uint64_t k = lane; k < c.padded; k += 32) d[k] = k < c.len ? s[k] : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Restore: POSD entries -> copy items (pack payload -> buffer chunk).
+// Validation mirrors write_content's range check (buffer.hpp:80) and the
+// pack's own section checks; errors set bits in *err (1 corrupt, 2 locator).
+__global__ void k_pack_items(const uint8_t* pack, uint64_t pack_bytes, const DevBuf* bufs,
+                             uint32_t nbufs, uint64_t chunk_size, CopyItem* items, uint32_t* err) {
+  const uint32_t n = *reinterpret_cast<const uint32_t*>(pack + 16);
+  const uint64_t payload_off = *reinterpret_cast<const uint64_t*>(pack + 24);
+  const uint64_t payload = *reinterpret_cast<const uint64_t*>(pack + 32);
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t* ent = pack + kPackHeader + e * kPackEntry;
+    uint64_t h = *reinterpret_cast<const uint64_t*>(ent);
+    uint64_t off = *reinterpret_cast<const uint64_t*>(ent + 8);
+    uint32_t c = *reinterpret_cast<const uint32_t*>(ent + 16);
+    uint32_t len = *reinterpret_cast<const uint32_t*>(ent + 20);
+    // binary search: buffers are registered by ascending handle
+    uint32_t lo = 0, hi = nbufs;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) / 2;
+      if (bufs[mid].handle < h) lo = mid + 1;
+      else hi = mid;
+    }
+    CopyItem ci{0, 0, 0, 0};
+    if (lo >= nbufs || bufs[lo].handle != h) {
+      atomicOr(err, 2u);
+    } else if ((uint64_t)c * chunk_size + len > bufs[lo].size || off + len > payload) {
+      atomicOr(err, 2u);
+    } else {
+      ci.src = (uint64_t)pack + payload_off + off;
+      ci.dst = bufs[lo].ptr + (uint64_t)c * chunk_size;
+      ci.len = len;
+      ci.padded = len;  // never write past the chunk on restore
+    }
+    items[e] = ci;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fill_bytes(seed) into device memory: word k (8 bytes, little endian) is the
+// (k+1)-th SplitMix64 output, state_k = seed + (k+1)*gamma (rng.hpp:15-20,
+// 43-54): each thread produces its words independently.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t k) {
+  uint64_t z = seed + (k + 1) * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+struct FillRange {
+  uint64_t ptr, n, seed;
+};
+
+constexpr int kFillMaxRanges = 256;  // by-value kernel parameter (6 KiB)
+struct FillBatch {
+  uint32_t count;
+  uint32_t pad;
+  FillRange r[kFillMaxRanges];
+};
+
+__global__ void k_fill(const __grid_constant__ FillBatch b) {
+  for (uint32_t ri = blockIdx.y; ri < b.count; ri += gridDim.y) {
+    const FillRange f = b.r[ri];
+    const uint64_t words = (f.n + 7) / 8;
+    const bool aligned = (f.ptr & 15) == 0;
+    for (uint64_t p = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 2; p < words;
+         p += (uint64_t)gridDim.x * blockDim.x * 2) {
+      uint64_t w0 = splitmix_at(f.seed, p), w1 = splitmix_at(f.seed, p + 1);
+      uint64_t byte0 = p * 8;
+      if (aligned && byte0 + 16 <= f.n) {
+        *reinterpret_cast<uint4*>(f.ptr + byte0) =
+            make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+      } else {
+        uint8_t* d = reinterpret_cast<uint8_t*>(f.ptr);
+        for (int k = 0; k < 16 && byte0 + k < f.n; ++k)
+          d[byte0 + k] = (uint8_t)((k < 8 ? w0 : w1) >> (8 * (k & 7)));
+      }
+    }
+  }
+}
+
+}  // namespace posdump

@@ -1,0 +1,1042 @@
+// posdump.cu -- host side of libposdump.so: the C ABI of include/posdump.h.
+//
+// Owns device memory for the buffer table, the per-chunk digest tables
+// (double-buffered by epoch), the dirty flags/bitmap, the O3 cache and the
+// launch plumbing.  There is no CPU path: every operation on buffer bytes is
+// a kernel from kernels.cuh, and a missing device is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/posdump.h"
+#include "crc_math.h"
+#include "kernels.cuh"
+#include "image_writer.h"
+
+using namespace posdump;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  throw Fail{code};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(POS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return POS_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return POS_E_OUT_OF_DEVICE_MEMORY;
+  }
+}
+
+template <typename T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t c = std::max<size_t>(count, 1);
+    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    if (e != cudaSuccess)
+      fail(POS_E_OUT_OF_DEVICE_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    n = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+struct PinnedArray {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    size_t c = std::max<size_t>(count, 1);
+    ck(cudaHostAlloc((void**)&p, c * sizeof(T), cudaHostAllocDefault), "cudaHostAlloc");
+    n = c;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Tables shared by every launch on a device: Z^512 (replicated in smem by the
+// kernel), Z^4, Z^16..Z^256, and x^(-8n) for n < 512.
+struct CrcTables {
+  DevArray<uint32_t> tables;  // 7 x 1024
+  DevArray<uint32_t> xinv;    // 512
+  int sm_count = 0;
+  void init(int device) {
+    std::vector<uint32_t> h(7 * 1024);
+    build_advance_table(512, h.data());
+    build_advance_table(4, h.data() + 1024);
+    for (int k = 0; k < 5; ++k) build_advance_table(16u << k, h.data() + 1024 * (2 + k));
+    std::vector<uint32_t> xi(512);
+    for (int n = 0; n < 512; ++n) xi[n] = xinv8nmodp(n);
+    tables.ensure(h.size());
+    xinv.ensure(xi.size());
+    ck(cudaMemcpy(tables.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "upload tables");
+    ck(cudaMemcpy(xinv.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice), "upload xinv");
+    ck(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
+    ck(cudaFuncSetAttribute(k_hash_chunks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kHashSmem),
+       "smem attr");
+    ck(cudaFuncSetAttribute(k_hash_chunks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kHashSmem),
+       "smem attr");
+    ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
+       "smem attr");
+  }
+};
+
+void require_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    fail(POS_E_NO_DEVICE, "no CUDA device: the dump path has no CPU fallback");
+  if (device < 0 || device >= n) fail(POS_E_INVALID_ARGUMENT, "bad device ordinal");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+}
+
+enum TimerId { kTimHash = 0, kTimCombine, kTimScan, kTimCopy, kTimDelta, kTimScatter, kTimCount };
+const char* kTimerNames[kTimCount] = {"hash", "combine", "scan", "copy", "delta", "scatter"};
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool used = false;
+};
+
+}  // namespace
+
+struct pos_ctx {
+  pos_config cfg{};
+  CrcTables crc;
+  // Buffer set (ascending handle).
+  std::vector<pos_buffer_desc> bufs;
+  std::vector<uint64_t> chunk_base;  // per buffer
+  std::vector<DevBuf> hbufs;
+  std::map<uint64_t, uint32_t> index_of;
+  uint64_t n_chunks = 0;
+  DevArray<DevBuf> d_bufs;
+  DevArray<uint2> d_chunk_map;
+  DevArray<uint32_t> d_digest[2];
+  int cur = 0;
+  bool prev_valid = false;
+  uint64_t epoch = 0;
+  DevArray<uint8_t> d_flags;
+  DevArray<uint32_t> d_bitmap;
+  DevArray<uint32_t> d_buf_crc;
+  DevArray<uint8_t> d_verdict;
+  DevArray<uint8_t> d_dag_dirty;
+  DevArray<uint32_t> d_tcs;  // Z^chunk_size
+  std::set<uint64_t> dirty_set;
+  bool dag_uploaded = false;
+  // O3 cache
+  DevArray<uint8_t> cache;
+  uint64_t cache_cap = 0;
+  uint64_t precopy_bytes = 0;
+  DevArray<CopyItem> d_items;
+  DevArray<uint64_t> d_scan;     // [n, total, overflow]
+  DevArray<uint4> d_work;
+  DevArray<uint32_t> d_err;
+  PinnedArray<uint64_t> h_scan;
+  PinnedArray<uint8_t> h_stage;  // delta header + work list upload
+  PinnedArray<uint8_t> h_dag;
+  cudaEvent_t stage_free = nullptr;
+  // timing
+  std::vector<cudaEvent_t> events;
+  Timer timers[kTimCount];
+  uint64_t launches = 0;
+
+  void timer_begin(TimerId t, cudaStream_t s) { ck(cudaEventRecord(timers[t].a, s), "event"); }
+  void timer_end(TimerId t, cudaStream_t s) {
+    ck(cudaEventRecord(timers[t].b, s), "event");
+    timers[t].used = true;
+  }
+  int hash_grid(uint64_t items) const {
+    uint64_t warps = (items + 0) / 1;
+    uint64_t blocks = (warps + (kHashThreads / 32) - 1) / (kHashThreads / 32);
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)crc.sm_count));
+  }
+};
+
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(POS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+void upload_dag_flags(pos_ctx* c, cudaStream_t s) {
+  if (c->dag_uploaded) return;
+  uint32_t nb = (uint32_t)c->bufs.size();
+  c->h_dag.ensure(nb);
+  if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
+  for (uint32_t i = 0; i < nb; ++i) c->h_dag.p[i] = c->dirty_set.count(c->bufs[i].handle) ? 1 : 0;
+  ck(cudaMemcpyAsync(c->d_dag_dirty.p, c->h_dag.p, nb, cudaMemcpyHostToDevice, s), "dag upload");
+  ck(cudaEventRecord(c->stage_free, s), "event");
+  c->dag_uploaded = true;
+}
+
+void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
+                 bool aligned, cudaStream_t s) {
+  int sms = c->crc.sm_count;
+  if (aligned) {
+    // 3 CTAs/SM fit in smem (64 KiB ring each); one elected thread per CTA.
+    int grid = sms * 3;
+    if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host));
+    k_copy_bulk<<<grid, 32, kCopySmem, s>>>(items, n_dev, n_host);
+  } else {
+    k_copy_simt<<<sms * 4, 256, 0, s>>>(items, n_dev, n_host);
+  }
+  check_launch("copy");
+  ++c->launches;
+}
+
+// Global per-device CRC engine for pos_crc32 (no context).
+std::mutex g_engine_mu;
+std::map<int, CrcTables*> g_engines;
+
+CrcTables& engine_for_current_device() {
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_engine_mu);
+  auto it = g_engines.find(dev);
+  if (it != g_engines.end()) return *it->second;
+  auto* e = new CrcTables();
+  e->init(dev);
+  g_engines[dev] = e;
+  return *e;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pos_strerror(int code) {
+  static const char* names[] = {"OK",           "PastTime",          "Livelock",
+                                "OutOfDeviceMemory", "InvalidLocator", "UseAfterFree",
+                                "FreedBuffer",  "BadState",          "PendingKernels",
+                                "UnknownApi",   "InvalidArgument",   "CorruptDag",
+                                "CorruptImage", "InvariantViolation", "StagingExhausted",
+                                "OracleMismatch"};
+  if (code >= 0 && code <= 15) return names[code];
+  if (code == POS_E_CUDA) return "CudaError";
+  if (code == POS_E_NO_DEVICE) return "NoDevice";
+  return "Unknown";
+}
+
+const char* pos_last_error(void) { return g_last_error.c_str(); }
+int pos_abi_version(void) { return POSDUMP_ABI_VERSION; }
+
+int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
+  return guarded([&] {
+    if (!cfg || !out) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (cfg->chunk_size == 0 || cfg->page_size == 0)
+      fail(POS_E_INVALID_ARGUMENT, "chunk_size and page_size must be positive");
+    if (cfg->chunk_size > (1ull << 31)) fail(POS_E_INVALID_ARGUMENT, "chunk_size too large");
+    require_device(cfg->device);
+    auto* c = new pos_ctx();
+    try {
+      c->cfg = *cfg;
+      c->crc.init(cfg->device);
+      std::vector<uint32_t> tcs(1024);
+      build_advance_table(cfg->chunk_size, tcs.data());
+      c->d_tcs.ensure(1024);
+      ck(cudaMemcpy(c->d_tcs.p, tcs.data(), 4096, cudaMemcpyHostToDevice), "upload tcs");
+      uint64_t cap = cfg->cache_capacity;
+      if (cap == 0) {
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        double frac = cfg->staging_fraction > 0 ? cfg->staging_fraction : 1.0 / 16.0;
+        cap = (uint64_t)((double)total_b * frac);  // staging_capacity() (config.hpp:43-45)
+      }
+      c->cache_cap = round_up(cap, 256);
+      c->cache.ensure(c->cache_cap);
+      c->d_scan.ensure(4);
+      c->d_err.ensure(1);
+      c->h_scan.ensure(4);
+      ck(cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming), "event");
+      for (auto& t : c->timers) {
+        ck(cudaEventCreate(&t.a), "event");
+        ck(cudaEventCreate(&t.b), "event");
+      }
+      c->events.resize(64);
+      for (auto& e : c->events) ck(cudaEventCreate(&e), "event");
+    } catch (...) {
+      pos_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int pos_ctx_destroy(pos_ctx* c) {
+  if (!c) return POS_OK;
+  cudaDeviceSynchronize();
+  c->crc.tables.release();
+  c->crc.xinv.release();
+  c->d_bufs.release();
+  c->d_chunk_map.release();
+  c->d_digest[0].release();
+  c->d_digest[1].release();
+  c->d_flags.release();
+  c->d_bitmap.release();
+  c->d_buf_crc.release();
+  c->d_verdict.release();
+  c->d_dag_dirty.release();
+  c->d_tcs.release();
+  c->cache.release();
+  c->d_items.release();
+  c->d_scan.release();
+  c->d_work.release();
+  c->d_err.release();
+  c->h_scan.release();
+  c->h_stage.release();
+  c->h_dag.release();
+  if (c->stage_free) cudaEventDestroy(c->stage_free);
+  for (auto& t : c->timers) {
+    if (t.a) cudaEventDestroy(t.a);
+    if (t.b) cudaEventDestroy(t.b);
+  }
+  for (auto e : c->events)
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return POS_OK;
+}
+
+int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
+  return guarded([&] {
+    if (!c || (!bufs && n)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    std::vector<pos_buffer_desc> v(bufs, bufs + n);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (v[i].size == 0) fail(POS_E_INVALID_ARGUMENT, "buffer of size 0");
+      if (i && v[i].handle <= v[i - 1].handle)
+        fail(POS_E_INVALID_ARGUMENT, "buffers must be registered by strictly ascending handle");
+    }
+    const uint64_t cs = c->cfg.chunk_size;
+    c->bufs = v;
+    c->hbufs.assign(n, DevBuf{});
+    c->chunk_base.assign(n, 0);
+    c->index_of.clear();
+    uint64_t g = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      const auto& d = v[i];
+      DevBuf& b = c->hbufs[i];
+      b.ptr = d.dev_ptr;
+      b.size = d.size;
+      b.handle = d.handle;
+      b.chunk_base = g;
+      uint64_t nc = (d.size + cs - 1) / cs;
+      if (nc > 0xFFFFFFFFull) fail(POS_E_INVALID_ARGUMENT, "too many chunks in one buffer");
+      b.nchunks = (uint32_t)nc;
+      uint64_t tail = d.size - (nc - 1) * cs;
+      b.k_tail = zeros_crc(tail);
+      b.x8_tail = x8nmodp(tail);
+      b.flags = (d.has_upstream ? kBufHasUpstream : 0) | (d.host_untouched ? kBufHostUntouched : 0) |
+                (d.written_since_ckpt ? kBufWrittenSinceCkpt : 0);
+      b.upstream_crc = d.upstream_crc;
+      c->chunk_base[i] = g;
+      c->index_of[d.handle] = i;
+      g += nc;
+    }
+    if (g > 0xFFFFFFFFull) fail(POS_E_INVALID_ARGUMENT, "more than 2^32 chunks");
+    c->n_chunks = g;
+    std::vector<uint2> cmap(g);
+    for (uint32_t i = 0; i < n; ++i)
+      for (uint32_t k = 0; k < c->hbufs[i].nchunks; ++k) cmap[c->chunk_base[i] + k] = make_uint2(i, k);
+    c->d_bufs.ensure(n);
+    c->d_chunk_map.ensure(g);
+    c->d_digest[0].ensure(g);
+    c->d_digest[1].ensure(g);
+    c->d_flags.ensure(g);
+    c->d_bitmap.ensure((g + 31) / 32);
+    c->d_buf_crc.ensure(n);
+    c->d_verdict.ensure(n);
+    c->d_dag_dirty.ensure(n);
+    c->d_items.ensure(g);
+    c->d_work.ensure(g);
+    if (n) ck(cudaMemcpy(c->d_bufs.p, c->hbufs.data(), n * sizeof(DevBuf), cudaMemcpyHostToDevice), "bufs");
+    if (g) ck(cudaMemcpy(c->d_chunk_map.p, cmap.data(), g * sizeof(uint2), cudaMemcpyHostToDevice), "cmap");
+    ck(cudaMemset(c->d_verdict.p, 0, std::max<uint32_t>(n, 1)), "memset");
+    ck(cudaMemset(c->d_dag_dirty.p, 0, std::max<uint32_t>(n, 1)), "memset");
+    c->cur = 0;
+    c->prev_valid = false;
+    c->epoch = 0;
+    c->dirty_set.clear();
+    c->dag_uploaded = false;
+    c->precopy_bytes = 0;
+  });
+}
+
+int pos_update_buffer(pos_ctx* c, const pos_buffer_desc* d) {
+  return guarded([&] {
+    if (!c || !d) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    auto it = c->index_of.find(d->handle);
+    if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "unknown handle");
+    uint32_t i = it->second;
+    if (d->dev_ptr != c->bufs[i].dev_ptr || d->size != c->bufs[i].size)
+      fail(POS_E_INVALID_ARGUMENT, "update may not move or resize a buffer");
+    c->bufs[i] = *d;
+    DevBuf& b = c->hbufs[i];
+    b.flags = (d->has_upstream ? kBufHasUpstream : 0) | (d->host_untouched ? kBufHostUntouched : 0) |
+              (d->written_since_ckpt ? kBufWrittenSinceCkpt : 0);
+    b.upstream_crc = d->upstream_crc;
+    ck(cudaMemcpy(c->d_bufs.p + i, &b, sizeof(DevBuf), cudaMemcpyHostToDevice), "update buf");
+  });
+}
+
+int pos_num_chunks(pos_ctx* c, uint64_t* out) {
+  return guarded([&] {
+    if (!c || !out) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    *out = c->n_chunks;
+  });
+}
+
+int pos_hash_chunks(pos_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    if (c->n_chunks == 0) return;
+    ck(cudaMemsetAsync(c->d_bitmap.p, 0, ((c->n_chunks + 31) / 32) * 4, s), "memset bitmap");
+    HashParams p{};
+    p.bufs = c->d_bufs.p;
+    p.chunk_map = c->d_chunk_map.p;
+    p.n_items = c->n_chunks;
+    p.chunk_size = c->cfg.chunk_size;
+    p.k_full = zeros_crc(c->cfg.chunk_size);
+    p.tables = c->crc.tables.p;
+    p.xinv = c->crc.xinv.p;
+    p.digest_cur = c->d_digest[c->cur].p;
+    p.digest_prev = c->d_digest[c->cur ^ 1].p;
+    p.flags = c->d_flags.p;
+    p.bitmap = c->d_bitmap.p;
+    p.prev_valid = c->prev_valid ? 1 : 0;
+    int grid = c->hash_grid(c->n_chunks);
+    c->timer_begin(kTimHash, s);
+    k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);
+    check_launch("k_hash_chunks");
+    c->timer_end(kTimHash, s);
+    ++c->launches;
+  });
+}
+
+int pos_commit_epoch(pos_ctx* c) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    c->cur ^= 1;
+    c->prev_valid = true;
+    ++c->epoch;
+    c->dirty_set.clear();
+    c->dag_uploaded = false;
+    c->precopy_bytes = 0;
+  });
+}
+
+static int read_back(pos_ctx* c, void* host, const void* dev, uint64_t bytes, void* stream) {
+  return guarded([&] {
+    if (!c || (!host && bytes)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!bytes) return;
+    ck(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, S(stream)), "read back");
+    ck(cudaStreamSynchronize(S(stream)), "sync");
+  });
+}
+
+int pos_read_digests(pos_ctx* c, uint32_t* host, uint64_t n, void* stream) {
+  if (c && n > c->n_chunks) return POS_E_INVALID_ARGUMENT;
+  return read_back(c, host, c ? c->d_digest[c->cur].p : nullptr, n * 4, stream);
+}
+int pos_read_flags(pos_ctx* c, uint8_t* host, uint64_t n, void* stream) {
+  if (c && n > c->n_chunks) return POS_E_INVALID_ARGUMENT;
+  return read_back(c, host, c ? c->d_flags.p : nullptr, n, stream);
+}
+int pos_read_bitmap(pos_ctx* c, uint32_t* host, uint64_t nwords, void* stream) {
+  if (c && nwords > (c->n_chunks + 31) / 32) return POS_E_INVALID_ARGUMENT;
+  return read_back(c, host, c ? c->d_bitmap.p : nullptr, nwords * 4, stream);
+}
+
+int pos_buffer_crc(pos_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    uint32_t nb = (uint32_t)c->bufs.size();
+    if (!nb) return;
+    upload_dag_flags(c, s);
+    c->timer_begin(kTimCombine, s);
+    k_buffer_crc<<<(nb + 127) / 128, 128, 0, s>>>(c->d_bufs.p, nb, c->d_digest[c->cur].p, c->d_tcs.p,
+                                                 c->d_dag_dirty.p, c->cfg.dedup, c->d_buf_crc.p,
+                                                 c->d_verdict.p);
+    check_launch("k_buffer_crc");
+    c->timer_end(kTimCombine, s);
+    ++c->launches;
+  });
+}
+
+int pos_read_buffer_crcs(pos_ctx* c, uint32_t* crcs, uint8_t* verdicts, uint32_t n, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (n > c->bufs.size()) fail(POS_E_INVALID_ARGUMENT, "n exceeds buffer count");
+    if (!n) return;
+    if (crcs) ck(cudaMemcpyAsync(crcs, c->d_buf_crc.p, n * 4, cudaMemcpyDeviceToHost, S(stream)), "rb");
+    if (verdicts)
+      ck(cudaMemcpyAsync(verdicts, c->d_verdict.p, n, cudaMemcpyDeviceToHost, S(stream)), "rb");
+    ck(cudaStreamSynchronize(S(stream)), "sync");
+  });
+}
+
+int pos_record_dirty(pos_ctx* c, const uint64_t* handles, uint32_t n) {
+  return guarded([&] {
+    if (!c || (!handles && n)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!c->index_of.count(handles[i])) continue;  // not in the snapshot (cr.hpp:904)
+      if (c->dirty_set.insert(handles[i]).second) c->dag_uploaded = false;
+    }
+  });
+}
+
+int pos_clear_dirty(pos_ctx* c) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    c->dirty_set.clear();
+    c->dag_uploaded = false;
+  });
+}
+
+int pos_compact(pos_ctx* c, int exclude_dag_dirty, void* stream, uint64_t* pack_bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    upload_dag_flags(c, s);
+    c->timer_begin(kTimScan, s);
+    k_pack_scan<<<1, kScanThreads, 0, s>>>(
+        c->d_bufs.p, c->d_chunk_map.p, c->n_chunks, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
+        c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
+        c->cache_cap, c->d_items.p, c->d_scan.p);
+    check_launch("k_pack_scan");
+    c->timer_end(kTimScan, s);
+    ++c->launches;
+    ck(cudaMemcpyAsync(c->h_scan.p, c->d_scan.p, 3 * 8, cudaMemcpyDeviceToHost, s), "scan result");
+    ck(cudaStreamSynchronize(s), "sync");
+    uint64_t n = c->h_scan.p[0], total = c->h_scan.p[1];
+    if (c->h_scan.p[2]) {
+      c->precopy_bytes = 0;
+      fail(POS_E_STAGING_EXHAUSTED, "pack of " + std::to_string(total) + " B exceeds cache of " +
+                                        std::to_string(c->cache_cap) + " B");
+    }
+    bool aligned = c->cfg.chunk_size % 16 == 0;
+    for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
+    if (n) {
+      c->timer_begin(kTimCopy, s);
+      launch_copy(c, c->d_items.p, nullptr, n, aligned, s);
+      c->timer_end(kTimCopy, s);
+    }
+    c->precopy_bytes = total;
+    if (pack_bytes) *pack_bytes = total;
+  });
+}
+
+int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    const uint64_t cs = c->cfg.chunk_size;
+    // at_final_stop: every buffer of dirty_set_ in the snapshot, ascending handle.
+    std::vector<uint4> work;
+    uint64_t payload = 0;
+    uint32_t entry = 0;
+    for (uint64_t h : c->dirty_set) {
+      uint32_t i = c->index_of.at(h);
+      const DevBuf& b = c->hbufs[i];
+      for (uint32_t k = 0; k < b.nchunks; ++k) {
+        uint64_t len = k + 1 == b.nchunks ? b.size - (uint64_t)k * cs : cs;
+        uint64_t g = c->chunk_base[i] + k;
+        work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
+        payload += round_up(len, 16);
+      }
+    }
+    const uint64_t n = work.size();
+    const uint64_t payload_off = round_up(kPackHeader + kPackEntry * n, kPackAlign);
+    const uint64_t total = payload_off + payload;
+    const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
+    if (offset + total > c->cache_cap)
+      fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
+    // Stage header (+ zero gap up to the payload) and the work list.
+    const uint64_t hdr_bytes = payload_off;
+    const uint64_t work_bytes = n * sizeof(uint4);
+    if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
+    c->h_stage.ensure(hdr_bytes + work_bytes);
+    uint8_t* st = c->h_stage.p;
+    std::memset(st, 0, hdr_bytes);
+    uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)n, flags = 1;
+    std::memcpy(st + 0, &magic, 4);
+    std::memcpy(st + 4, &ver, 4);
+    std::memcpy(st + 8, &cs, 8);
+    std::memcpy(st + 16, &nn, 4);
+    std::memcpy(st + 20, &flags, 4);
+    std::memcpy(st + 24, &payload_off, 8);
+    std::memcpy(st + 32, &payload, 8);
+    std::memcpy(st + 40, &c->epoch, 8);
+    std::memcpy(st + 48, &total, 8);
+    if (n) std::memcpy(st + hdr_bytes, work.data(), work_bytes);
+    uint8_t* pack = c->cache.p + offset;
+    // Only the header and the entry gap go up; the kernel writes the entries.
+    ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
+    if (hdr_bytes > kPackHeader + kPackEntry * n)
+      ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0,
+                         hdr_bytes - kPackHeader - kPackEntry * n, s),
+         "gap");
+    if (n) ck(cudaMemcpyAsync(c->d_work.p, st + hdr_bytes, work_bytes, cudaMemcpyHostToDevice, s), "work");
+    ck(cudaEventRecord(c->stage_free, s), "event");
+    if (n) {
+      HashParams p{};
+      p.bufs = c->d_bufs.p;
+      p.chunk_map = c->d_chunk_map.p;
+      p.n_items = n;
+      p.chunk_size = cs;
+      p.k_full = zeros_crc(cs);
+      p.tables = c->crc.tables.p;
+      p.xinv = c->crc.xinv.p;
+      p.digest_cur = c->d_digest[c->cur].p;
+      p.work = c->d_work.p;
+      p.pack = pack;
+      p.payload_off = payload_off;
+      int grid = c->hash_grid(n);
+      c->timer_begin(kTimDelta, s);
+      k_hash_chunks<true><<<grid, kHashThreads, kHashSmem, s>>>(p);
+      check_launch("k_hash_chunks<copy>");
+      c->timer_end(kTimDelta, s);
+      ++c->launches;
+    }
+    if (pack_offset) *pack_offset = offset;
+    if (pack_bytes) *pack_bytes = total;
+  });
+}
+
+int pos_d2h_async(pos_ctx* c, void* host_dst, uint64_t offset, uint64_t bytes, uint64_t slice,
+                  void* stream) {
+  return guarded([&] {
+    if (!c || (!host_dst && bytes)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (offset + bytes > c->cache_cap) fail(POS_E_INVALID_LOCATOR, "range outside the cache");
+    if (slice == 0) slice = 8ull << 20;
+    for (uint64_t o = 0; o < bytes; o += slice) {
+      uint64_t n = std::min(slice, bytes - o);
+      ck(cudaMemcpyAsync(static_cast<uint8_t*>(host_dst) + o, c->cache.p + offset + o, n,
+                         cudaMemcpyDeviceToHost, S(stream)),
+         "d2h");
+    }
+  });
+}
+
+int pos_cache_info(pos_ctx* c, uint64_t* dev_ptr, uint64_t* capacity) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (dev_ptr) *dev_ptr = (uint64_t)c->cache.p;
+    if (capacity) *capacity = c->cache_cap;
+  });
+}
+
+int pos_scatter(pos_ctx* c, uint64_t pack_dev, uint64_t pack_bytes, void* stream) {
+  return guarded([&] {
+    if (!c || !pack_dev) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    if (pack_bytes < kPackHeader) fail(POS_E_CORRUPT_IMAGE, "pack shorter than its header");
+    uint8_t hdr[kPackHeader];
+    ck(cudaMemcpyAsync(hdr, (const void*)pack_dev, kPackHeader, cudaMemcpyDeviceToHost, s), "hdr");
+    ck(cudaStreamSynchronize(s), "sync");
+    uint32_t magic, n;
+    uint64_t cs, payload_off, payload;
+    std::memcpy(&magic, hdr, 4);
+    std::memcpy(&cs, hdr + 8, 8);
+    std::memcpy(&n, hdr + 16, 4);
+    std::memcpy(&payload_off, hdr + 24, 8);
+    std::memcpy(&payload, hdr + 32, 8);
+    if (magic != kPackMagic) fail(POS_E_CORRUPT_IMAGE, "bad pack magic");
+    if (cs != c->cfg.chunk_size) fail(POS_E_CORRUPT_IMAGE, "pack chunk_size differs from the context");
+    if (kPackHeader + (uint64_t)kPackEntry * n > payload_off || payload_off + payload > pack_bytes)
+      fail(POS_E_CORRUPT_IMAGE, "pack sections exceed its size");
+    if (!n) return;
+    c->d_items.ensure(std::max<uint64_t>(n, c->n_chunks));
+    ck(cudaMemsetAsync(c->d_err.p, 0, 4, s), "memset");
+    c->timer_begin(kTimScatter, s);
+    k_pack_items<<<(n + 255) / 256, 256, 0, s>>>((const uint8_t*)pack_dev, pack_bytes, c->d_bufs.p,
+                                                (uint32_t)c->bufs.size(), c->cfg.chunk_size,
+                                                c->d_items.p, c->d_err.p);
+    check_launch("k_pack_items");
+    ++c->launches;
+    uint32_t err = 0;
+    ck(cudaMemcpyAsync(c->h_scan.p, c->d_err.p, 4, cudaMemcpyDeviceToHost, s), "err");
+    ck(cudaStreamSynchronize(s), "sync");
+    std::memcpy(&err, c->h_scan.p, 4);
+    if (err & 1) fail(POS_E_CORRUPT_IMAGE, "malformed pack entry");
+    if (err & 2) fail(POS_E_INVALID_LOCATOR, "pack entry outside its buffer or unknown handle");
+    // Bulk path needs 16-B aligned chunk starts and payloads (payloads are by
+    // construction); the <16 B remainder is written byte-exact.
+    bool aligned = c->cfg.chunk_size % 16 == 0 && payload_off % 16 == 0 && pack_dev % 16 == 0;
+    for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
+    launch_copy(c, c->d_items.p, nullptr, n, aligned, s);
+    c->timer_end(kTimScatter, s);
+  });
+}
+
+static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
+  return guarded([&] {
+    if (!out) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    int cnt = 0;
+    if (e != cudaSuccess || cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+      fail(POS_E_NO_DEVICE, "no CUDA device: the dump path has no CPU fallback");
+    if (n == 0) {
+      *out = 0;
+      return;
+    }
+    if (!ptr) fail(POS_E_INVALID_ARGUMENT, "null device pointer");
+    CrcTables& t = engine_for_current_device();
+    // One virtual buffer of 64 KiB chunks, digests folded by k_buffer_crc.
+    const uint64_t cs = 65536;
+    uint64_t nc = (n + cs - 1) / cs;
+    DevBuf b{};
+    b.ptr = ptr;
+    b.size = n;
+    b.handle = 1;
+    b.nchunks = (uint32_t)nc;
+    uint64_t tail = n - (nc - 1) * cs;
+    b.k_tail = zeros_crc(tail);
+    b.x8_tail = x8nmodp(tail);
+    std::vector<uint2> cmap(nc);
+    for (uint64_t k = 0; k < nc; ++k) cmap[k] = make_uint2(0, (uint32_t)k);
+    std::vector<uint32_t> tcs(1024);
+    build_advance_table(cs, tcs.data());
+    DevArray<DevBuf> db;
+    DevArray<uint2> dm;
+    DevArray<uint32_t> dd, dt, dc;
+    DevArray<uint8_t> dz;
+    db.ensure(1);
+    dm.ensure(nc);
+    dd.ensure(nc);
+    dt.ensure(1024);
+    dc.ensure(1);
+    dz.ensure(2);
+    auto cleanup = [&] {
+      db.release();
+      dm.release();
+      dd.release();
+      dt.release();
+      dc.release();
+      dz.release();
+    };
+    try {
+      ck(cudaMemcpyAsync(db.p, &b, sizeof b, cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaMemcpyAsync(dm.p, cmap.data(), nc * 8, cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaMemcpyAsync(dt.p, tcs.data(), 4096, cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaMemsetAsync(dz.p, 0, 2, s), "memset");
+      HashParams p{};
+      p.bufs = db.p;
+      p.chunk_map = dm.p;
+      p.n_items = nc;
+      p.chunk_size = cs;
+      p.k_full = zeros_crc(cs);
+      p.tables = t.tables.p;
+      p.xinv = t.xinv.p;
+      p.digest_cur = dd.p;
+      p.digest_prev = dd.p;
+      p.flags = nullptr;  // digests only
+      p.bitmap = nullptr;
+      uint64_t blocks = (nc + 15) / 16;
+      int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)t.sm_count));
+      k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);
+      check_launch("k_hash_chunks");
+      k_buffer_crc<<<1, 32, 0, s>>>(db.p, 1, dd.p, dt.p, dz.p, 0, dc.p, dz.p + 1);
+      check_launch("k_buffer_crc");
+      uint32_t r = 0;
+      ck(cudaMemcpyAsync(&r, dc.p, 4, cudaMemcpyDeviceToHost, s), "d2h");
+      ck(cudaStreamSynchronize(s), "sync");
+      *out = r;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int pos_crc32(uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream) {
+  return crc_range(out, dev_ptr, n, S(stream));
+}
+
+int pos_crc32_update(uint32_t crc, uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream) {
+  uint32_t part = 0;
+  int rc = crc_range(&part, dev_ptr, n, S(stream));
+  if (rc != POS_OK) return rc;
+  if (!out) return POS_E_INVALID_ARGUMENT;
+  *out = crc32_combine(crc, part, n);  // crc32_update continues a final CRC (crc32.hpp:26-32)
+  return POS_OK;
+}
+
+int pos_fill(uint64_t dev_ptr, uint64_t n, uint64_t seed, void* stream) {
+  uint64_t r[3] = {dev_ptr, n, seed};
+  return pos_fill_batch(r, 1, stream);
+}
+
+int pos_fill_batch(const uint64_t* ranges, uint32_t count, void* stream) {
+  return guarded([&] {
+    if (!ranges && count) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+      fail(POS_E_NO_DEVICE, "no CUDA device");
+    cudaStream_t s = S(stream);
+    // Ranges travel by value in the kernel parameters: fully asynchronous.
+    for (uint32_t base = 0; base < count; base += kFillMaxRanges) {
+      FillBatch b{};
+      b.count = std::min<uint32_t>(kFillMaxRanges, count - base);
+      uint64_t maxn = 0;
+      for (uint32_t i = 0; i < b.count; ++i) {
+        const uint64_t* r = ranges + 3 * (uint64_t)(base + i);
+        b.r[i] = FillRange{r[0], r[1], r[2]};
+        maxn = std::max(maxn, r[1]);
+      }
+      uint64_t pairs = (maxn + 15) / 16;
+      dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((pairs + 255) / 256, 1184)), b.count);
+      k_fill<<<grid, 256, 0, s>>>(b);
+      check_launch("k_fill");
+    }
+  });
+}
+
+int pos_event_record(pos_ctx* c, uint32_t slot, void* stream) {
+  return guarded([&] {
+    if (!c || slot >= c->events.size()) fail(POS_E_INVALID_ARGUMENT, "bad event slot");
+    ck(cudaEventRecord(c->events[slot], S(stream)), "event record");
+  });
+}
+
+int pos_event_elapsed(pos_ctx* c, uint32_t a, uint32_t b, float* ms) {
+  return guarded([&] {
+    if (!c || !ms || a >= c->events.size() || b >= c->events.size())
+      fail(POS_E_INVALID_ARGUMENT, "bad event slot");
+    ck(cudaEventSynchronize(c->events[b]), "event sync");
+    ck(cudaEventElapsedTime(ms, c->events[a], c->events[b]), "elapsed");
+  });
+}
+
+int pos_stream_wait_event(pos_ctx* c, uint32_t slot, void* stream) {
+  return guarded([&] {
+    if (!c || slot >= c->events.size()) fail(POS_E_INVALID_ARGUMENT, "bad event slot");
+    ck(cudaStreamWaitEvent(S(stream), c->events[slot], 0), "stream wait event");
+  });
+}
+
+int pos_launch_count(pos_ctx* c, uint64_t* out) {
+  return guarded([&] {
+    if (!c || !out) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    *out = c->launches;
+  });
+}
+
+int pos_last_kernel_ms(pos_ctx* c, const char* which, float* ms) {
+  return guarded([&] {
+    if (!c || !which || !ms) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    for (int t = 0; t < kTimCount; ++t) {
+      if (std::strcmp(which, kTimerNames[t]) != 0) continue;
+      if (!c->timers[t].used) fail(POS_E_BAD_STATE, "no launch recorded");
+      ck(cudaEventSynchronize(c->timers[t].b), "event sync");
+      ck(cudaEventElapsedTime(ms, c->timers[t].a, c->timers[t].b), "elapsed");
+      return;
+    }
+    fail(POS_E_INVALID_ARGUMENT, "unknown timer");
+  });
+}
+
+int pos_pack_apply_host(const uint8_t* pack, uint64_t pack_bytes, const uint64_t* handles,
+                        uint8_t* const* hosts, const uint64_t* sizes, uint32_t nb, uint32_t threads) {
+  return guarded([&] {
+    if (!pack || (nb && (!handles || !hosts || !sizes))) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (pack_bytes < kPackHeader) fail(POS_E_CORRUPT_IMAGE, "pack shorter than its header");
+    uint32_t magic, n;
+    uint64_t cs, payload_off, payload;
+    std::memcpy(&magic, pack, 4);
+    std::memcpy(&cs, pack + 8, 8);
+    std::memcpy(&n, pack + 16, 4);
+    std::memcpy(&payload_off, pack + 24, 8);
+    std::memcpy(&payload, pack + 32, 8);
+    if (magic != kPackMagic) fail(POS_E_CORRUPT_IMAGE, "bad pack magic");
+    if (kPackHeader + (uint64_t)kPackEntry * n > payload_off || payload_off + payload > pack_bytes)
+      fail(POS_E_CORRUPT_IMAGE, "pack sections exceed its size");
+    // Resolve + validate every entry before writing anything (write_content
+    // checks before it copies, buffer.hpp:80).
+    struct Op { uint8_t* dst; const uint8_t* src; uint64_t len; };
+    std::vector<Op> ops(n);
+    for (uint32_t e = 0; e < n; ++e) {
+      const uint8_t* ent = pack + kPackHeader + (uint64_t)e * kPackEntry;
+      uint64_t h, off;
+      uint32_t c, len;
+      std::memcpy(&h, ent, 8);
+      std::memcpy(&off, ent + 8, 8);
+      std::memcpy(&c, ent + 16, 4);
+      std::memcpy(&len, ent + 20, 4);
+      const uint64_t* it = std::lower_bound(handles, handles + nb, h);
+      if (it == handles + nb || *it != h) fail(POS_E_INVALID_LOCATOR, "pack entry for unknown handle");
+      uint32_t b = (uint32_t)(it - handles);
+      if ((uint64_t)c * cs + len > sizes[b] || off + len > payload)
+        fail(POS_E_INVALID_LOCATOR, "pack entry outside its buffer");
+      ops[e] = Op{hosts[b] + (uint64_t)c * cs, pack + payload_off + off, len};
+    }
+    uint32_t nt = std::max<uint32_t>(1, std::min<uint32_t>(threads, 64));
+    if (nt == 1 || n < 2 * nt) {
+      for (const Op& o : ops) std::memcpy(o.dst, o.src, o.len);
+      return;
+    }
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (uint32_t e = t; e < n; e += nt) std::memcpy(ops[e].dst, ops[e].src, ops[e].len);
+      });
+    for (auto& th : pool) th.join();
+  });
+}
+
+int pos_image_write(const pos_image_desc* img, uint8_t* out, uint64_t cap, uint64_t* size) {
+  return guarded([&] {
+    if (!img || !size) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    std::string err;
+    int rc = write_posi_image(*img, out, cap, size, &err);
+    if (rc != POS_OK) fail(rc, err);
+  });
+}
+
+// ---- plumbing ----------------------------------------------------------
+
+int pos_device_count(int* n) {
+  return guarded([&] {
+    if (!n) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+    cudaGetLastError();
+    *n = c;
+  });
+}
+
+int pos_set_device(int device) {
+  return guarded([&] { require_device(device); });
+}
+
+int pos_dev_malloc(uint64_t bytes, uint64_t* dev_ptr) {
+  return guarded([&] {
+    if (!dev_ptr) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<uint64_t>(bytes, 1));
+    if (e != cudaSuccess)
+      fail(e == cudaErrorMemoryAllocation ? POS_E_OUT_OF_DEVICE_MEMORY : POS_E_CUDA,
+           std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    *dev_ptr = (uint64_t)p;
+  });
+}
+
+int pos_dev_free(uint64_t dev_ptr) {
+  return guarded([&] { ck(cudaFree((void*)dev_ptr), "cudaFree"); });
+}
+
+int pos_host_malloc_pinned(uint64_t bytes, void** host) {
+  return guarded([&] {
+    if (!host) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaHostAlloc(host, std::max<uint64_t>(bytes, 1), cudaHostAllocDefault), "cudaHostAlloc");
+  });
+}
+
+int pos_host_free_pinned(void* host) {
+  return guarded([&] { ck(cudaFreeHost(host), "cudaFreeHost"); });
+}
+
+int pos_memcpy(uint64_t dst, uint64_t src, uint64_t bytes, int kind, void* stream) {
+  return guarded([&] {
+    if (kind < 1 || kind > 3) fail(POS_E_INVALID_ARGUMENT, "bad memcpy kind");
+    if (!bytes) return;
+    ck(cudaMemcpyAsync((void*)dst, (const void*)src, bytes, (cudaMemcpyKind)kind, S(stream)),
+       "cudaMemcpyAsync");
+  });
+}
+
+int pos_memset(uint64_t dev_ptr, int value, uint64_t bytes, void* stream) {
+  return guarded([&] {
+    if (!bytes) return;
+    ck(cudaMemsetAsync((void*)dev_ptr, value, bytes, S(stream)), "cudaMemsetAsync");
+  });
+}
+
+int pos_stream_create(void** stream) {
+  return guarded([&] {
+    if (!stream) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    *stream = s;
+  });
+}
+
+int pos_stream_destroy(void* stream) {
+  return guarded([&] { ck(cudaStreamDestroy(S(stream)), "cudaStreamDestroy"); });
+}
+
+int pos_stream_sync(void* stream) {
+  return guarded([&] { ck(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize"); });
+}
+
+int pos_device_sync(void) {
+  return guarded([&] { ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); });
+}
+
+int pos_stream_wait(void* waiter, void* signaller) {
+  return guarded([&] {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e, S(signaller)), "event record");
+    ck(cudaStreamWaitEvent(S(waiter), e, 0), "stream wait");
+    cudaEventDestroy(e);
+  });
+}
+
+}  // extern "C"

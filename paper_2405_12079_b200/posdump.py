@@ -1,0 +1,453 @@
+"""Host-side mirror of the reference's dump-path interface over libposdump.so.
+
+Names follow the reference (proj/include/gpucrsim): ``crc32`` /
+``crc32_update`` (crc32.hpp:26-34), ``GpuBuffer.chunk_count/chunk_bytes``
+(buffer.hpp:44-49), and a ``DumpEngine`` exposing the hot-path members of
+``CrEngine`` (cr.hpp:124-1322): ``plan_precopy`` / ``scan_dedup`` /
+``dedup_verdicts`` / ``record_dirty`` / ``dirty_set`` / ``at_final_stop`` /
+``finalize_image`` / ``materialize``.  Errors raise ``SimError`` with the
+reference's Errc names.  Every byte-level operation is a CUDA kernel behind
+the C ABI; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import SimError, CorruptImageError, NoDeviceError, check  # noqa: F401
+
+kDeviceAddrBase = 0x7000_0000_0000  # config.hpp:14
+H2D, D2H, D2D = 1, 2, 3
+
+
+def lib():
+    return _lib.load()
+
+
+def _s(stream) -> Optional[int]:
+    return None if stream is None else int(stream)
+
+
+# ---------------------------------------------------------------------------
+# plumbing
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib().pos_device_count(C.byref(n)))
+    return n.value
+
+
+class DeviceMemory:
+    """A raw device allocation (cudaMalloc), freed on close/GC."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_uint64(0)
+        check(lib().pos_dev_malloc(nbytes, C.byref(p)))
+        self.ptr, self.nbytes = p.value, nbytes
+
+    def close(self):
+        if self.ptr:
+            lib().pos_dev_free(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, data, offset: int = 0, stream=None):
+        a = np.ascontiguousarray(np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data.view(np.uint8))
+        check(lib().pos_memcpy(self.ptr + offset, a.ctypes.data, a.nbytes, H2D, _s(stream)))
+        check(lib().pos_stream_sync(_s(stream)))
+
+    def download(self, nbytes: Optional[int] = None, offset: int = 0, stream=None) -> np.ndarray:
+        n = self.nbytes - offset if nbytes is None else nbytes
+        out = np.empty(n, dtype=np.uint8)
+        check(lib().pos_memcpy(out.ctypes.data, self.ptr + offset, n, D2H, _s(stream)))
+        check(lib().pos_stream_sync(_s(stream)))
+        return out
+
+
+class PinnedHost:
+    """Page-locked host memory (cudaHostAlloc) viewed as a numpy array."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p(0)
+        check(lib().pos_host_malloc_pinned(max(nbytes, 1), C.byref(p)))
+        self.ptr, self.nbytes = p.value, nbytes
+        self.array = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(self.ptr))[:nbytes]
+
+    def close(self):
+        if self.ptr:
+            self.array = None
+            lib().pos_host_free_pinned(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Stream:
+    def __init__(self):
+        s = C.c_void_p(0)
+        check(lib().pos_stream_create(C.byref(s)))
+        self.handle = s.value
+
+    def __int__(self):
+        return self.handle
+
+    def synchronize(self):
+        check(lib().pos_stream_sync(self.handle))
+
+    def wait(self, other: "Stream"):
+        check(lib().pos_stream_wait(self.handle, int(other)))
+
+    def close(self):
+        if self.handle:
+            lib().pos_stream_destroy(self.handle)
+            self.handle = 0
+
+
+def device_synchronize():
+    check(lib().pos_device_sync())
+
+
+# ---------------------------------------------------------------------------
+# crc32 over device memory (crc32.hpp:26-34)
+
+def crc32(dev_ptr: int, n: int, stream=None) -> int:
+    out = C.c_uint32(0)
+    check(lib().pos_crc32(dev_ptr, n, C.byref(out), _s(stream)))
+    return out.value
+
+
+def crc32_update(crc: int, dev_ptr: int, n: int, stream=None) -> int:
+    out = C.c_uint32(0)
+    check(lib().pos_crc32_update(crc, dev_ptr, n, C.byref(out), _s(stream)))
+    return out.value
+
+
+def fill_bytes(dev_ptr: int, n: int, seed: int, stream=None) -> None:
+    """Device fill_bytes (rng.hpp:43-54); asynchronous on `stream`."""
+    check(lib().pos_fill(dev_ptr, n, seed & 0xFFFFFFFFFFFFFFFF, _s(stream)))
+
+
+def fill_batch(ranges: Sequence[tuple[int, int, int]], stream=None) -> None:
+    if not ranges:
+        return
+    a = np.array([[p, n, s & 0xFFFFFFFFFFFFFFFF] for p, n, s in ranges], dtype=np.uint64)
+    check(lib().pos_fill_batch(a.ctypes.data, len(ranges), _s(stream)))
+
+
+# ---------------------------------------------------------------------------
+# buffers
+
+@dataclass
+class Upstream:
+    """buffer.hpp:20-25 (+ the cr.hpp:420 host watermark verdict)."""
+    crc: int
+    host_untouched: bool = True
+
+
+@dataclass
+class GpuBuffer:
+    """The fields of gpucrsim::GpuBuffer (buffer.hpp:27-41) the path reads."""
+    handle: int
+    dev_ptr: int
+    size: int
+    upstream: Optional[Upstream] = None
+    written_since_ckpt: bool = True
+
+    def chunk_count(self, chunk_size: int) -> int:  # buffer.hpp:44, :119
+        return (self.size + chunk_size - 1) // chunk_size
+
+    def chunk_bytes(self, idx: int, chunk_size: int) -> int:  # buffer.hpp:46-49
+        return min(chunk_size, self.size - idx * chunk_size)
+
+    def desc(self) -> _lib.pos_buffer_desc:
+        d = _lib.pos_buffer_desc()
+        d.handle, d.dev_ptr, d.size = self.handle, self.dev_ptr, self.size
+        d.has_upstream = 1 if self.upstream is not None else 0
+        d.upstream_crc = self.upstream.crc if self.upstream else 0
+        d.host_untouched = 1 if (self.upstream and self.upstream.host_untouched) else 0
+        d.written_since_ckpt = 1 if self.written_since_ckpt else 0
+        return d
+
+
+# ---------------------------------------------------------------------------
+# POSD packs
+
+PACK_HEADER, PACK_ENTRY = 64, 32
+
+
+def parse_pack(pack: np.ndarray) -> dict:
+    """Header + entries of a POSD pack held in host memory."""
+    b = pack.view(np.uint8)
+    if b[:4].tobytes() != b"POSD":
+        raise CorruptImageError(_lib.CODES["CorruptImage"], "bad pack magic")
+    hdr = b[:64]
+    n = int(hdr[16:20].view(np.uint32)[0])
+    ents = b[64:64 + 32 * n].reshape(n, 32) if n else np.zeros((0, 32), np.uint8)
+    return {
+        "chunk_size": int(hdr[8:16].view(np.uint64)[0]),
+        "n_entries": n,
+        "flags": int(hdr[20:24].view(np.uint32)[0]),
+        "payload_off": int(hdr[24:32].view(np.uint64)[0]),
+        "payload_bytes": int(hdr[32:40].view(np.uint64)[0]),
+        "epoch": int(hdr[40:48].view(np.uint64)[0]),
+        "total": int(hdr[48:56].view(np.uint64)[0]),
+        "handle": ents[:, 0:8].copy().view(np.uint64).ravel(),
+        "offset": ents[:, 8:16].copy().view(np.uint64).ravel(),
+        "chunk": ents[:, 16:20].copy().view(np.uint32).ravel(),
+        "len": ents[:, 20:24].copy().view(np.uint32).ravel(),
+        "crc": ents[:, 24:28].copy().view(np.uint32).ravel(),
+    }
+
+
+def apply_pack_host(pack: np.ndarray, handles: Sequence[int], hosts: Sequence[np.ndarray],
+                    threads: int = 1) -> None:
+    """Apply a POSD pack onto host copies of the buffers (cr.hpp:499-501)."""
+    n = len(handles)
+    h = np.ascontiguousarray(np.array(handles, dtype=np.uint64))
+    ptrs = (C.c_void_p * max(n, 1))(*[x.ctypes.data for x in hosts])
+    sizes = np.array([x.nbytes for x in hosts], dtype=np.uint64)
+    check(lib().pos_pack_apply_host(pack.ctypes.data, pack.nbytes, h.ctypes.data, ptrs,
+                                    sizes.ctypes.data, n, threads))
+
+
+# ---------------------------------------------------------------------------
+# the engine
+
+@dataclass
+class SimConfig:
+    """The SimConfig keys of the path (config.hpp:18-45)."""
+    chunk_size: int = 64 * 1024
+    page_size: int = 4096
+    device_capacity: int = 80_000_000_000
+    staging_fraction: float = 1.0 / 16.0
+    dedup: bool = True
+    cache_capacity: int = 0  # explicit O3 cache size; 0 => staging_capacity of the device
+
+
+class DumpEngine:
+    """Hot-path members of gpucrsim::CrEngine over the CUDA path."""
+
+    def __init__(self, cfg: SimConfig = SimConfig(), device: int = 0):
+        self.cfg = cfg
+        c = _lib.pos_config()
+        c.chunk_size, c.page_size = cfg.chunk_size, cfg.page_size
+        c.cache_capacity = cfg.cache_capacity
+        c.staging_fraction = cfg.staging_fraction
+        c.device, c.dedup = device, 1 if cfg.dedup else 0
+        ctx = C.c_void_p(0)
+        check(lib().pos_ctx_create(C.byref(c), C.byref(ctx)))
+        self.ctx = ctx.value
+        self.buffers: list[GpuBuffer] = []
+        self.precopy_bytes = 0
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().pos_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # snapshot_buffers_ = active_handles() (cr.hpp:346)
+    def register_buffers(self, bufs: Iterable[GpuBuffer]) -> None:
+        self.buffers = sorted(bufs, key=lambda b: b.handle)
+        arr = (_lib.pos_buffer_desc * max(len(self.buffers), 1))(*[b.desc() for b in self.buffers])
+        check(lib().pos_register_buffers(self.ctx, arr, len(self.buffers)))
+
+    def update_buffer(self, b: GpuBuffer) -> None:
+        d = b.desc()
+        check(lib().pos_update_buffer(self.ctx, C.byref(d)))
+
+    @property
+    def n_chunks(self) -> int:
+        n = C.c_uint64(0)
+        check(lib().pos_num_chunks(self.ctx, C.byref(n)))
+        return n.value
+
+    # ---- O2
+    def hash_chunks(self, stream=None) -> None:
+        check(lib().pos_hash_chunks(self.ctx, _s(stream)))
+
+    def commit_epoch(self) -> None:
+        check(lib().pos_commit_epoch(self.ctx))
+
+    def digests(self, stream=None) -> np.ndarray:
+        out = np.empty(self.n_chunks, dtype=np.uint32)
+        check(lib().pos_read_digests(self.ctx, out.ctypes.data, out.size, _s(stream)))
+        return out
+
+    def flags(self, stream=None) -> np.ndarray:
+        out = np.empty(self.n_chunks, dtype=np.uint8)
+        check(lib().pos_read_flags(self.ctx, out.ctypes.data, out.size, _s(stream)))
+        return out
+
+    def bitmap(self, stream=None) -> np.ndarray:
+        out = np.empty((self.n_chunks + 31) // 32, dtype=np.uint32)
+        check(lib().pos_read_bitmap(self.ctx, out.ctypes.data, out.size, _s(stream)))
+        return out
+
+    # ---- O1 (scan_dedup, cr.hpp:416-425)
+    def scan_dedup(self, stream=None) -> None:
+        check(lib().pos_buffer_crc(self.ctx, _s(stream)))
+
+    def buffer_crcs(self, stream=None) -> tuple[np.ndarray, np.ndarray]:
+        n = len(self.buffers)
+        crcs = np.empty(n, dtype=np.uint32)
+        ver = np.empty(n, dtype=np.uint8)
+        check(lib().pos_read_buffer_crcs(self.ctx, crcs.ctypes.data, ver.ctypes.data, n, _s(stream)))
+        return crcs, ver
+
+    def dedup_verdicts(self, stream=None) -> dict[int, bool]:
+        """dedup_ok_ (cr.hpp:141): only buffers with upstream provenance."""
+        _, ver = self.buffer_crcs(stream)
+        return {b.handle: bool(v) for b, v in zip(self.buffers, ver) if b.upstream is not None}
+
+    # ---- DAG write sets (record_dirty, cr.hpp:901-931)
+    def record_dirty(self, handles: Iterable[int]) -> None:
+        a = np.array(list(handles), dtype=np.uint64)
+        check(lib().pos_record_dirty(self.ctx, a.ctypes.data if a.size else None, a.size))
+
+    def clear_dirty(self) -> None:
+        check(lib().pos_clear_dirty(self.ctx))
+
+    # ---- O3 compaction
+    def compact(self, exclude_dag_dirty: bool = True, stream=None) -> int:
+        n = C.c_uint64(0)
+        check(lib().pos_compact(self.ctx, 1 if exclude_dag_dirty else 0, _s(stream), C.byref(n)))
+        self.precopy_bytes = n.value
+        return n.value
+
+    def plan_precopy(self, stream=None, exclude_dag_dirty: bool = True) -> int:
+        """hash -> O1 verdicts -> compaction into the cache (cr.hpp:377-406).
+        Returns the pre-copy pack size (bytes at cache offset 0)."""
+        self.hash_chunks(stream)
+        self.scan_dedup(stream)
+        return self.compact(exclude_dag_dirty, stream)
+
+    # ---- STW delta-copy (at_final_stop, cr.hpp:599-621)
+    def at_final_stop(self, stream=None) -> tuple[int, int]:
+        off, n = C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_delta_copy(self.ctx, _s(stream), C.byref(off), C.byref(n)))
+        return off.value, n.value
+
+    # ---- host leg
+    def d2h_async(self, host_ptr: int, offset: int, nbytes: int, stream=None, slice_bytes: int = 0) -> None:
+        check(lib().pos_d2h_async(self.ctx, host_ptr, offset, nbytes, slice_bytes, _s(stream)))
+
+    def cache(self) -> tuple[int, int]:
+        p, cap = C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_cache_info(self.ctx, C.byref(p), C.byref(cap)))
+        return p.value, cap.value
+
+    # ---- restore scatter (materialize / load_complete, cr.hpp:1026-1084)
+    def materialize(self, pack_dev_ptr: int, pack_bytes: int, stream=None) -> None:
+        check(lib().pos_scatter(self.ctx, pack_dev_ptr, pack_bytes, _s(stream)))
+
+    # ---- timing
+    def event_record(self, slot: int, stream=None) -> None:
+        check(lib().pos_event_record(self.ctx, slot, _s(stream)))
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        ms = C.c_float(0)
+        check(lib().pos_event_elapsed(self.ctx, a, b, C.byref(ms)))
+        return ms.value
+
+    def stream_wait_event(self, slot: int, stream=None) -> None:
+        check(lib().pos_stream_wait_event(self.ctx, slot, _s(stream)))
+
+    def kernel_ms(self, which: str) -> float:
+        ms = C.c_float(0)
+        check(lib().pos_last_kernel_ms(self.ctx, which.encode(), C.byref(ms)))
+        return ms.value
+
+    @property
+    def launches(self) -> int:
+        n = C.c_uint64(0)
+        check(lib().pos_launch_count(self.ctx, C.byref(n)))
+        return n.value
+
+
+# ---------------------------------------------------------------------------
+# POSI image (image.hpp:136-207)
+
+@dataclass
+class GpuBufferRec:
+    handle: int
+    kind: int = 0  # 0 Inline, 1 DedupRef, 2 Recompute
+    inline_bytes: Optional[np.ndarray] = None
+    dedup_first_page: int = 0
+    dedup_page_count: int = 0
+    dedup_offset: int = 0
+    dedup_crc: int = 0
+    recompute_nodes: list = field(default_factory=list)
+
+
+@dataclass
+class CheckpointImage:
+    page_size: int = 4096
+    host_pages: list = field(default_factory=list)  # [(index, bytes)]
+    gpu_records: list = field(default_factory=list)
+    dag_bytes: bytes = b""
+    stream_ids: list = field(default_factory=list)
+    allocs: list = field(default_factory=list)  # [(handle, base, size)]
+    cursor: int = 0
+    next_handle: int = 1
+    next_base: int = kDeviceAddrBase
+
+
+def write_image(img: CheckpointImage) -> bytes:
+    keep = []
+    pages = (_lib.pos_image_page * max(len(img.host_pages), 1))()
+    for i, (idx, data) in enumerate(img.host_pages):
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8))
+        if a.nbytes != img.page_size:
+            raise SimError(_lib.CODES["InvariantViolation"], "host page size mismatch")
+        keep.append(a)
+        pages[i].index, pages[i].bytes = idx, a.ctypes.data
+    recs = (_lib.pos_image_rec * max(len(img.gpu_records), 1))()
+    for i, r in enumerate(img.gpu_records):
+        recs[i].handle, recs[i].kind = r.handle, r.kind
+        if r.kind == 0:
+            a = np.ascontiguousarray(np.asarray(r.inline_bytes, dtype=np.uint8).ravel())
+            keep.append(a)
+            recs[i].inline_bytes, recs[i].inline_len = a.ctypes.data, a.nbytes
+        recs[i].dedup_first_page = r.dedup_first_page
+        recs[i].dedup_page_count = r.dedup_page_count
+        recs[i].dedup_offset = r.dedup_offset
+        recs[i].dedup_crc = r.dedup_crc
+        if r.recompute_nodes:
+            a = np.array(r.recompute_nodes, dtype=np.uint64)
+            keep.append(a)
+            recs[i].recompute, recs[i].n_recompute = a.ctypes.data, a.size
+    allocs = (_lib.pos_image_alloc * max(len(img.allocs), 1))(*[_lib.pos_image_alloc(*a) for a in img.allocs])
+    streams = np.array(img.stream_ids, dtype=np.uint64)
+    dag = np.frombuffer(img.dag_bytes, dtype=np.uint8) if img.dag_bytes else np.zeros(0, np.uint8)
+    d = _lib.pos_image_desc()
+    d.page_size = img.page_size
+    d.pages, d.n_pages = C.cast(pages, C.c_void_p), len(img.host_pages)
+    d.recs, d.n_recs = C.cast(recs, C.c_void_p), len(img.gpu_records)
+    d.allocs, d.n_allocs = C.cast(allocs, C.c_void_p), len(img.allocs)
+    d.stream_ids, d.n_streams = (streams.ctypes.data if streams.size else None), streams.size
+    d.cursor, d.next_handle, d.next_base = img.cursor, img.next_handle, img.next_base
+    d.dag_bytes, d.dag_len = (dag.ctypes.data if dag.size else None), dag.size
+    size = C.c_uint64(0)
+    check(lib().pos_image_write(C.byref(d), None, 0, C.byref(size)))
+    out = np.empty(size.value, dtype=np.uint8)
+    check(lib().pos_image_write(C.byref(d), out.ctypes.data, out.nbytes, C.byref(size)))
+    return out.tobytes()

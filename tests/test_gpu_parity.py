@@ -1,0 +1,411 @@
+"""GPU parity: every kernel of the dump path through the C ABI, against the
+C restatement (oracle/) on the same seeded inputs.  Integer/byte work, so
+every comparison is bit-exact.
+
+Edge cases follow the reference: short tails (buffer.hpp:46-49), chunk_size
+of any positive value (config.hpp:70-71), 1-byte buffers (buffer.hpp:109),
+unknown handles / out-of-range writes (buffer.hpp:80-86), corrupt input.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2405_12079_b200 as pd
+from oracle_ctypes import or_buffer_t
+
+pytestmark = pytest.mark.gpu
+
+
+def mb(orc, seed, n):
+    out = np.empty(n, np.uint8)
+    orc.or_fill_bytes(seed, out.ctypes.data, n)
+    return out
+
+
+def ocrc(orc, a):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return orc.or_crc32(a.ctypes.data, a.nbytes)
+
+
+def odigests(orc, a, cs):
+    n = orc.or_chunk_count(a.size, cs)
+    out = np.empty(n, np.uint32)
+    orc.or_chunk_digests(a.ctypes.data, a.size, cs, out.ctypes.data)
+    return out
+
+
+def opack(orc, bufs, cs, flags, epoch=0, pflags=0):
+    arr = (or_buffer_t * len(bufs))(*[or_buffer_t(h, a.ctypes.data, a.size) for h, a in bufs])
+    n = orc.or_build_pack(arr, len(bufs), cs, flags.ctypes.data, epoch, pflags, None)
+    out = np.empty(n, np.uint8)
+    orc.or_build_pack(arr, len(bufs), cs, flags.ctypes.data, epoch, pflags, out.ctypes.data)
+    return out
+
+
+class Proc:
+    """A set of device buffers with a host mirror (the oracle's view)."""
+
+    def __init__(self, orc, sizes, seed0=100, handles=None, align=256, offsets=None):
+        self.orc = orc
+        self.sizes = list(sizes)
+        self.handles = list(handles or range(1, len(sizes) + 1))
+        offsets = offsets or [0] * len(sizes)
+        self.mem = []
+        self.bufs = []
+        self.host = []
+        for i, (n, off) in enumerate(zip(self.sizes, offsets)):
+            m = pd.DeviceMemory(n + off + align)
+            ptr = m.ptr + off
+            self.mem.append(m)
+            self.bufs.append(pd.GpuBuffer(handle=self.handles[i], dev_ptr=ptr, size=n))
+            pd.fill_bytes(ptr, n, seed0 + i)
+            self.host.append(mb(orc, seed0 + i, n))
+        pd.device_synchronize()
+
+    def write(self, i, off, n, seed):
+        pd.fill_bytes(self.bufs[i].dev_ptr + off, n, seed)
+        self.host[i][off:off + n] = mb(self.orc, seed, n)
+
+    def read(self, i):
+        b = self.bufs[i]
+        out = np.empty(b.size, np.uint8)
+        pd.check(pd.lib().pos_memcpy(out.ctypes.data, b.dev_ptr, b.size, 2, None))
+        pd.device_synchronize()
+        return out
+
+    def zero(self, i):
+        b = self.bufs[i]
+        pd.check(pd.lib().pos_memset(b.dev_ptr, 0, b.size, None))
+
+
+def download_cache(eng, offset, n):
+    pin = pd.PinnedHost(n)
+    eng.d2h_async(pin.ptr, offset, n, slice_bytes=1 << 16)
+    pd.device_synchronize()
+    out = pin.array.copy()
+    pin.close()
+    return out
+
+
+# ---------------------------------------------------------------------------
+
+def test_device_fill_matches_fill_bytes(orc):
+    for n, off in [(1, 0), (7, 3), (16, 0), (17, 1), (1000, 5), (65536 + 9, 0)]:
+        m = pd.DeviceMemory(n + off + 16)
+        pd.fill_bytes(m.ptr + off, n, 12345 + n)
+        pd.device_synchronize()
+        assert np.array_equal(m.download(n, off), mb(orc, 12345 + n, n))
+
+
+@pytest.mark.parametrize("n", [1, 2, 15, 16, 17, 100, 511, 512, 513, 4095, 4096, 65535, 65536,
+                               65537, 1 << 20, (3 << 20) + 7])
+def test_crc32_device_matches_reference(orc, n):
+    m = pd.DeviceMemory(n + 64)
+    pd.fill_bytes(m.ptr, n + 64, 7 + n)
+    pd.device_synchronize()
+    host = mb(orc, 7 + n, n + 64)
+    for off in (0, 1, 3, 8, 15):
+        assert pd.crc32(m.ptr + off, n) == ocrc(orc, host[off:off + n]), (n, off)
+
+
+def test_crc32_known_vector_and_update(orc):  # test_memory.cpp:10-17
+    m = pd.DeviceMemory(16)
+    m.upload(np.frombuffer(b"123456789", np.uint8))
+    assert pd.crc32(m.ptr, 9) == 0xCBF43926
+    c = pd.crc32_update(0, m.ptr, 4)
+    c = pd.crc32_update(c, m.ptr + 4, 5)
+    assert c == 0xCBF43926
+    assert pd.crc32(m.ptr, 0) == 0
+
+
+@pytest.mark.parametrize("cs", [4096, 65536, 1000, 7, 16, 65537, 1 << 20])
+def test_chunk_digests_and_epoch_bitmap(orc, cs):
+    sizes = [3 * cs, 10000, 1, 2 * cs + 5, 70001]
+    p = Proc(orc, sizes)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=8 << 20))
+    eng.register_buffers(p.bufs)
+    eng.hash_chunks()
+    want = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests(), want)
+    assert eng.flags().all()  # fresh epoch: everything ships
+    eng.commit_epoch()
+    # epoch 1: rewrite a few ranges (straddling chunk boundaries, and one no-op)
+    p.write(0, cs - 3, 10, 999)
+    p.write(3, 2 * cs, 5, 998)
+    p.write(4, 0, 1, 997)
+    pd.device_synchronize()
+    prev = want
+    eng.hash_chunks()
+    cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests(), cur)
+    oflags = np.zeros(cur.size, np.uint8)
+    orc.or_dirty_flags(prev.ctypes.data, cur.ctypes.data, cur.size, 1, oflags.ctypes.data)
+    assert np.array_equal(eng.flags(), oflags)
+    bm = np.zeros((cur.size + 31) // 32, np.uint32)
+    orc.or_pack_bitmap(oflags.ctypes.data, cur.size, bm.ctypes.data)
+    assert np.array_equal(eng.bitmap(), bm)
+    eng.close()
+
+
+def test_unaligned_buffers(orc):
+    cs = 4096
+    p = Proc(orc, [5000, 12345, 3], offsets=[1, 7, 13])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    n = eng.plan_precopy()
+    want = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests(), want)
+    pack = download_cache(eng, 0, n)
+    flags = np.ones(want.size, np.uint8)
+    assert np.array_equal(pack, opack(orc, list(zip(p.handles, p.host)), cs, flags))
+    eng.close()
+
+
+def test_buffer_crc_and_dedup_verdicts(orc):
+    """scan_dedup (cr.hpp:416-425) + finalize_image gate (cr.hpp:720):
+    clean -> ok, rewritten -> not ok, host touched -> not ok, no upstream ->
+    absent, DAG-written -> not ok (mirrors test_cr.cpp:375-415)."""
+    cs = 65536
+    sizes = [65536, 100000, 65536 * 3, 4096, 777]
+    p = Proc(orc, sizes, seed0=300)
+    crcs = [ocrc(orc, h) for h in p.host]
+    p.bufs[0].upstream = pd.Upstream(crcs[0], True)        # clean
+    p.bufs[1].upstream = pd.Upstream(crcs[1], True)        # rewritten below
+    p.bufs[2].upstream = pd.Upstream(crcs[2], False)       # host touched
+    p.bufs[3].upstream = None                              # no provenance
+    p.bufs[4].upstream = pd.Upstream(crcs[4], True)        # DAG-flagged
+    p.write(1, 500, 3, 42)
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=8 << 20))
+    eng.register_buffers(p.bufs)
+    eng.record_dirty([5, 999])  # 999 is not in the snapshot: ignored (cr.hpp:904)
+    eng.hash_chunks()
+    eng.scan_dedup()
+    got, ver = eng.buffer_crcs()
+    assert [int(x) for x in got] == [ocrc(orc, h) for h in p.host]
+    assert eng.dedup_verdicts() == {1: True, 2: False, 3: False, 5: False}
+    for i, b in enumerate(p.bufs):
+        want = orc.or_dedup_verdict(b.upstream is not None, ocrc(orc, p.host[i]),
+                                    b.upstream.crc if b.upstream else 0,
+                                    b.upstream.host_untouched if b.upstream else 0)
+        assert bool(ver[i]) == (bool(want) and b.handle != 5)
+    # dedup disabled (config.hpp:36): no verdict is ok
+    eng2 = pd.DumpEngine(pd.SimConfig(chunk_size=cs, dedup=False, cache_capacity=8 << 20))
+    eng2.register_buffers(p.bufs)
+    eng2.hash_chunks()
+    eng2.scan_dedup()
+    assert not any(eng2.dedup_verdicts().values())
+    eng.close()
+    eng2.close()
+
+
+@pytest.mark.parametrize("cs", [4096, 65536, 1000])
+def test_compact_pack_is_bit_exact(orc, cs):
+    """O3 pack == oracle pack for the eligible chunks: dirty, not dedup-ok,
+    not DAG-dirty (chunk_copied abandons those, cr.hpp:487)."""
+    sizes = [4 * cs, 3 * cs + 11, 17, 5 * cs, 9000]
+    p = Proc(orc, sizes, seed0=500)
+    crcs = [ocrc(orc, h) for h in p.host]
+    p.bufs[2].upstream = pd.Upstream(crcs[2], True)  # dedup-ok: never packed
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=16 << 20))
+    eng.register_buffers(p.bufs)
+    eng.hash_chunks()
+    eng.commit_epoch()
+    rng = np.random.default_rng(cs)
+    for i, n in enumerate(sizes):
+        for _ in range(2):
+            off = int(rng.integers(0, n))
+            p.write(i, off, min(n - off, int(rng.integers(1, 300))), int(rng.integers(1, 1 << 40)))
+    pd.device_synchronize()
+    eng.record_dirty([4])
+    prev = np.concatenate([odigests(orc, h, cs) for h in p.host])  # placeholder, recomputed below
+    n = eng.plan_precopy(exclude_dag_dirty=True)
+    cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    flags = eng.flags()
+    # eligibility mask
+    g = 0
+    elig = flags.copy()
+    for i, b in enumerate(p.bufs):
+        nc = b.chunk_count(cs)
+        if b.handle == 4 or (b.upstream is not None and ocrc(orc, p.host[i]) == b.upstream.crc):
+            elig[g:g + nc] = 0
+        g += nc
+    want = opack(orc, list(zip(p.handles, p.host)), cs, elig, epoch=1)
+    got = download_cache(eng, 0, n)
+    assert n == want.size
+    assert np.array_equal(got, want)
+    assert np.array_equal(eng.digests(), cur)
+    del prev
+    eng.close()
+
+
+def test_delta_copy_pack_and_digests(orc):
+    """at_final_stop (cr.hpp:599-621): whole DAG-flagged buffers, after the
+    pre-copy pack, ascending handle; digests refreshed from what was copied."""
+    cs = 4096
+    sizes = [3 * cs, 5000, 100, 2 * cs]
+    p = Proc(orc, sizes, seed0=700, handles=[2, 4, 6, 8])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
+    eng.register_buffers(p.bufs)
+    n0 = eng.plan_precopy()
+    eng.record_dirty([8, 4])
+    p.write(1, 10, 4000, 31)   # the app writes while the pre-copy drains
+    p.write(3, 0, 2 * cs, 32)
+    pd.device_synchronize()
+    off, n1 = eng.at_final_stop()
+    assert off == (n0 + 255) // 256 * 256
+    got = download_cache(eng, off, n1)
+    g_flags = np.concatenate([np.full(b.chunk_count(cs), b.handle in (4, 8), np.uint8) for b in p.bufs])
+    want = opack(orc, list(zip(p.handles, p.host)), cs, g_flags, epoch=0, pflags=1)
+    assert np.array_equal(got, want)
+    cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests()[g_flags == 1], cur[g_flags == 1])
+    eng.close()
+
+
+def test_scatter_restores_state(orc):
+    """materialize/load_complete (cr.hpp:1026-1084): packs applied in order
+    reproduce the buffers."""
+    cs = 4096
+    sizes = [3 * cs, 5000, 1, 2 * cs + 100]
+    p = Proc(orc, sizes, seed0=900)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
+    eng.register_buffers(p.bufs)
+    n = eng.plan_precopy()
+    full = download_cache(eng, 0, n)
+    eng.commit_epoch()
+    p.write(3, cs + 7, 20, 5)
+    p.write(0, 0, 1, 6)
+    pd.device_synchronize()
+    n2 = eng.plan_precopy()
+    delta = download_cache(eng, 0, n2)
+    assert n2 < n
+    for i in range(len(sizes)):
+        p.zero(i)
+    for pack in (full, delta):
+        dev = pd.DeviceMemory(pack.size)
+        dev.upload(pack)
+        eng.materialize(dev.ptr, pack.size)
+    pd.device_synchronize()
+    for i in range(len(sizes)):
+        assert np.array_equal(p.read(i), p.host[i])
+    # corrupt input
+    bad = full.copy()
+    bad[:4] = 0
+    dev = pd.DeviceMemory(bad.size)
+    dev.upload(bad)
+    with pytest.raises(pd.CorruptImageError):
+        eng.materialize(dev.ptr, bad.size)
+    # entry for an unknown handle -> InvalidLocator (buffer.hpp:80)
+    bad = full.copy()
+    bad[64:72] = np.frombuffer(np.uint64(12345).tobytes(), np.uint8)
+    dev.upload(bad)
+    with pytest.raises(pd.SimError) as e:
+        eng.materialize(dev.ptr, bad.size)
+    assert e.value.errc == "InvalidLocator"
+    eng.close()
+
+
+def test_staging_exhausted(orc):
+    cs = 4096
+    p = Proc(orc, [64 * cs], seed0=11)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=16 * cs))
+    eng.register_buffers(p.bufs)
+    with pytest.raises(pd.SimError) as e:
+        eng.plan_precopy()
+    assert e.value.errc == "StagingExhausted"
+    eng.close()
+
+
+def test_host_image_end_to_end(orc, ref):
+    """Epoch 0 full pack + epoch 1 pre-copy + STW delta applied to the host
+    image reproduce the device state; the POSI bytes equal the reference's
+    write_image over the same Inline contents."""
+    from oracle_ctypes import ref_image  # noqa: F401
+    cs = 65536
+    sizes = [1 << 20, 300000, 65536, 12345]
+    p = Proc(orc, sizes, seed0=1200)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=8 << 20))
+    eng.register_buffers(p.bufs)
+    image = [np.zeros(n, np.uint8) for n in sizes]
+    n = eng.plan_precopy()
+    pd.apply_pack_host(download_cache(eng, 0, n), p.handles, image)
+    eng.commit_epoch()
+    p.write(0, 3 * cs + 5, 100, 77)
+    p.write(1, 0, 10, 78)
+    pd.device_synchronize()
+    eng.record_dirty([3])
+    n = eng.plan_precopy()
+    pd.apply_pack_host(download_cache(eng, 0, n), p.handles, image)
+    p.write(2, 100, 100, 79)
+    pd.device_synchronize()
+    off, n2 = eng.at_final_stop()
+    pd.apply_pack_host(download_cache(eng, off, n2), p.handles, image)
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i])
+    img = pd.CheckpointImage()
+    img.gpu_records = [pd.GpuBufferRec(h, 0, inline_bytes=image[i]) for i, h in enumerate(p.handles)]
+    img.allocs = [(h, 0x7000_0000_0000 + 0x100000 * i, sizes[i]) for i, h in enumerate(p.handles)]
+    ours = pd.write_image(img)
+    # reference writer over the oracle's view of the device
+    from oracle_ctypes import Rec, Alloc
+    recs = (Rec * 4)()
+    for i, h in enumerate(p.handles):
+        recs[i].handle, recs[i].kind = h, 0
+        recs[i].inline_bytes, recs[i].inline_len = p.host[i].ctypes.data, sizes[i]
+    allocs = (Alloc * 4)(*[Alloc(*a) for a in img.allocs])
+    args = [4096, None, 0, recs, 4, allocs, 4, None, 0, 0, 1, 0x7000_0000_0000, None, 0]
+    nref = ref.ref_write_image(*args, None, 0)
+    out = np.empty(nref, np.uint8)
+    ref.ref_write_image(*args, out.ctypes.data, nref)
+    assert ours == out.tobytes()
+    eng.close()
+
+
+@pytest.mark.slow
+def test_c1_full_size_properties(orc):
+    """BASELINE config 1 at full size (1 GiB, 64 x 16 MiB, 64 KiB chunks):
+    golden digests of buffers 0 and 63, fold == whole CRC for every buffer
+    (checksum of checksums), 10% random rewrite -> exactly those chunks dirty,
+    pack -> scatter into zeroed buffers -> digests identical."""
+    import json
+    import os
+    kat = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "kat.json")))
+    cs, nb, size = 65536, 64, 16 << 20
+    mem = pd.DeviceMemory(nb * size)
+    bufs = [pd.GpuBuffer(handle=i + 1, dev_ptr=mem.ptr + i * size, size=size) for i in range(nb)]
+    pd.fill_batch([(b.dev_ptr, size, 1000 + i) for i, b in enumerate(bufs)])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=512 << 20))
+    eng.register_buffers(bufs)
+    eng.hash_chunks()
+    eng.scan_dedup()
+    d = eng.digests().reshape(nb, 256)
+    for k, g in kat["c1_buffers"].items():
+        i = int(k)
+        assert f"{d[i, 0]:08x}" == g["chunk0"] and f"{d[i, 255]:08x}" == g["chunk255"]
+        assert f"{ocrc(orc, d[i].copy().view(np.uint8)):08x}" == g["digests_crc"]
+    crcs, _ = eng.buffer_crcs()
+    for i in range(nb):
+        assert crcs[i] == orc.or_fold_digests(d[i].copy().ctypes.data, size, cs)
+    assert f"{crcs[0]:08x}" == kat["c1_buffers"]["0"]["whole"]
+    assert f"{crcs[63]:08x}" == kat["c1_buffers"]["63"]["whole"]
+    eng.commit_epoch()
+    rng = np.random.default_rng(1)
+    dirty = rng.choice(nb * 256, 1638, replace=False)
+    pd.fill_batch([(bufs[g // 256].dev_ptr + (g % 256) * cs, cs, orc.or_mix64(1, int(g))) for g in dirty])
+    n = eng.plan_precopy()
+    flags = eng.flags()
+    assert set(np.nonzero(flags)[0]) == set(int(g) for g in dirty)
+    assert n == (64 + 32 * 1638 + 255) // 256 * 256 + 1638 * cs
+    before = eng.digests().copy()
+    cache_ptr, _ = eng.cache()
+    # zero the dirty chunks, scatter the pack back, re-hash: identical digests
+    for g in dirty:
+        pd.check(pd.lib().pos_memset(bufs[g // 256].dev_ptr + (g % 256) * cs, 0, cs, None))
+    pack = pd.DeviceMemory(n)
+    pd.check(pd.lib().pos_memcpy(pack.ptr, cache_ptr, n, 3, None))
+    eng.materialize(pack.ptr, n)
+    eng.hash_chunks()
+    assert np.array_equal(eng.digests(), before)
+    eng.close()
