@@ -333,9 +333,10 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         eng.event_record(5, copy)
         copy.synchronize()
         ckpt.synchronize()
-        if e2e:  # host image = the checkpoint target (captured_)
-            pd.apply_pack_host(pin.array[:nbytes], handles, host_image, threads=8)
-            pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=8)
+        # host image = the checkpoint target (captured_); inside the e2e wall
+        # clock, always outside the device-timed region
+        pd.apply_pack_host(pin.array[:nbytes], handles, host_image, threads=8)
+        pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=8)
         t1 = time.perf_counter()
         ms = eng.event_elapsed(0, 5)
         stw = eng.event_elapsed(3, 4)
@@ -383,12 +384,14 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     d2h_bytes = statistics.mean(r["precopy_bytes"] + r["delta_bytes"] for r in res)
     step_ms, stw_ms, e2e_ms = all_max(dist, [step_ms, stw_ms, e2e_ms], local)
 
-    # host-link peak: plain pinned D2H of 256 MiB (CUDA events)
-    eng.event_record(6, copy)
-    pd.check(pd.lib().pos_memcpy(pin.ptr, flush.ptr, min(flush.nbytes, pin.nbytes), D2H, int(copy)))
-    eng.event_record(7, copy)
-    link_ms = eng.event_elapsed(6, 7)
-    link_peak = min(flush.nbytes, pin.nbytes) / (link_ms * 1e-3) / 1e9
+    # host-link peak: best of 5 plain pinned D2H copies of 256 MiB (CUDA events)
+    link_n = min(flush.nbytes, pin.nbytes)
+    link_peak = 0.0
+    for _ in range(5):
+        eng.event_record(6, copy)
+        pd.check(pd.lib().pos_memcpy(pin.ptr, flush.ptr, link_n, D2H, int(copy)))
+        eng.event_record(7, copy)
+        link_peak = max(link_peak, link_n / (eng.event_elapsed(6, 7) * 1e-3) / 1e9)
     d2h_achieved = statistics.mean((r["precopy_bytes"] + r["delta_bytes"]) / (r["d2h_ms"] * 1e-3) / 1e9
                                    for r in res)
 
@@ -440,7 +443,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
             "host_link": {"bound": "pcie", "achieved": round(d2h_achieved, 2), "peak": round(link_peak, 2),
                           "unit": "GB/s", "frac": round(d2h_achieved / link_peak, 4),
-                          "peak_source": "pinned cudaMemcpyAsync D2H 256 MiB, measured in this run"},
+                          "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run"},
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
                           for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",

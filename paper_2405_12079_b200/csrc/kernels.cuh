@@ -269,9 +269,11 @@ __global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem + kRepTableBytes);
   const int lane = threadIdx.x & 31;
   const uint32_t lsel = (uint32_t)lane * 4;
+  // Item i goes to CTA i % grid, warp (i / grid) % 16: consecutive items land
+  // on different SMs, so a short list still spreads over the whole chip.
   const uint64_t nwarps = (uint64_t)gridDim.x * (kHashThreads / 32);
-  for (uint64_t it = (uint64_t)blockIdx.x * (kHashThreads / 32) + (threadIdx.x >> 5);
-       it < p.n_items; it += nwarps) {
+  for (uint64_t it = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < p.n_items;
+       it += nwarps) {
     uint64_t g, dst_off = 0;
     uint32_t entry = 0;
     if (COPY) {

@@ -188,10 +188,10 @@ struct pos_ctx {
     ck(cudaEventRecord(timers[t].b, s), "event");
     timers[t].used = true;
   }
+  // One CTA per SM (152 KiB of smem tables); items are dealt round-robin over
+  // CTAs first, so even a short list occupies every SM.
   int hash_grid(uint64_t items) const {
-    uint64_t warps = (items + 0) / 1;
-    uint64_t blocks = (warps + (kHashThreads / 32) - 1) / (kHashThreads / 32);
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)crc.sm_count));
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(items, (uint64_t)crc.sm_count));
   }
 };
 
