@@ -276,9 +276,33 @@ def cpu_reference_run(wl: Workload, steps: int, warmup: int, threads: int, sampl
 # ---------------------------------------------------------------------------
 # GPU arm
 
+def bind_numa_local(device: int) -> str:
+    """Pin this process to the CPUs local to the GPU (pinned host buffers are
+    then allocated on the GPU's NUMA node, the PCIe root it hangs off)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        bus = pynvml.nvmlDeviceGetPciInfo(h).busId
+        bus = bus.decode() if isinstance(bus, bytes) else bus
+        path = f"/sys/bus/pci/devices/{bus.lower()[-12:]}/local_cpulist"
+        if not os.path.exists(path):
+            path = f"/sys/bus/pci/devices/{bus.lower()}/local_cpulist"
+        spec = open(path).read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        os.sched_setaffinity(0, cpus)
+        return spec
+    except Exception as ex:  # not fatal: report it
+        return f"unbound ({type(ex).__name__})"
+
+
 def run_gpu(args, wl: Workload, world, rank, local, dist):
     import paper_2405_12079_b200 as pd
     from paper_2405_12079_b200.posdump import D2H
+    numa = bind_numa_local(local)
     pd.check(pd.lib().pos_set_device(local))
 
     total = wl.total
@@ -291,13 +315,21 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # produced on the device
     pd.fill_batch([(b.dev_ptr, b.size, 5000 + b.handle) for b in bufs])
     pd.device_synchronize()
-    for b in bufs:
-        if b.handle in wl.params:
-            b.upstream = pd.Upstream(pd.crc32(b.dev_ptr, b.size), True)
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0))
     eng.register_buffers(bufs)
+    if wl.params:  # note_h2d_provenance (process.hpp:505-522): Upstream.crc on device
+        eng.hash_chunks()
+        eng.scan_dedup()
+        crcs, _ = eng.buffer_crcs()
+        for b, c in zip(bufs, crcs):
+            if b.handle in wl.params:
+                b.upstream = pd.Upstream(int(c), True)
+                eng.update_buffer(b)
     cache_ptr, cache_cap = eng.cache()
-    pin = pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20)))
+    # Landing ring of pinned buffers: the host applies step e's packs out of
+    # one buffer while step e+1 DMA-writes the next (DMA into lines the CPU
+    # just read costs ~30% of the link).
+    pins = [pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20))) for _ in range(3)]
     host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
@@ -306,6 +338,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
 
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
     def checkpoint(e: int, e2e: bool):
+        pin = pins[e % len(pins)]
         for h, o, n, seed in wl.epoch_writes(e):  # untimed application iteration
             b = by_handle[h]
             pd.fill_bytes(b.dev_ptr + o, n, seed)
@@ -313,17 +346,25 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         pd.device_synchronize()
         window = wl.window(e)
         launches0 = eng.launches
+
+        def run_app():  # the application's own host thread submits the window
+            for k in window:
+                pd.fill_batch([(by_handle[h].dev_ptr, by_handle[h].size, s) for h, s in k], stream=app)
+            eng.event_record(2, app)
+
         t0 = time.perf_counter()
         eng.event_record(0, ckpt)
-        for k in window:  # app stream: pre-copy window kernels
-            pd.fill_batch([(by_handle[h].dev_ptr, by_handle[h].size, s) for h, s in k], stream=app)
-        eng.event_record(2, app)
+        app_thread = threading.Thread(target=run_app)
+        app_thread.start()
         nbytes = eng.plan_precopy(stream=ckpt, exclude_dag_dirty=True)
         eng.event_record(1, ckpt)
         copy.wait(ckpt)
         eng.d2h_async(pin.ptr, 0, nbytes, stream=copy)
+        eng.event_record(8, copy)
         # final stop: DAG write sets of the window -> dirty_set_, drain the app
+        app_thread.join()
         eng.record_dirty(sorted({h for k in window for h, _ in k}))
+        eng.prepare_final_stop(stream=ckpt)
         eng.stream_wait_event(2, ckpt)
         eng.event_record(3, ckpt)
         doff, dbytes = eng.at_final_stop(stream=ckpt)
@@ -335,8 +376,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         ckpt.synchronize()
         # host image = the checkpoint target (captured_); inside the e2e wall
         # clock, always outside the device-timed region
-        pd.apply_pack_host(pin.array[:nbytes], handles, host_image, threads=8)
-        pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=8)
+        if not args.no_host_apply:
+            pd.apply_pack_host(pin.array[:nbytes], handles, host_image, threads=8)
+            pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=8)
         t1 = time.perf_counter()
         ms = eng.event_elapsed(0, 5)
         stw = eng.event_elapsed(3, 4)
@@ -347,6 +389,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             except pd.SimError:
                 return 0.0
         hash_ms = kms("hash")
+        if args.trace:
+            marks = {"compacted": 1, "app_drained": 2, "stop": 3, "stw_end": 4, "precopy_d2h_end": 8, "end": 5}
+            print(json.dumps({k: round(eng.event_elapsed(0, v), 4) for k, v in marks.items()}), file=sys.stderr)
         r = {"ms": ms, "stw_ms": stw, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
              "precopy_bytes": nbytes, "delta_bytes": dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": eng.event_elapsed(1, 5), "compact_ms": kms("copy"),
@@ -374,7 +419,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         e += 1
     # verify the host image against the device (bit-exact)
     dev_bytes = mem.download()
-    ok = all(np.array_equal(img, dev_bytes[b.dev_ptr - mem.ptr:b.dev_ptr - mem.ptr + b.size])
+    ok = args.no_host_apply or all(np.array_equal(img, dev_bytes[b.dev_ptr - mem.ptr:b.dev_ptr - mem.ptr + b.size])
              for b, img in zip(bufs, host_image))
 
     step_ms = sum(r["ms"] for r in res) / len(res)
@@ -385,6 +430,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     step_ms, stw_ms, e2e_ms = all_max(dist, [step_ms, stw_ms, e2e_ms], local)
 
     # host-link peak: best of 5 plain pinned D2H copies of 256 MiB (CUDA events)
+    pin = pins[0]
     link_n = min(flush.nbytes, pin.nbytes)
     link_peak = 0.0
     for _ in range(5):
@@ -433,7 +479,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             "data": "synthetic",
             "config": {"workload": wl.desc, "chunk_size": CHUNK, "state_bytes_per_gpu": total,
                        "d2h_bytes_per_step": int(d2h_bytes), "parallelism": f"replicas{world}",
-                       "l2": "flushed between steps (256 MiB memset)",
+                       "l2": "flushed between steps (256 MiB memset)", "host_cpus": numa,
                        "value_counts": "checkpointed state bytes (incremental: only dirty chunks cross PCIe)"},
             "gpu_launches": int(statistics.mean(r["launches"] for r in res)),
             "roofline": {"bound": "hbm", "kernel": "k_hash_chunks", "achieved": round(achieved, 1),
@@ -484,6 +530,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c1", "c2"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
+    ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

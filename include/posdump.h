@@ -144,6 +144,11 @@ int pos_compact(pos_ctx* ctx, int exclude_dag_dirty, void* stream, uint64_t* pac
  * *pack_offset (256-B aligned, after the pre-copy pack), refreshing their
  * digests.  Asynchronous on `stream`. */
 int pos_delta_copy(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes);
+/* Stage the delta pack's header and work list ahead of the stop (the DAG
+ * write sets are known at submission, process.hpp:313-344), so the STW window
+ * holds only the kernel.  pos_delta_copy re-stages if dirty_set_ or the
+ * pre-copy pack changed since. */
+int pos_delta_prepare(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes);
 
 /* ---- host leg ------------------------------------------------------------- */
 /* Pinned D2H of cache[offset, offset+bytes) into host_dst, on `stream`, in

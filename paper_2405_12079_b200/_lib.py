@@ -109,6 +109,7 @@ SIGNATURES = {
     "pos_clear_dirty": [P],
     "pos_compact": [P, I32, P, PU64],
     "pos_delta_copy": [P, P, PU64, PU64],
+    "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],
     "pos_cache_info": [P, PU64, PU64],
     "pos_scatter": [P, U64, U64, P],

@@ -31,7 +31,8 @@ struct DevBuf {              // one registered allocation (GpuBuffer, buffer.hpp
   uint32_t x8_tail;          // x^(8 * last chunk length) mod P
   uint32_t flags;            // kBuf* bits
   uint32_t upstream_crc;     // Upstream::crc
-  uint32_t pad[3];
+  uint32_t x8_lastseg;       // x^(8 * length of the tail chunk's last segment)
+  uint32_t pad[2];
 };
 static_assert(sizeof(DevBuf) == 64, "DevBuf layout");
 
@@ -73,12 +74,20 @@ struct HashParams {
   const uint4* work;         // {g, entry, dst_off lo, dst_off hi}
   uint8_t* pack;             // pack base
   uint64_t payload_off;      // payload offset within the pack
+  // Segmented chunks (nseg > 1): warp unit = (item, segment of seg_bytes);
+  // the last segment to finish folds the segment registers.
+  uint32_t nseg;
+  uint32_t seg_bytes;
+  const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
+  uint32_t* seg_raw;         // [n_chunks * nseg]
+  uint32_t* seg_cnt;         // [n_chunks], zero between launches
 };
 
 // Hash kernel geometry.
 constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
 constexpr int kStepBytes = 512;              // one warp step: 32 lanes x 16 B
 constexpr int kUnroll = 8;                   // warp steps per batch (4 KiB per warp)
+constexpr int kPrefetchSteps = 32;           // L2 bulk-prefetch distance (16 KiB per warp)
 constexpr uint32_t kRepTableBytes = 131072;  // lane-replicated Z^512: 4 x 256 x 32 lanes x 4 B
 constexpr uint32_t kSmallTablesBytes = 6 * 4096;
 constexpr uint32_t kHashSmem = kRepTableBytes + kSmallTablesBytes;
@@ -92,6 +101,11 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
+}
+
+// TMA bulk prefetch of [p, p+bytes) into L2 (16-B aligned, bytes % 16 == 0).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
@@ -181,32 +195,53 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
     blk = 1;
   }
   const uint64_t full_end = nblk - 1;  // steps [blk, full_end) are fully inside
-  // Software-pipelined batches of kUnroll steps (4 KiB per warp in flight,
-  // plus the next batch's loads issued before this batch's lookups).
+  // Software-pipelined batches of kUnroll steps, ping-ponging between two
+  // register buffers (the next batch's loads are in flight while this batch's
+  // lookups run), plus a TMA bulk prefetch into L2 kPrefetchSteps ahead so the
+  // LDGs mostly hit L2.
+  auto prefetch = [&](uint64_t from_blk) {
+    if (lane == 0 && from_blk * kStepBytes < end) {
+      uint64_t lo = from_blk * kStepBytes;
+      uint64_t hi = (from_blk + kUnroll) * kStepBytes;
+      hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
+      if (hi > lo) l2_prefetch(reinterpret_cast<const void*>(a0 + lo), (uint32_t)(hi - lo));
+    }
+  };
+  auto load_batch = [&](uint4 (&buf)[kUnroll], uint64_t at) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) buf[u] = ldg_stream(base + (at + u) * 32);
+  };
+  auto run_batch = [&](const uint4 (&buf)[kUnroll], uint64_t at) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (vec_copy) stg_stream(dbase + (at + u) * 32, buf[u]);
+      c0 = adv512(rep, lsel, c0 ^ buf[u].x);
+      c1 = adv512(rep, lsel, c1 ^ buf[u].y);
+      c2 = adv512(rep, lsel, c2 ^ buf[u].z);
+      c3 = adv512(rep, lsel, c3 ^ buf[u].w);
+    }
+  };
+  if (lane == 0) {  // head of the chunk
+    uint64_t hi = (uint64_t)kPrefetchSteps * kStepBytes;
+    hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
+    if (hi) l2_prefetch(reinterpret_cast<const void*>(a0), (uint32_t)hi);
+  }
   if (blk + kUnroll <= full_end) {
-    uint4 cur[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) cur[u] = ldg_stream(base + (blk + u) * 32);
+    uint4 bufA[kUnroll], bufB[kUnroll];
+    load_batch(bufA, blk);
     for (;;) {
-      const uint64_t nxt_blk = blk + kUnroll;
-      const bool more = nxt_blk + kUnroll <= full_end;
-      uint4 nxt[kUnroll];
-      if (more) {
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) nxt[u] = ldg_stream(base + (nxt_blk + u) * 32);
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (vec_copy) stg_stream(dbase + (blk + u) * 32, cur[u]);
-        c0 = adv512(rep, lsel, c0 ^ cur[u].x);
-        c1 = adv512(rep, lsel, c1 ^ cur[u].y);
-        c2 = adv512(rep, lsel, c2 ^ cur[u].z);
-        c3 = adv512(rep, lsel, c3 ^ cur[u].w);
-      }
-      blk = nxt_blk;
-      if (!more) break;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) cur[u] = nxt[u];
+      const bool moreB = blk + 2 * kUnroll <= full_end;
+      if (moreB) load_batch(bufB, blk + kUnroll);
+      prefetch(blk + kPrefetchSteps);
+      run_batch(bufA, blk);
+      blk += kUnroll;
+      if (!moreB) break;
+      const bool moreA = blk + 2 * kUnroll <= full_end;
+      if (moreA) load_batch(bufA, blk + kUnroll);
+      prefetch(blk + kPrefetchSteps);
+      run_batch(bufB, blk);
+      blk += kUnroll;
+      if (!moreA) break;
     }
   }
   for (; blk < full_end; ++blk) {
@@ -272,17 +307,20 @@ __global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
   // Item i goes to CTA i % grid, warp (i / grid) % 16: consecutive items land
   // on different SMs, so a short list still spreads over the whole chip.
   const uint64_t nwarps = (uint64_t)gridDim.x * (kHashThreads / 32);
-  for (uint64_t it = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < p.n_items;
+  const uint64_t n_units = p.n_items * p.nseg;
+  for (uint64_t it = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < n_units;
        it += nwarps) {
+    const uint64_t item = p.nseg == 1 ? it : it / p.nseg;
+    const uint32_t seg = p.nseg == 1 ? 0u : (uint32_t)(it % p.nseg);
     uint64_t g, dst_off = 0;
     uint32_t entry = 0;
     if (COPY) {
-      uint4 w = p.work[it];
+      uint4 w = p.work[item];
       g = w.x;
       entry = w.y;
       dst_off = (uint64_t)w.z | ((uint64_t)w.w << 32);
     } else {
-      g = it;
+      g = item;
     }
     const uint2 cm = p.chunk_map[g];
     const DevBuf& b = p.bufs[cm.x];
@@ -291,7 +329,40 @@ __global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
     const uint64_t len = last ? b.size - start : p.chunk_size;
     const uint32_t k_len = last ? b.k_tail : p.k_full;
     uint8_t* dst = COPY ? p.pack + p.payload_off + dst_off : nullptr;
-    uint32_t crc = warp_crc32<COPY>(rep, small, p.xinv, lsel, lane, b.ptr + start, len, k_len, dst);
+    uint32_t crc;
+    // Whole chunk (nseg == 1), or this warp's segment: raw register (init 0)
+    // at the segment end.
+    const uint64_t lo = (uint64_t)seg * p.seg_bytes;
+    const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
+    const uint32_t r = n ? warp_crc32<COPY>(rep, small, p.xinv, lsel, lane, b.ptr + start + lo, n,
+                                            p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
+                         : 0u;
+    if (p.nseg == 1) {
+      crc = r;
+    } else {
+      const uint32_t raw = r;
+      uint32_t old = 0;
+      if (lane == 31) {
+        p.seg_raw[g * p.nseg + seg] = raw;
+        __threadfence();
+        old = atomicAdd(p.seg_cnt + g, 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 31);
+      if (old != p.nseg - 1) continue;  // not the last segment of this chunk
+      __threadfence();
+      // raw(chunk) = XOR_s Z^(len - end_s)(raw_s); segments past the tail are empty.
+      const uint32_t m = (uint32_t)((len - 1) / p.seg_bytes);  // last non-empty segment
+      const uint32_t xl = len == p.chunk_size ? p.xseg[1] : b.x8_lastseg;
+      uint32_t v = 0;
+      if ((uint32_t)lane <= m) {
+        v = __ldcg(p.seg_raw + g * p.nseg + lane);
+        if ((uint32_t)lane < m) v = multmodp(p.xseg[m - 1 - lane], multmodp(xl, v));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+      crc = v ^ k_len;
+      if (lane == 31) p.seg_cnt[g] = 0;
+    }
     if (lane == 31) {
       p.digest_cur[g] = crc;
       if (COPY) {

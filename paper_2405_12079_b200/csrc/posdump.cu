@@ -164,8 +164,16 @@ struct pos_ctx {
   DevArray<uint8_t> d_verdict;
   DevArray<uint8_t> d_dag_dirty;
   DevArray<uint32_t> d_tcs;  // Z^chunk_size
+  // chunk segmentation (parallelism for short chunk lists)
+  uint32_t nseg = 1, seg_bytes = 0;
+  DevArray<uint32_t> d_xseg, d_seg_raw, d_seg_cnt;
   std::set<uint64_t> dirty_set;
   bool dag_uploaded = false;
+  uint64_t dirty_version = 0;
+  // STW delta staged ahead of the stop (pos_delta_prepare)
+  bool delta_ready = false;
+  uint64_t delta_version = 0, delta_precopy = 0, delta_n = 0, delta_offset = 0, delta_total = 0,
+           delta_payload_off = 0;
   // O3 cache
   DevArray<uint8_t> cache;
   uint64_t cache_cap = 0;
@@ -325,6 +333,9 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_verdict.release();
   c->d_dag_dirty.release();
   c->d_tcs.release();
+  c->d_xseg.release();
+  c->d_seg_raw.release();
+  c->d_seg_cnt.release();
   c->cache.release();
   c->d_items.release();
   c->d_scan.release();
@@ -382,6 +393,30 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
     }
     if (g > 0xFFFFFFFFull) fail(POS_E_INVALID_ARGUMENT, "more than 2^32 chunks");
     c->n_chunks = g;
+    // Split chunks into segments when there are too few chunks to give every
+    // warp of the grid several units (>= 16 KiB per segment, power of 2).
+    {
+      const uint64_t warps = (uint64_t)c->crc.sm_count * (kHashThreads / 32);
+      uint32_t nseg = 1;
+      while (nseg < 32 && g * nseg < 4 * warps && cs % (2ull * nseg * kStepBytes) == 0 &&
+             cs / (2ull * nseg) >= 16384)
+        nseg *= 2;
+      c->nseg = nseg;
+      c->seg_bytes = (uint32_t)(cs / nseg);
+      std::vector<uint32_t> xs(32);
+      for (int k = 0; k < 32; ++k) xs[k] = x8nmodp((uint64_t)k * c->seg_bytes);
+      c->d_xseg.ensure(32);
+      ck(cudaMemcpy(c->d_xseg.p, xs.data(), 32 * 4, cudaMemcpyHostToDevice), "xseg");
+      for (uint32_t i = 0; i < n; ++i) {
+        DevBuf& b = c->hbufs[i];
+        uint64_t tail = b.size - (uint64_t)(b.nchunks - 1) * cs;
+        uint64_t m = (tail - 1) / c->seg_bytes;
+        b.x8_lastseg = x8nmodp(tail - m * c->seg_bytes);
+      }
+      c->d_seg_raw.ensure(std::max<uint64_t>(g, 1) * nseg);
+      c->d_seg_cnt.ensure(std::max<uint64_t>(g, 1));
+      ck(cudaMemset(c->d_seg_cnt.p, 0, std::max<uint64_t>(g, 1) * 4), "memset");
+    }
     std::vector<uint2> cmap(g);
     for (uint32_t i = 0; i < n; ++i)
       for (uint32_t k = 0; k < c->hbufs[i].nchunks; ++k) cmap[c->chunk_base[i] + k] = make_uint2(i, k);
@@ -405,6 +440,8 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
     c->epoch = 0;
     c->dirty_set.clear();
     c->dag_uploaded = false;
+    ++c->dirty_version;
+    c->delta_ready = false;
     c->precopy_bytes = 0;
   });
 }
@@ -453,7 +490,12 @@ int pos_hash_chunks(pos_ctx* c, void* stream) {
     p.flags = c->d_flags.p;
     p.bitmap = c->d_bitmap.p;
     p.prev_valid = c->prev_valid ? 1 : 0;
-    int grid = c->hash_grid(c->n_chunks);
+    p.nseg = c->nseg;
+    p.seg_bytes = c->seg_bytes;
+    p.xseg = c->d_xseg.p;
+    p.seg_raw = c->d_seg_raw.p;
+    p.seg_cnt = c->d_seg_cnt.p;
+    int grid = c->hash_grid(c->n_chunks * c->nseg);
     c->timer_begin(kTimHash, s);
     k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);
     check_launch("k_hash_chunks");
@@ -470,6 +512,8 @@ int pos_commit_epoch(pos_ctx* c) {
     ++c->epoch;
     c->dirty_set.clear();
     c->dag_uploaded = false;
+    ++c->dirty_version;
+    c->delta_ready = false;
     c->precopy_bytes = 0;
   });
 }
@@ -531,7 +575,10 @@ int pos_record_dirty(pos_ctx* c, const uint64_t* handles, uint32_t n) {
     if (!c || (!handles && n)) fail(POS_E_INVALID_ARGUMENT, "null argument");
     for (uint32_t i = 0; i < n; ++i) {
       if (!c->index_of.count(handles[i])) continue;  // not in the snapshot (cr.hpp:904)
-      if (c->dirty_set.insert(handles[i]).second) c->dag_uploaded = false;
+      if (c->dirty_set.insert(handles[i]).second) {
+        c->dag_uploaded = false;
+        ++c->dirty_version;
+      }
     }
   });
 }
@@ -541,6 +588,7 @@ int pos_clear_dirty(pos_ctx* c) {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
     c->dirty_set.clear();
     c->dag_uploaded = false;
+    ++c->dirty_version;
   });
 }
 
@@ -578,59 +626,84 @@ int pos_compact(pos_ctx* c, int exclude_dag_dirty, void* stream, uint64_t* pack_
   });
 }
 
+static void delta_prepare(pos_ctx* c, cudaStream_t s) {
+  const uint64_t cs = c->cfg.chunk_size;
+  // at_final_stop: every buffer of dirty_set_ in the snapshot, ascending handle.
+  std::vector<uint4> work;
+  uint64_t payload = 0;
+  uint32_t entry = 0;
+  for (uint64_t h : c->dirty_set) {
+    uint32_t i = c->index_of.at(h);
+    const DevBuf& b = c->hbufs[i];
+    for (uint32_t k = 0; k < b.nchunks; ++k) {
+      uint64_t len = k + 1 == b.nchunks ? b.size - (uint64_t)k * cs : cs;
+      uint64_t g = c->chunk_base[i] + k;
+      work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
+      payload += round_up(len, 16);
+    }
+  }
+  const uint64_t n = work.size();
+  const uint64_t payload_off = round_up(kPackHeader + kPackEntry * n, kPackAlign);
+  const uint64_t total = payload_off + payload;
+  const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
+  if (offset + total > c->cache_cap) fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
+  // Stage the header (+ zero gap up to the payload) and the work list.
+  const uint64_t hdr_bytes = payload_off;
+  const uint64_t work_bytes = n * sizeof(uint4);
+  if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
+  c->h_stage.ensure(hdr_bytes + work_bytes);
+  uint8_t* st = c->h_stage.p;
+  std::memset(st, 0, kPackHeader);
+  uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)n, flags = 1;
+  std::memcpy(st + 0, &magic, 4);
+  std::memcpy(st + 4, &ver, 4);
+  std::memcpy(st + 8, &cs, 8);
+  std::memcpy(st + 16, &nn, 4);
+  std::memcpy(st + 20, &flags, 4);
+  std::memcpy(st + 24, &payload_off, 8);
+  std::memcpy(st + 32, &payload, 8);
+  std::memcpy(st + 40, &c->epoch, 8);
+  std::memcpy(st + 48, &total, 8);
+  if (n) std::memcpy(st + hdr_bytes, work.data(), work_bytes);
+  uint8_t* pack = c->cache.p + offset;
+  // Only the header and the entry gap go up; the kernel writes the entries.
+  ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
+  if (hdr_bytes > kPackHeader + kPackEntry * n)
+    ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0, hdr_bytes - kPackHeader - kPackEntry * n, s),
+       "gap");
+  if (n) ck(cudaMemcpyAsync(c->d_work.p, st + hdr_bytes, work_bytes, cudaMemcpyHostToDevice, s), "work");
+  ck(cudaEventRecord(c->stage_free, s), "event");
+  c->delta_ready = true;
+  c->delta_version = c->dirty_version;
+  c->delta_precopy = c->precopy_bytes;
+  c->delta_n = n;
+  c->delta_offset = offset;
+  c->delta_total = total;
+  c->delta_payload_off = payload_off;
+}
+
+static bool delta_current(const pos_ctx* c) {
+  return c->delta_ready && c->delta_version == c->dirty_version && c->delta_precopy == c->precopy_bytes;
+}
+
+int pos_delta_prepare(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    delta_prepare(c, S(stream));
+    if (pack_offset) *pack_offset = c->delta_offset;
+    if (pack_bytes) *pack_bytes = c->delta_total;
+  });
+}
+
 int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     cudaStream_t s = S(stream);
-    const uint64_t cs = c->cfg.chunk_size;
-    // at_final_stop: every buffer of dirty_set_ in the snapshot, ascending handle.
-    std::vector<uint4> work;
-    uint64_t payload = 0;
-    uint32_t entry = 0;
-    for (uint64_t h : c->dirty_set) {
-      uint32_t i = c->index_of.at(h);
-      const DevBuf& b = c->hbufs[i];
-      for (uint32_t k = 0; k < b.nchunks; ++k) {
-        uint64_t len = k + 1 == b.nchunks ? b.size - (uint64_t)k * cs : cs;
-        uint64_t g = c->chunk_base[i] + k;
-        work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
-        payload += round_up(len, 16);
-      }
-    }
-    const uint64_t n = work.size();
-    const uint64_t payload_off = round_up(kPackHeader + kPackEntry * n, kPackAlign);
-    const uint64_t total = payload_off + payload;
-    const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
-    if (offset + total > c->cache_cap)
-      fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
-    // Stage header (+ zero gap up to the payload) and the work list.
-    const uint64_t hdr_bytes = payload_off;
-    const uint64_t work_bytes = n * sizeof(uint4);
-    if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
-    c->h_stage.ensure(hdr_bytes + work_bytes);
-    uint8_t* st = c->h_stage.p;
-    std::memset(st, 0, hdr_bytes);
-    uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)n, flags = 1;
-    std::memcpy(st + 0, &magic, 4);
-    std::memcpy(st + 4, &ver, 4);
-    std::memcpy(st + 8, &cs, 8);
-    std::memcpy(st + 16, &nn, 4);
-    std::memcpy(st + 20, &flags, 4);
-    std::memcpy(st + 24, &payload_off, 8);
-    std::memcpy(st + 32, &payload, 8);
-    std::memcpy(st + 40, &c->epoch, 8);
-    std::memcpy(st + 48, &total, 8);
-    if (n) std::memcpy(st + hdr_bytes, work.data(), work_bytes);
-    uint8_t* pack = c->cache.p + offset;
-    // Only the header and the entry gap go up; the kernel writes the entries.
-    ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
-    if (hdr_bytes > kPackHeader + kPackEntry * n)
-      ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0,
-                         hdr_bytes - kPackHeader - kPackEntry * n, s),
-         "gap");
-    if (n) ck(cudaMemcpyAsync(c->d_work.p, st + hdr_bytes, work_bytes, cudaMemcpyHostToDevice, s), "work");
-    ck(cudaEventRecord(c->stage_free, s), "event");
+    if (!delta_current(c)) delta_prepare(c, s);
+    c->delta_ready = false;  // one launch per preparation
+    const uint64_t n = c->delta_n, cs = c->cfg.chunk_size;
     if (n) {
       HashParams p{};
       p.bufs = c->d_bufs.p;
@@ -642,17 +715,22 @@ int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pa
       p.xinv = c->crc.xinv.p;
       p.digest_cur = c->d_digest[c->cur].p;
       p.work = c->d_work.p;
-      p.pack = pack;
-      p.payload_off = payload_off;
-      int grid = c->hash_grid(n);
+      p.pack = c->cache.p + c->delta_offset;
+      p.payload_off = c->delta_payload_off;
+      p.nseg = c->nseg;
+      p.seg_bytes = c->seg_bytes;
+      p.xseg = c->d_xseg.p;
+      p.seg_raw = c->d_seg_raw.p;
+      p.seg_cnt = c->d_seg_cnt.p;
+      int grid = c->hash_grid(n * c->nseg);
       c->timer_begin(kTimDelta, s);
       k_hash_chunks<true><<<grid, kHashThreads, kHashSmem, s>>>(p);
       check_launch("k_hash_chunks<copy>");
       c->timer_end(kTimDelta, s);
       ++c->launches;
     }
-    if (pack_offset) *pack_offset = offset;
-    if (pack_bytes) *pack_bytes = total;
+    if (pack_offset) *pack_offset = c->delta_offset;
+    if (pack_bytes) *pack_bytes = c->delta_total;
   });
 }
 
@@ -787,6 +865,8 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
       p.digest_prev = dd.p;
       p.flags = nullptr;  // digests only
       p.bitmap = nullptr;
+      p.nseg = 1;
+      p.seg_bytes = (uint32_t)cs;
       uint64_t blocks = (nc + 15) / 16;
       int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)t.sm_count));
       k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);

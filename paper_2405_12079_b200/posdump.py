@@ -346,6 +346,12 @@ class DumpEngine:
         check(lib().pos_delta_copy(self.ctx, _s(stream), C.byref(off), C.byref(n)))
         return off.value, n.value
 
+    def prepare_final_stop(self, stream=None) -> tuple[int, int]:
+        """Stage the delta pack layout before the stop (pos_delta_prepare)."""
+        off, n = C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_delta_prepare(self.ctx, _s(stream), C.byref(off), C.byref(n)))
+        return off.value, n.value
+
     # ---- host leg
     def d2h_async(self, host_ptr: int, offset: int, nbytes: int, stream=None, slice_bytes: int = 0) -> None:
         check(lib().pos_d2h_async(self.ctx, host_ptr, offset, nbytes, slice_bytes, _s(stream)))

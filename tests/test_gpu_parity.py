@@ -148,9 +148,9 @@ def test_chunk_digests_and_epoch_bitmap(orc, cs):
     eng.close()
 
 
-def test_unaligned_buffers(orc):
-    cs = 4096
-    p = Proc(orc, [5000, 12345, 3], offsets=[1, 7, 13])
+@pytest.mark.parametrize("cs", [4096, 65536])
+def test_unaligned_buffers(orc, cs):
+    p = Proc(orc, [5000, 12345, 3, 3 * cs + 77], offsets=[1, 7, 13, 5])
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
     eng.register_buffers(p.bufs)
     n = eng.plan_precopy()
@@ -240,18 +240,20 @@ def test_compact_pack_is_bit_exact(orc, cs):
     eng.close()
 
 
-def test_delta_copy_pack_and_digests(orc):
+@pytest.mark.parametrize("cs,offsets", [(4096, None), (65536, None), (65536, [0, 3, 0, 9])])
+def test_delta_copy_pack_and_digests(orc, cs, offsets):
     """at_final_stop (cr.hpp:599-621): whole DAG-flagged buffers, after the
     pre-copy pack, ascending handle; digests refreshed from what was copied."""
-    cs = 4096
-    sizes = [3 * cs, 5000, 100, 2 * cs]
-    p = Proc(orc, sizes, seed0=700, handles=[2, 4, 6, 8])
+    sizes = [3 * cs, 5000, 100, 2 * cs + 33]
+    p = Proc(orc, sizes, seed0=700, handles=[2, 4, 6, 8], offsets=offsets)
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
     eng.register_buffers(p.bufs)
     n0 = eng.plan_precopy()
     eng.record_dirty([8, 4])
     p.write(1, 10, 4000, 31)   # the app writes while the pre-copy drains
     p.write(3, 0, 2 * cs, 32)
+    pd.device_synchronize()
+    assert eng.prepare_final_stop() == eng.prepare_final_stop()  # idempotent staging
     pd.device_synchronize()
     off, n1 = eng.at_final_stop()
     assert off == (n0 + 255) // 256 * 256
