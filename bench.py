@@ -354,16 +354,20 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
 
         t0 = time.perf_counter()
         eng.event_record(0, ckpt)
+        # The window's kernels are in the DAG from submission (their spec write
+        # sets, process.hpp:313-344): their buffers are left to the STW pass,
+        # as record_dirty's copy cancellation does (cr.hpp:909-918).
+        eng.record_dirty(sorted({h for k in window for h, _ in k}))
+        eng.launch_precopy(stream=ckpt, exclude_dag_dirty=True)  # async: hash..compact
         app_thread = threading.Thread(target=run_app)
         app_thread.start()
-        nbytes = eng.plan_precopy(stream=ckpt, exclude_dag_dirty=True)
+        nbytes = eng.precopy_size()
         eng.event_record(1, ckpt)
         copy.wait(ckpt)
         eng.d2h_async(pin.ptr, 0, nbytes, stream=copy)
         eng.event_record(8, copy)
         # final stop: DAG write sets of the window -> dirty_set_, drain the app
         app_thread.join()
-        eng.record_dirty(sorted({h for k in window for h, _ in k}))
         eng.prepare_final_stop(stream=ckpt)
         eng.stream_wait_event(2, ckpt)
         eng.event_record(3, ckpt)

@@ -137,6 +137,12 @@ int pos_clear_dirty(pos_ctx* ctx);
  * Synchronises `stream` once to learn the pack size; the copy itself is left
  * running on `stream`.  POS_E_STAGING_EXHAUSTED if it does not fit. */
 int pos_compact(pos_ctx* ctx, int exclude_dag_dirty, void* stream, uint64_t* pack_bytes);
+/* The whole pre-copy, asynchronous (plan_precopy, cr.hpp:377-406):
+ * pos_hash_chunks + pos_buffer_crc + scan + compaction, with the copy
+ * kernel's item count read on the device -- no host round trip.  The pack
+ * size becomes available through pos_precopy_size (waits for the scan only). */
+int pos_precopy(pos_ctx* ctx, int exclude_dag_dirty, void* stream);
+int pos_precopy_size(pos_ctx* ctx, uint64_t* pack_bytes);
 
 /* ---- STW delta-copy --------------------------------------------------- */
 /* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is

@@ -108,6 +108,8 @@ SIGNATURES = {
     "pos_record_dirty": [P, P, U32],
     "pos_clear_dirty": [P],
     "pos_compact": [P, I32, P, PU64],
+    "pos_precopy": [P, I32, P],
+    "pos_precopy_size": [P, PU64],
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],

@@ -31,8 +31,7 @@ struct DevBuf {              // one registered allocation (GpuBuffer, buffer.hpp
   uint32_t x8_tail;          // x^(8 * last chunk length) mod P
   uint32_t flags;            // kBuf* bits
   uint32_t upstream_crc;     // Upstream::crc
-  uint32_t x8_lastseg;       // x^(8 * length of the tail chunk's last segment)
-  uint32_t pad[2];
+  uint32_t pad[3];
 };
 static_assert(sizeof(DevBuf) == 64, "DevBuf layout");
 
@@ -79,6 +78,7 @@ struct HashParams {
   uint32_t nseg;
   uint32_t seg_bytes;
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
+  const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
   uint32_t* seg_raw;         // [n_chunks * nseg]
   uint32_t* seg_cnt;         // [n_chunks], zero between launches
 };
@@ -86,11 +86,19 @@ struct HashParams {
 // Hash kernel geometry.
 constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
 constexpr int kStepBytes = 512;              // one warp step: 32 lanes x 16 B
-constexpr int kUnroll = 8;                   // warp steps per batch (4 KiB per warp)
+constexpr int kUnrollDefault = 8;            // warp steps per batch (4 KiB per warp)
 constexpr int kPrefetchSteps = 32;           // L2 bulk-prefetch distance (16 KiB per warp)
+// Measured (tools/read_micro.cu): the bulk L2 prefetch lifts a lone warp from
+// 9.2 to 11.6 GB/s but costs ~4% when every warp streams, so it is off.
+constexpr bool kL2Prefetch = false;
 constexpr uint32_t kRepTableBytes = 131072;  // lane-replicated Z^512: 4 x 256 x 32 lanes x 4 B
 constexpr uint32_t kSmallTablesBytes = 6 * 4096;
-constexpr uint32_t kHashSmem = kRepTableBytes + kSmallTablesBytes;
+// The replicated table sits at ABSOLUTE shared address 0x10000, so the PRMT
+// that extracts a state byte also supplies the table base (byte 2 = 1) and no
+// per-lookup add is needed; the small tables sit at the start of the dynamic
+// window (which begins at the ~1 KiB reserved offset).
+constexpr uint32_t kRepAbs = 0x10000;
+constexpr uint32_t kHashSmem = 0x30000;
 
 // ---------------------------------------------------------------------------
 // Load helpers.
@@ -145,17 +153,20 @@ __device__ __forceinline__ uint4 load_masked(uint64_t a0, uint64_t blk, int lane
 // own bank (conflict-free LDS) and one PRMT builds the address:
 // __byte_perm(x, lane*4, 0x55k4) = lane*4 + byte_k(x)*256.
 
-__device__ __forceinline__ uint32_t lds_u32(const uint8_t* smem, uint32_t off) {
-  return *reinterpret_cast<const uint32_t*>(smem + off);
+template <int IMM>
+__device__ __forceinline__ uint32_t lds_abs(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(IMM));
+  return v;
 }
 
-__device__ __forceinline__ uint32_t adv512(const uint8_t* rep, uint32_t lsel, uint32_t x) {
-  uint32_t o0 = __byte_perm(x, lsel, 0x5504);
-  uint32_t o1 = __byte_perm(x, lsel, 0x5514);
-  uint32_t o2 = __byte_perm(x, lsel, 0x5524);
-  uint32_t o3 = __byte_perm(x, lsel, 0x5534);
-  return lds_u32(rep, o0) ^ lds_u32(rep, o1 + 128) ^ lds_u32(rep, o2 + 65536) ^
-         lds_u32(rep, o3 + 65536 + 128);
+// lsel = lane*4 | kRepAbs: __byte_perm(x, lsel, 0x76k4) = kRepAbs + byte_k(x)*256 + lane*4.
+__device__ __forceinline__ uint32_t adv512(uint32_t lsel, uint32_t x) {
+  uint32_t o0 = __byte_perm(x, lsel, 0x7604);
+  uint32_t o1 = __byte_perm(x, lsel, 0x7614);
+  uint32_t o2 = __byte_perm(x, lsel, 0x7624);
+  uint32_t o3 = __byte_perm(x, lsel, 0x7634);
+  return lds_abs<0>(o0) ^ lds_abs<128>(o1) ^ lds_abs<65536>(o2) ^ lds_abs<65536 + 128>(o3);
 }
 
 __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
@@ -171,8 +182,8 @@ __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
 // with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
 // which leaves a register that starts at 0 unchanged.  COPY: every loaded
 // vector is also stored at dst (only when src is 16-B aligned).
-template <bool COPY>
-__device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_t* small,
+template <bool COPY, int kUnroll>
+__device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
                                                const uint32_t* xinv, uint32_t lsel, int lane,
                                                uint64_t src, uint64_t len, uint32_t k_len,
                                                uint8_t* dst) {
@@ -188,10 +199,10 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
   uint64_t blk = 0;
   if (lead != 0 && nblk > 1) {  // first step straddles the aligned base
     uint4 v = load_masked(a0, 0, lane, lead, end);
-    c0 = adv512(rep, lsel, c0 ^ v.x);
-    c1 = adv512(rep, lsel, c1 ^ v.y);
-    c2 = adv512(rep, lsel, c2 ^ v.z);
-    c3 = adv512(rep, lsel, c3 ^ v.w);
+    c0 = adv512(lsel, c0 ^ v.x);
+    c1 = adv512(lsel, c1 ^ v.y);
+    c2 = adv512(lsel, c2 ^ v.z);
+    c3 = adv512(lsel, c3 ^ v.w);
     blk = 1;
   }
   const uint64_t full_end = nblk - 1;  // steps [blk, full_end) are fully inside
@@ -200,7 +211,7 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
   // lookups run), plus a TMA bulk prefetch into L2 kPrefetchSteps ahead so the
   // LDGs mostly hit L2.
   auto prefetch = [&](uint64_t from_blk) {
-    if (lane == 0 && from_blk * kStepBytes < end) {
+    if (kL2Prefetch && lane == 0 && from_blk * kStepBytes < end) {
       uint64_t lo = from_blk * kStepBytes;
       uint64_t hi = (from_blk + kUnroll) * kStepBytes;
       hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
@@ -215,13 +226,13 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (vec_copy) stg_stream(dbase + (at + u) * 32, buf[u]);
-      c0 = adv512(rep, lsel, c0 ^ buf[u].x);
-      c1 = adv512(rep, lsel, c1 ^ buf[u].y);
-      c2 = adv512(rep, lsel, c2 ^ buf[u].z);
-      c3 = adv512(rep, lsel, c3 ^ buf[u].w);
+      c0 = adv512(lsel, c0 ^ buf[u].x);
+      c1 = adv512(lsel, c1 ^ buf[u].y);
+      c2 = adv512(lsel, c2 ^ buf[u].z);
+      c3 = adv512(lsel, c3 ^ buf[u].w);
     }
   };
-  if (lane == 0) {  // head of the chunk
+  if (kL2Prefetch && lane == 0) {  // head of the chunk
     uint64_t hi = (uint64_t)kPrefetchSteps * kStepBytes;
     hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
     if (hi) l2_prefetch(reinterpret_cast<const void*>(a0), (uint32_t)hi);
@@ -247,10 +258,10 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
   for (; blk < full_end; ++blk) {
     uint4 v = ldg_stream(base + blk * 32);
     if (vec_copy) stg_stream(dbase + blk * 32, v);
-    c0 = adv512(rep, lsel, c0 ^ v.x);
-    c1 = adv512(rep, lsel, c1 ^ v.y);
-    c2 = adv512(rep, lsel, c2 ^ v.z);
-    c3 = adv512(rep, lsel, c3 ^ v.w);
+    c0 = adv512(lsel, c0 ^ v.x);
+    c1 = adv512(lsel, c1 ^ v.y);
+    c2 = adv512(lsel, c2 ^ v.z);
+    c3 = adv512(lsel, c3 ^ v.w);
   }
   // Last (partial) step: bytes past `end` read as zero.
   uint4 v = load_masked(a0, full_end, lane, lead, end);
@@ -285,28 +296,30 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* rep, const uint32_
 }
 
 __device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* tables) {
-  uint32_t* s32 = reinterpret_cast<uint32_t*>(smem);
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if (sbase + kSmallTablesBytes > kRepAbs) __trap();  // layout assumption (reserved smem < 40 KiB)
+  uint32_t* rep = reinterpret_cast<uint32_t*>(smem + (kRepAbs - sbase));
   for (int i = threadIdx.x; i < 32768; i += blockDim.x) {
     int t2 = (i >> 5) & 1, e = (i >> 6) & 255, pair = i >> 14;
-    s32[i] = __ldg(tables + (pair * 2 + t2) * 256 + e);
+    rep[i] = __ldg(tables + (pair * 2 + t2) * 256 + e);
   }
-  for (int i = threadIdx.x; i < 6 * 1024; i += blockDim.x) s32[32768 + i] = __ldg(tables + 1024 + i);
+  uint32_t* small = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < 6 * 1024; i += blockDim.x) small[i] = __ldg(tables + 1024 + i);
   __syncthreads();
 }
 
 // O2 (COPY=false): every chunk -> digest, dirty flag, bitmap bit.
 // STW delta-copy (COPY=true): every work item -> digest + pack entry + payload.
-template <bool COPY>
-__global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
+template <bool COPY, int kThreads = kHashThreads, int kUnroll = kUnrollDefault>
+__global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   load_hash_tables(smem, p.tables);
-  const uint8_t* rep = smem;
-  const uint32_t* small = reinterpret_cast<const uint32_t*>(smem + kRepTableBytes);
+  const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
-  const uint32_t lsel = (uint32_t)lane * 4;
+  const uint32_t lsel = (uint32_t)lane * 4 | kRepAbs;
   // Item i goes to CTA i % grid, warp (i / grid) % 16: consecutive items land
   // on different SMs, so a short list still spreads over the whole chip.
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kHashThreads / 32);
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kThreads / 32);
   const uint64_t n_units = p.n_items * p.nseg;
   for (uint64_t it = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < n_units;
        it += nwarps) {
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
-    const uint32_t r = n ? warp_crc32<COPY>(rep, small, p.xinv, lsel, lane, b.ptr + start + lo, n,
+    const uint32_t r = n ? warp_crc32<COPY, kUnroll>(small, p.xinv, lsel, lane, b.ptr + start + lo, n,
                                             p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
                          : 0u;
     if (p.nseg == 1) {
@@ -352,7 +365,7 @@ __global__ void __launch_bounds__(kHashThreads, 1) k_hash_chunks(HashParams p) {
       __threadfence();
       // raw(chunk) = XOR_s Z^(len - end_s)(raw_s); segments past the tail are empty.
       const uint32_t m = (uint32_t)((len - 1) / p.seg_bytes);  // last non-empty segment
-      const uint32_t xl = len == p.chunk_size ? p.xseg[1] : b.x8_lastseg;
+      const uint32_t xl = len == p.chunk_size ? p.xseg[1] : p.lastseg[cm.x];
       uint32_t v = 0;
       if ((uint32_t)lane <= m) {
         v = __ldcg(p.seg_raw + g * p.nseg + lane);
@@ -454,6 +467,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     result[0] = N;
     result[1] = total;
     result[2] = overflow;
+    result[3] = overflow ? 0 : N;  // items for the copy kernel
   }
   if (overflow) return;
   if (t == 0) {

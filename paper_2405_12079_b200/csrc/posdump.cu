@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -95,6 +96,45 @@ struct PinnedArray {
   }
 };
 
+// Hash kernel variants (threads per CTA x warp steps per batch); one CTA per
+// SM either way.  POSDUMP_HASH_CFG selects one for tuning runs.
+enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12 };
+
+HashCfg hash_cfg() {
+  static const HashCfg c = [] {
+    const char* e = std::getenv("POSDUMP_HASH_CFG");
+    if (!e) return kCfg512x8;
+    if (!std::strcmp(e, "256x16")) return kCfg256x16;
+    if (!std::strcmp(e, "384x12")) return kCfg384x12;
+    return kCfg512x8;
+  }();
+  return c;
+}
+
+int hash_threads() {
+  switch (hash_cfg()) {
+    case kCfg256x16: return 256;
+    case kCfg384x12: return 384;
+    default: return 512;
+  }
+}
+
+template <bool COPY>
+void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
+  switch (hash_cfg()) {
+    case kCfg256x16: k_hash_chunks<COPY, 256, 16><<<grid, 256, kHashSmem, s>>>(p); break;
+    case kCfg384x12: k_hash_chunks<COPY, 384, 12><<<grid, 384, kHashSmem, s>>>(p); break;
+    default: k_hash_chunks<COPY, 512, 8><<<grid, 512, kHashSmem, s>>>(p); break;
+  }
+}
+
+template <bool COPY>
+void set_hash_smem() {
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 384, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+}
+
 // Tables shared by every launch on a device: Z^512 (replicated in smem by the
 // kernel), Z^4, Z^16..Z^256, and x^(-8n) for n < 512.
 struct CrcTables {
@@ -113,12 +153,8 @@ struct CrcTables {
     ck(cudaMemcpy(tables.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "upload tables");
     ck(cudaMemcpy(xinv.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice), "upload xinv");
     ck(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
-    ck(cudaFuncSetAttribute(k_hash_chunks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kHashSmem),
-       "smem attr");
-    ck(cudaFuncSetAttribute(k_hash_chunks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kHashSmem),
-       "smem attr");
+    set_hash_smem<false>();
+    set_hash_smem<true>();
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
   }
@@ -165,8 +201,11 @@ struct pos_ctx {
   DevArray<uint8_t> d_dag_dirty;
   DevArray<uint32_t> d_tcs;  // Z^chunk_size
   // chunk segmentation (parallelism for short chunk lists)
-  uint32_t nseg = 1, seg_bytes = 0;
-  DevArray<uint32_t> d_xseg, d_seg_raw, d_seg_cnt;
+  // level L = log2(nseg): x^(8 k cs/2^L) (32 per level) and, per buffer,
+  // x^(8 * last segment length of the tail chunk); valid_levels bitmask.
+  uint32_t seg_levels = 1;
+  DevArray<uint32_t> d_xseg, d_lastseg, d_seg_raw, d_seg_cnt;
+  DevArray<uint64_t> d_result;  // async pre-copy: [n, total, overflow, n_items]
   std::set<uint64_t> dirty_set;
   bool dag_uploaded = false;
   uint64_t dirty_version = 0;
@@ -186,6 +225,8 @@ struct pos_ctx {
   PinnedArray<uint8_t> h_stage;  // delta header + work list upload
   PinnedArray<uint8_t> h_dag;
   cudaEvent_t stage_free = nullptr;
+  cudaEvent_t scanned = nullptr;
+  bool pack_pending = false;
   // timing
   std::vector<cudaEvent_t> events;
   Timer timers[kTimCount];
@@ -304,6 +345,7 @@ int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
       c->d_err.ensure(1);
       c->h_scan.ensure(4);
       ck(cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->scanned, cudaEventDisableTiming), "event");
       for (auto& t : c->timers) {
         ck(cudaEventCreate(&t.a), "event");
         ck(cudaEventCreate(&t.b), "event");
@@ -334,6 +376,8 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_dag_dirty.release();
   c->d_tcs.release();
   c->d_xseg.release();
+  c->d_lastseg.release();
+  c->d_result.release();
   c->d_seg_raw.release();
   c->d_seg_cnt.release();
   c->cache.release();
@@ -345,6 +389,7 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->h_stage.release();
   c->h_dag.release();
   if (c->stage_free) cudaEventDestroy(c->stage_free);
+  if (c->scanned) cudaEventDestroy(c->scanned);
   for (auto& t : c->timers) {
     if (t.a) cudaEventDestroy(t.a);
     if (t.b) cudaEventDestroy(t.b);
@@ -393,27 +438,31 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
     }
     if (g > 0xFFFFFFFFull) fail(POS_E_INVALID_ARGUMENT, "more than 2^32 chunks");
     c->n_chunks = g;
-    // Split chunks into segments when there are too few chunks to give every
-    // warp of the grid several units (>= 16 KiB per segment, power of 2).
+    // Segment tables for nseg = 2^L (L < 6, segment >= 8 KiB, cs % (nseg*512) == 0):
+    // used when a launch has too few chunks to occupy every warp.
     {
-      const uint64_t warps = (uint64_t)c->crc.sm_count * (kHashThreads / 32);
-      uint32_t nseg = 1;
-      while (nseg < 32 && g * nseg < 4 * warps && cs % (2ull * nseg * kStepBytes) == 0 &&
-             cs / (2ull * nseg) >= 16384)
-        nseg *= 2;
-      c->nseg = nseg;
-      c->seg_bytes = (uint32_t)(cs / nseg);
-      std::vector<uint32_t> xs(32);
-      for (int k = 0; k < 32; ++k) xs[k] = x8nmodp((uint64_t)k * c->seg_bytes);
-      c->d_xseg.ensure(32);
-      ck(cudaMemcpy(c->d_xseg.p, xs.data(), 32 * 4, cudaMemcpyHostToDevice), "xseg");
-      for (uint32_t i = 0; i < n; ++i) {
-        DevBuf& b = c->hbufs[i];
-        uint64_t tail = b.size - (uint64_t)(b.nchunks - 1) * cs;
-        uint64_t m = (tail - 1) / c->seg_bytes;
-        b.x8_lastseg = x8nmodp(tail - m * c->seg_bytes);
+      std::vector<uint32_t> xs(6 * 32), ls(6 * (size_t)std::max<uint32_t>(n, 1));
+      c->seg_levels = 0;
+      for (int L = 0; L < 6; ++L) {
+        uint64_t nseg = 1ull << L;
+        if (cs % (nseg * kStepBytes) != 0 || (L > 0 && cs / nseg < 8192)) break;
+        c->seg_levels = L + 1;
+        uint64_t sb = cs / nseg;
+        for (int k = 0; k < 32; ++k) xs[L * 32 + k] = x8nmodp((uint64_t)k * sb);
+        for (uint32_t i = 0; i < n; ++i) {
+          const DevBuf& b = c->hbufs[i];
+          uint64_t tail = b.size - (uint64_t)(b.nchunks - 1) * cs;
+          uint64_t m = (tail - 1) / sb;
+          ls[L * (size_t)n + i] = x8nmodp(tail - m * sb);
+        }
       }
-      c->d_seg_raw.ensure(std::max<uint64_t>(g, 1) * nseg);
+      if (c->seg_levels == 0) c->seg_levels = 1;  // nseg = 1 always valid
+      c->d_xseg.ensure(xs.size());
+      c->d_lastseg.ensure(ls.size());
+      ck(cudaMemcpy(c->d_xseg.p, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice), "xseg");
+      ck(cudaMemcpy(c->d_lastseg.p, ls.data(), ls.size() * 4, cudaMemcpyHostToDevice), "lastseg");
+      uint32_t nseg = 1u << (c->seg_levels - 1);
+      c->d_seg_raw.ensure(std::max<uint64_t>(g, 1) * nseg);  // enough for any level
       c->d_seg_cnt.ensure(std::max<uint64_t>(g, 1));
       ck(cudaMemset(c->d_seg_cnt.p, 0, std::max<uint64_t>(g, 1) * 4), "memset");
     }
@@ -470,6 +519,29 @@ int pos_num_chunks(pos_ctx* c, uint64_t* out) {
   });
 }
 
+
+// Segments for a launch over `items` chunks: split chunks only when the list
+// cannot give every warp of the grid one chunk (measured: splitting a list
+// that already covers half the warps costs more than it balances).
+static void set_segments(const pos_ctx* c, uint64_t items, HashParams& p) {
+  const uint64_t warps = (uint64_t)c->crc.sm_count * (hash_threads() / 32);
+  int L = 0;
+  if (items < warps / 2)
+    while (L + 1 < (int)c->seg_levels && (items << L) < warps) ++L;
+  if (const char* e = std::getenv("POSDUMP_NSEG")) {  // tuning override
+    int want = 0;
+    for (unsigned v = (unsigned)std::strtoul(e, nullptr, 10); v > 1; v >>= 1) ++want;
+    if (want < (int)c->seg_levels) L = want;
+  }
+  const uint32_t nb = (uint32_t)std::max<size_t>(c->bufs.size(), 1);
+  p.nseg = 1u << L;
+  p.seg_bytes = (uint32_t)(c->cfg.chunk_size >> L);
+  p.xseg = c->d_xseg.p + 32 * L;
+  p.lastseg = c->d_lastseg.p + (size_t)nb * L;
+  p.seg_raw = c->d_seg_raw.p;
+  p.seg_cnt = c->d_seg_cnt.p;
+}
+
 int pos_hash_chunks(pos_ctx* c, void* stream) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
@@ -490,14 +562,10 @@ int pos_hash_chunks(pos_ctx* c, void* stream) {
     p.flags = c->d_flags.p;
     p.bitmap = c->d_bitmap.p;
     p.prev_valid = c->prev_valid ? 1 : 0;
-    p.nseg = c->nseg;
-    p.seg_bytes = c->seg_bytes;
-    p.xseg = c->d_xseg.p;
-    p.seg_raw = c->d_seg_raw.p;
-    p.seg_cnt = c->d_seg_cnt.p;
-    int grid = c->hash_grid(c->n_chunks * c->nseg);
+    set_segments(c, c->n_chunks, p);
+    int grid = c->hash_grid(c->n_chunks * p.nseg);
     c->timer_begin(kTimHash, s);
-    k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);
+    launch_hash<false>(grid, s, p);
     check_launch("k_hash_chunks");
     c->timer_end(kTimHash, s);
     ++c->launches;
@@ -592,36 +660,70 @@ int pos_clear_dirty(pos_ctx* c) {
   });
 }
 
+// Scan + compaction, fully asynchronous: the copy kernel reads its item count
+// from the scan's device-side result, and the result is mirrored into pinned
+// memory behind an event for pack_size().
+static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s) {
+  upload_dag_flags(c, s);
+  c->timer_begin(kTimScan, s);
+  k_pack_scan<<<1, kScanThreads, 0, s>>>(
+      c->d_bufs.p, c->d_chunk_map.p, c->n_chunks, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
+      c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
+      c->cache_cap, c->d_items.p, c->d_scan.p);
+  check_launch("k_pack_scan");
+  c->timer_end(kTimScan, s);
+  ++c->launches;
+  ck(cudaMemcpyAsync(c->h_scan.p, c->d_scan.p, 4 * 8, cudaMemcpyDeviceToHost, s), "scan result");
+  ck(cudaEventRecord(c->scanned, s), "event");
+  bool aligned = c->cfg.chunk_size % 16 == 0;
+  for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
+  c->timer_begin(kTimCopy, s);
+  launch_copy(c, c->d_items.p, c->d_scan.p + 3, 0, aligned, s);
+  c->timer_end(kTimCopy, s);
+  c->pack_pending = true;
+}
+
+static uint64_t pack_size(pos_ctx* c) {
+  if (!c->pack_pending) fail(POS_E_BAD_STATE, "no pre-copy pack in flight");
+  ck(cudaEventSynchronize(c->scanned), "scan sync");
+  c->pack_pending = false;
+  uint64_t total = c->h_scan.p[1];
+  if (c->h_scan.p[2]) {
+    c->precopy_bytes = 0;
+    fail(POS_E_STAGING_EXHAUSTED, "pack of " + std::to_string(total) + " B exceeds cache of " +
+                                      std::to_string(c->cache_cap) + " B");
+  }
+  c->precopy_bytes = total;
+  return total;
+}
+
 int pos_compact(pos_ctx* c, int exclude_dag_dirty, void* stream, uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    launch_pack(c, exclude_dag_dirty, S(stream));
+    uint64_t total = pack_size(c);
+    if (pack_bytes) *pack_bytes = total;
+  });
+}
+
+int pos_precopy(pos_ctx* c, int exclude_dag_dirty, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     cudaStream_t s = S(stream);
-    upload_dag_flags(c, s);
-    c->timer_begin(kTimScan, s);
-    k_pack_scan<<<1, kScanThreads, 0, s>>>(
-        c->d_bufs.p, c->d_chunk_map.p, c->n_chunks, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
-        c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
-        c->cache_cap, c->d_items.p, c->d_scan.p);
-    check_launch("k_pack_scan");
-    c->timer_end(kTimScan, s);
-    ++c->launches;
-    ck(cudaMemcpyAsync(c->h_scan.p, c->d_scan.p, 3 * 8, cudaMemcpyDeviceToHost, s), "scan result");
-    ck(cudaStreamSynchronize(s), "sync");
-    uint64_t n = c->h_scan.p[0], total = c->h_scan.p[1];
-    if (c->h_scan.p[2]) {
-      c->precopy_bytes = 0;
-      fail(POS_E_STAGING_EXHAUSTED, "pack of " + std::to_string(total) + " B exceeds cache of " +
-                                        std::to_string(c->cache_cap) + " B");
-    }
-    bool aligned = c->cfg.chunk_size % 16 == 0;
-    for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
-    if (n) {
-      c->timer_begin(kTimCopy, s);
-      launch_copy(c, c->d_items.p, nullptr, n, aligned, s);
-      c->timer_end(kTimCopy, s);
-    }
-    c->precopy_bytes = total;
+    int rc = pos_hash_chunks(c, stream);
+    if (rc != POS_OK) throw Fail{rc};
+    rc = pos_buffer_crc(c, stream);
+    if (rc != POS_OK) throw Fail{rc};
+    launch_pack(c, exclude_dag_dirty, s);
+  });
+}
+
+int pos_precopy_size(pos_ctx* c, uint64_t* pack_bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    uint64_t total = pack_size(c);
     if (pack_bytes) *pack_bytes = total;
   });
 }
@@ -717,14 +819,10 @@ int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pa
       p.work = c->d_work.p;
       p.pack = c->cache.p + c->delta_offset;
       p.payload_off = c->delta_payload_off;
-      p.nseg = c->nseg;
-      p.seg_bytes = c->seg_bytes;
-      p.xseg = c->d_xseg.p;
-      p.seg_raw = c->d_seg_raw.p;
-      p.seg_cnt = c->d_seg_cnt.p;
-      int grid = c->hash_grid(n * c->nseg);
+      set_segments(c, n, p);
+      int grid = c->hash_grid(n * p.nseg);
       c->timer_begin(kTimDelta, s);
-      k_hash_chunks<true><<<grid, kHashThreads, kHashSmem, s>>>(p);
+      launch_hash<true>(grid, s, p);
       check_launch("k_hash_chunks<copy>");
       c->timer_end(kTimDelta, s);
       ++c->launches;
@@ -869,7 +967,7 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
       p.seg_bytes = (uint32_t)cs;
       uint64_t blocks = (nc + 15) / 16;
       int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)t.sm_count));
-      k_hash_chunks<false><<<grid, kHashThreads, kHashSmem, s>>>(p);
+      launch_hash<false>(grid, s, p);
       check_launch("k_hash_chunks");
       k_buffer_crc<<<1, 32, 0, s>>>(db.p, 1, dd.p, dt.p, dz.p, 0, dc.p, dz.p + 1);
       check_launch("k_buffer_crc");

@@ -336,9 +336,18 @@ class DumpEngine:
     def plan_precopy(self, stream=None, exclude_dag_dirty: bool = True) -> int:
         """hash -> O1 verdicts -> compaction into the cache (cr.hpp:377-406).
         Returns the pre-copy pack size (bytes at cache offset 0)."""
-        self.hash_chunks(stream)
-        self.scan_dedup(stream)
-        return self.compact(exclude_dag_dirty, stream)
+        self.launch_precopy(stream, exclude_dag_dirty)
+        return self.precopy_size()
+
+    def launch_precopy(self, stream=None, exclude_dag_dirty: bool = True) -> None:
+        """Asynchronous pre-copy (pos_precopy); pair with precopy_size()."""
+        check(lib().pos_precopy(self.ctx, 1 if exclude_dag_dirty else 0, _s(stream)))
+
+    def precopy_size(self) -> int:
+        n = C.c_uint64(0)
+        check(lib().pos_precopy_size(self.ctx, C.byref(n)))
+        self.precopy_bytes = n.value
+        return n.value
 
     # ---- STW delta-copy (at_final_stop, cr.hpp:599-621)
     def at_final_stop(self, stream=None) -> tuple[int, int]:

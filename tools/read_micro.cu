@@ -1,0 +1,104 @@
+// Memory-side ceiling for the hash kernel's access pattern: warp-per-chunk
+// streaming reads (LDG.128, ping-pong batches of U steps of 512 B) with a
+// trivial XOR reduction instead of CRC lookups.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/read_micro tools/read_micro.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint4 ldg(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void l2pf(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// PF: 0 none, 1 bulk 16 KiB ahead per batch, 2 whole chunk upfront, 3 per-lane prefetch.global.L2
+template <int U, int PF = 0>
+__global__ void k_read(const uint8_t* base, uint64_t nchunks, uint64_t cbytes, uint32_t* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+  uint32_t acc = 0;
+  for (uint64_t c = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; c < nchunks; c += nw) {
+    const uint4* p = reinterpret_cast<const uint4*>(base + c * cbytes) + lane;
+    const uint64_t steps = cbytes / 512;
+    const uint8_t* cb = base + c * cbytes;
+    if (PF == 2 && lane == 0) l2pf(cb, (uint32_t)cbytes);
+    if (PF == 1 && lane == 0) l2pf(cb, (uint32_t)(cbytes < 16384 ? cbytes : 16384));
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = ldg(p + u * 32);
+    for (uint64_t s = 0; s < steps; s += 2 * U) {
+      if (PF == 1 && lane == 0 && (s + 32) < steps) l2pf(cb + (s + 32) * 512, 2 * U * 512);
+      if (PF == 3 && (s + 32) < steps) asm volatile("prefetch.global.L2 [%0];" ::"l"(cb + (s + 32) * 512 + lane * 128));
+      if (s + U < steps) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) b[u] = ldg(p + (s + U + u) * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc ^= a[u].x ^ a[u].y ^ a[u].z ^ a[u].w;
+      if (s + 2 * U < steps) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) a[u] = ldg(p + (s + 2 * U + u) * 32);
+      }
+      if (s + U < steps) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= b[u].x ^ b[u].y ^ b[u].z ^ b[u].w;
+      }
+    }
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+template <int U, int PF = 0>
+float run(const uint8_t* d, uint64_t bytes, uint64_t cb, int blocks, int threads, uint32_t* out,
+          uint8_t* flush) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) {
+    cudaMemset(flush, r, 256 << 20);
+    cudaEventRecord(a);
+    k_read<U, PF><<<blocks, threads>>>(d, bytes / cb, cb, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return bytes / (best * 1e-3) / 1e9;
+}
+
+int main() {
+  const uint64_t bytes = 1ull << 30;
+  uint8_t *d, *flush;
+  uint32_t* out;
+  cudaMalloc(&d, bytes);
+  cudaMalloc(&flush, 256 << 20);
+  cudaMalloc(&out, 4);
+  cudaMemset(d, 1, bytes);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int thr : {256, 512}) {
+    printf("100MB 64K chunks %d thr U8: pf0 %7.1f pf1 %7.1f pf2 %7.1f pf3 %7.1f\n", thr,
+           run<8, 0>(d, 1526ull * 65536, 65536, sms, thr, out, flush), run<8, 1>(d, 1526ull * 65536, 65536, sms, thr, out, flush),
+           run<8, 2>(d, 1526ull * 65536, 65536, sms, thr, out, flush), run<8, 3>(d, 1526ull * 65536, 65536, sms, thr, out, flush));
+    printf("1GiB  64K chunks %d thr U8: pf0 %7.1f pf1 %7.1f pf2 %7.1f pf3 %7.1f\n", thr,
+           run<8, 0>(d, bytes, 65536, sms, thr, out, flush), run<8, 1>(d, bytes, 65536, sms, thr, out, flush),
+           run<8, 2>(d, bytes, 65536, sms, thr, out, flush), run<8, 3>(d, bytes, 65536, sms, thr, out, flush));
+  }
+  // one warp per SM streaming: per-warp throughput
+  for (int pf = 0; pf < 4; ++pf) {
+    float g = pf == 0 ? run<8, 0>(d, 148ull * 65536 * 4, 65536 * 4, sms, 32, out, flush)
+            : pf == 1 ? run<8, 1>(d, 148ull * 65536 * 4, 65536 * 4, sms, 32, out, flush)
+            : pf == 2 ? run<8, 2>(d, 148ull * 65536 * 4, 65536 * 4, sms, 32, out, flush)
+                      : run<8, 3>(d, 148ull * 65536 * 4, 65536 * 4, sms, 32, out, flush);
+    printf("1 warp/SM, 256 KiB each, pf%d: %7.1f GB/s total = %.2f GB/s per warp\n", pf, g, g / 148);
+  }
+  return 0;
+}
