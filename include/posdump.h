@@ -143,6 +143,17 @@ int pos_compact(pos_ctx* ctx, int exclude_dag_dirty, void* stream, uint64_t* pac
  * size becomes available through pos_precopy_size (waits for the scan only). */
 int pos_precopy(pos_ctx* ctx, int exclude_dag_dirty, void* stream);
 int pos_precopy_size(pos_ctx* ctx, uint64_t* pack_bytes);
+/* Pipelined pre-copy: the buffer set in up to `waves` (<= 16) contiguous
+ * groups of whole buffers; per wave, on ckpt_stream: hash -> O1 -> scan ->
+ * compaction into its own POSD pack (packs chained in the cache); and, when
+ * host_dst != NULL, each wave's pack is copied to host_dst at the same offset
+ * on copy_stream as soon as it is in the cache -- the D2H of wave k overlaps
+ * the hashing of wave k+1.  offsets[] / sizes[] (capacity 16) receive each
+ * pack's cache offset and size; returns after the last scan (copies may still
+ * be in flight on copy_stream). */
+int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
+                          void* copy_stream, void* host_dst, uint64_t slice_bytes,
+                          uint64_t* offsets, uint64_t* sizes, uint32_t* n_packs);
 
 /* ---- STW delta-copy --------------------------------------------------- */
 /* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is

@@ -110,6 +110,7 @@ SIGNATURES = {
     "pos_compact": [P, I32, P, PU64],
     "pos_precopy": [P, I32, P],
     "pos_precopy_size": [P, PU64],
+    "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],

@@ -77,6 +77,7 @@ struct HashParams {
   // the last segment to finish folds the segment registers.
   uint32_t nseg;
   uint32_t seg_bytes;
+  uint64_t item_base;        // hash mode: first global chunk of this launch
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
   const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
   uint32_t* seg_raw;         // [n_chunks * nseg]
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
       entry = w.y;
       dst_off = (uint64_t)w.z | ((uint64_t)w.w << 32);
     } else {
-      g = item;
+      g = p.item_base + item;
     }
     const uint2 cm = p.chunk_map[g];
     const DevBuf& b = p.bufs[cm.x];
@@ -423,15 +424,21 @@ __global__ void k_buffer_crc(const DevBuf* bufs, uint32_t nbufs, const uint32_t*
 constexpr int kScanThreads = 1024;
 
 __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
-    const DevBuf* bufs, const uint2* chunk_map, uint64_t n_chunks, uint64_t chunk_size,
-    const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty, int exclude_dag,
-    const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* pack,
-    uint64_t pack_capacity, CopyItem* items, uint64_t* result /* [n, total, overflow] */) {
+    const DevBuf* bufs, const uint2* chunk_map, uint64_t chunk_lo, uint64_t chunk_hi,
+    uint64_t chunk_size, const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty,
+    int exclude_dag, const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* cache,
+    uint64_t cache_capacity, uint64_t* cursor, CopyItem* items,
+    uint64_t* result /* [n, total, overflow, n_items, base] */) {
   __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
   const int t = threadIdx.x;
+  // The pack goes at the running cache cursor (packs of earlier waves end
+  // there); items are written at [0, N) of `items`.
+  const uint64_t base = *cursor;
+  uint8_t* pack = cache + base;
+  const uint64_t n_chunks = chunk_hi - chunk_lo;
   const uint64_t per = (n_chunks + kScanThreads - 1) / kScanThreads;
-  const uint64_t lo = (uint64_t)t * per < n_chunks ? (uint64_t)t * per : n_chunks;
-  const uint64_t hi = lo + per < n_chunks ? lo + per : n_chunks;
+  const uint64_t lo = chunk_lo + ((uint64_t)t * per < n_chunks ? (uint64_t)t * per : n_chunks);
+  const uint64_t hi = lo + per < chunk_hi ? lo + per : chunk_hi;
   auto chunk_len = [&](uint2 cm) -> uint64_t {
     const DevBuf& b = bufs[cm.x];
     uint64_t start = (uint64_t)cm.y * chunk_size;
@@ -462,12 +469,15 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   const uint64_t payload_off =
       (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
   const uint64_t total = payload_off + B;
-  const bool overflow = total > pack_capacity;
+  const bool overflow = base + total > cache_capacity;
+  __syncthreads();  // every thread has read *cursor
   if (t == 0) {
     result[0] = N;
     result[1] = total;
     result[2] = overflow;
     result[3] = overflow ? 0 : N;  // items for the copy kernel
+    result[4] = base;
+    if (!overflow) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
   }
   if (overflow) return;
   if (t == 0) {

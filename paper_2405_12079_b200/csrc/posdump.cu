@@ -169,8 +169,8 @@ void require_device(int device) {
   ck(cudaSetDevice(device), "cudaSetDevice");
 }
 
-enum TimerId { kTimHash = 0, kTimCombine, kTimScan, kTimCopy, kTimDelta, kTimScatter, kTimCount };
-const char* kTimerNames[kTimCount] = {"hash", "combine", "scan", "copy", "delta", "scatter"};
+enum TimerId { kTimHash = 0, kTimCombine, kTimScan, kTimCopy, kTimDelta, kTimScatter, kTimD2H, kTimCount };
+const char* kTimerNames[kTimCount] = {"hash", "combine", "scan", "copy", "delta", "scatter", "d2h"};
 
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -225,7 +225,13 @@ struct pos_ctx {
   PinnedArray<uint8_t> h_stage;  // delta header + work list upload
   PinnedArray<uint8_t> h_dag;
   cudaEvent_t stage_free = nullptr;
-  cudaEvent_t scanned = nullptr;
+  // Pre-copy packs: one per wave, chained at a device-side cache cursor.
+  static constexpr uint32_t kMaxWaves = 16;
+  DevArray<uint64_t> d_cursor;                     // [1]
+  cudaEvent_t scanned[kMaxWaves] = {};
+  cudaEvent_t copied[kMaxWaves] = {};
+  cudaEvent_t wave_hash[kMaxWaves][2] = {};
+  uint32_t waves_last = 0;                          // waves of the last pre-copy (hash timing)
   bool pack_pending = false;
   // timing
   std::vector<cudaEvent_t> events;
@@ -341,11 +347,17 @@ int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
       }
       c->cache_cap = round_up(cap, 256);
       c->cache.ensure(c->cache_cap);
-      c->d_scan.ensure(4);
+      c->d_scan.ensure(8 * pos_ctx::kMaxWaves);
       c->d_err.ensure(1);
-      c->h_scan.ensure(4);
+      c->h_scan.ensure(8 * pos_ctx::kMaxWaves);
       ck(cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&c->scanned, cudaEventDisableTiming), "event");
+      for (uint32_t w = 0; w < pos_ctx::kMaxWaves; ++w) {
+        ck(cudaEventCreateWithFlags(&c->scanned[w], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->copied[w], cudaEventDisableTiming), "event");
+        ck(cudaEventCreate(&c->wave_hash[w][0]), "event");
+        ck(cudaEventCreate(&c->wave_hash[w][1]), "event");
+      }
+      c->d_cursor.ensure(1);
       for (auto& t : c->timers) {
         ck(cudaEventCreate(&t.a), "event");
         ck(cudaEventCreate(&t.b), "event");
@@ -389,7 +401,13 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->h_stage.release();
   c->h_dag.release();
   if (c->stage_free) cudaEventDestroy(c->stage_free);
-  if (c->scanned) cudaEventDestroy(c->scanned);
+  for (uint32_t w = 0; w < pos_ctx::kMaxWaves; ++w) {
+    if (c->scanned[w]) cudaEventDestroy(c->scanned[w]);
+    if (c->copied[w]) cudaEventDestroy(c->copied[w]);
+    if (c->wave_hash[w][0]) cudaEventDestroy(c->wave_hash[w][0]);
+    if (c->wave_hash[w][1]) cudaEventDestroy(c->wave_hash[w][1]);
+  }
+  c->d_cursor.release();
   for (auto& t : c->timers) {
     if (t.a) cudaEventDestroy(t.a);
     if (t.b) cudaEventDestroy(t.b);
@@ -660,48 +678,104 @@ int pos_clear_dirty(pos_ctx* c) {
   });
 }
 
-// Scan + compaction, fully asynchronous: the copy kernel reads its item count
-// from the scan's device-side result, and the result is mirrored into pinned
-// memory behind an event for pack_size().
-static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s) {
+// Scan + compaction of chunks [lo, hi) into a pack at the device-side cache
+// cursor, fully asynchronous: the copy kernel reads its item count from the
+// scan's device-side result, which is mirrored into pinned memory behind
+// event scanned[slot] for pack_result().
+static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
+                        uint32_t slot) {
   upload_dag_flags(c, s);
+  uint64_t* res = c->d_scan.p + 8 * slot;
   c->timer_begin(kTimScan, s);
   k_pack_scan<<<1, kScanThreads, 0, s>>>(
-      c->d_bufs.p, c->d_chunk_map.p, c->n_chunks, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
+      c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
-      c->cache_cap, c->d_items.p, c->d_scan.p);
+      c->cache_cap, c->d_cursor.p, c->d_items.p, res);
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
   ++c->launches;
-  ck(cudaMemcpyAsync(c->h_scan.p, c->d_scan.p, 4 * 8, cudaMemcpyDeviceToHost, s), "scan result");
-  ck(cudaEventRecord(c->scanned, s), "event");
+  ck(cudaMemcpyAsync(c->h_scan.p + 8 * slot, res, 5 * 8, cudaMemcpyDeviceToHost, s), "scan result");
+  ck(cudaEventRecord(c->scanned[slot], s), "event");
   bool aligned = c->cfg.chunk_size % 16 == 0;
   for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
   c->timer_begin(kTimCopy, s);
-  launch_copy(c, c->d_items.p, c->d_scan.p + 3, 0, aligned, s);
+  launch_copy(c, c->d_items.p, res + 3, 0, aligned, s);
   c->timer_end(kTimCopy, s);
+  ck(cudaEventRecord(c->copied[slot], s), "event");
   c->pack_pending = true;
+}
+
+struct PackResult {
+  uint64_t base, total, n;
+};
+
+static PackResult pack_result(pos_ctx* c, uint32_t slot) {
+  ck(cudaEventSynchronize(c->scanned[slot]), "scan sync");
+  const uint64_t* r = c->h_scan.p + 8 * slot;
+  if (r[2]) {
+    c->precopy_bytes = 0;
+    c->pack_pending = false;
+    fail(POS_E_STAGING_EXHAUSTED, "pack of " + std::to_string(r[1]) + " B at cache offset " +
+                                      std::to_string(r[4]) + " exceeds the cache of " +
+                                      std::to_string(c->cache_cap) + " B");
+  }
+  return PackResult{r[4], r[1], r[0]};
 }
 
 static uint64_t pack_size(pos_ctx* c) {
   if (!c->pack_pending) fail(POS_E_BAD_STATE, "no pre-copy pack in flight");
-  ck(cudaEventSynchronize(c->scanned), "scan sync");
+  PackResult r = pack_result(c, 0);
   c->pack_pending = false;
-  uint64_t total = c->h_scan.p[1];
-  if (c->h_scan.p[2]) {
-    c->precopy_bytes = 0;
-    fail(POS_E_STAGING_EXHAUSTED, "pack of " + std::to_string(total) + " B exceeds cache of " +
-                                      std::to_string(c->cache_cap) + " B");
-  }
-  c->precopy_bytes = total;
-  return total;
+  c->precopy_bytes = r.total;
+  return r.total;
+}
+
+static void reset_cursor(pos_ctx* c, cudaStream_t s) {
+  ck(cudaMemsetAsync(c->d_cursor.p, 0, 8, s), "cursor");
+}
+
+static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uint32_t wave) {
+  if (hi <= lo) return;  // the caller zeroes the bitmap (boundary words are shared)
+  HashParams p{};
+  p.bufs = c->d_bufs.p;
+  p.chunk_map = c->d_chunk_map.p;
+  p.n_items = hi - lo;
+  p.item_base = lo;
+  p.chunk_size = c->cfg.chunk_size;
+  p.k_full = zeros_crc(c->cfg.chunk_size);
+  p.tables = c->crc.tables.p;
+  p.xinv = c->crc.xinv.p;
+  p.digest_cur = c->d_digest[c->cur].p;
+  p.digest_prev = c->d_digest[c->cur ^ 1].p;
+  p.flags = c->d_flags.p;
+  p.bitmap = c->d_bitmap.p;
+  p.prev_valid = c->prev_valid ? 1 : 0;
+  set_segments(c, hi - lo, p);
+  int grid = c->hash_grid((hi - lo) * p.nseg);
+  ck(cudaEventRecord(c->wave_hash[wave][0], s), "event");
+  launch_hash<false>(grid, s, p);
+  check_launch("k_hash_chunks");
+  ck(cudaEventRecord(c->wave_hash[wave][1], s), "event");
+  ++c->launches;
+}
+
+static void combine_range(pos_ctx* c, uint32_t b0, uint32_t b1, cudaStream_t s) {
+  if (b1 <= b0) return;
+  upload_dag_flags(c, s);
+  uint32_t nb = b1 - b0;
+  k_buffer_crc<<<(nb + 127) / 128, 128, 0, s>>>(c->d_bufs.p + b0, nb, c->d_digest[c->cur].p, c->d_tcs.p,
+                                               c->d_dag_dirty.p + b0, c->cfg.dedup, c->d_buf_crc.p + b0,
+                                               c->d_verdict.p + b0);
+  check_launch("k_buffer_crc");
+  ++c->launches;
 }
 
 int pos_compact(pos_ctx* c, int exclude_dag_dirty, void* stream, uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
-    launch_pack(c, exclude_dag_dirty, S(stream));
+    reset_cursor(c, S(stream));
+    launch_pack(c, exclude_dag_dirty, S(stream), 0, c->n_chunks, 0);
     uint64_t total = pack_size(c);
     if (pack_bytes) *pack_bytes = total;
   });
@@ -716,7 +790,64 @@ int pos_precopy(pos_ctx* c, int exclude_dag_dirty, void* stream) {
     if (rc != POS_OK) throw Fail{rc};
     rc = pos_buffer_crc(c, stream);
     if (rc != POS_OK) throw Fail{rc};
-    launch_pack(c, exclude_dag_dirty, s);
+    reset_cursor(c, s);
+    launch_pack(c, exclude_dag_dirty, s, 0, c->n_chunks, 0);
+  });
+}
+
+int pos_precopy_pipelined(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
+                          void* copy_stream, void* host_dst, uint64_t slice, uint64_t* offsets,
+                          uint64_t* sizes, uint32_t* n_packs) {
+  return guarded([&] {
+    if (!c || !offsets || !sizes || !n_packs) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(ckpt_stream), cs = S(copy_stream);
+    const uint32_t nb = (uint32_t)c->bufs.size();
+    uint32_t W = std::max<uint32_t>(1, std::min<uint32_t>(waves, pos_ctx::kMaxWaves));
+    W = std::min<uint32_t>(W, std::max<uint32_t>(nb, 1));
+    // Wave boundaries at buffer starts, ~equal chunk counts (O1 needs whole buffers).
+    std::vector<uint32_t> bb(1, 0);
+    for (uint32_t w = 1; w < W; ++w) {
+      uint64_t target = c->n_chunks * w / W;
+      uint32_t b = bb.back();
+      while (b < nb && c->chunk_base[b] < target) ++b;
+      if (b > bb.back() && b < nb) bb.push_back(b);
+    }
+    bb.push_back(nb);
+    W = (uint32_t)bb.size() - 1;
+    auto chunk_of = [&](uint32_t b) { return b < nb ? c->chunk_base[b] : c->n_chunks; };
+    reset_cursor(c, s);
+    upload_dag_flags(c, s);
+    if (c->n_chunks)
+      ck(cudaMemsetAsync(c->d_bitmap.p, 0, ((c->n_chunks + 31) / 32) * 4, s), "memset bitmap");
+    c->timer_begin(kTimHash, s);
+    for (uint32_t w = 0; w < W; ++w) {
+      hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
+      combine_range(c, bb[w], bb[w + 1], s);
+      launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w);
+    }
+    c->timer_end(kTimHash, s);
+    c->waves_last = W;
+    uint64_t end = 0;
+    for (uint32_t w = 0; w < W; ++w) {
+      PackResult r = pack_result(c, w);
+      offsets[w] = r.base;
+      sizes[w] = r.total;
+      end = r.base + (r.total + kPackAlign - 1) / kPackAlign * kPackAlign;
+      if (host_dst) {
+        ck(cudaStreamWaitEvent(cs, c->copied[w], 0), "wait copy");
+        if (w == 0) c->timer_begin(kTimD2H, cs);
+        if (slice == 0) slice = 8ull << 20;
+        for (uint64_t o = 0; o < r.total; o += slice)
+          ck(cudaMemcpyAsync(static_cast<uint8_t*>(host_dst) + r.base + o, c->cache.p + r.base + o,
+                             std::min(slice, r.total - o), cudaMemcpyDeviceToHost, cs),
+             "d2h");
+      }
+    }
+    if (host_dst) c->timer_end(kTimD2H, cs);
+    c->pack_pending = false;
+    c->precopy_bytes = end;
+    *n_packs = W;
   });
 }
 
@@ -1059,6 +1190,18 @@ int pos_launch_count(pos_ctx* c, uint64_t* out) {
 int pos_last_kernel_ms(pos_ctx* c, const char* which, float* ms) {
   return guarded([&] {
     if (!c || !which || !ms) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!std::strcmp(which, "hash_waves")) {  // sum of the last pipelined pre-copy's hash kernels
+      if (!c->waves_last) fail(POS_E_BAD_STATE, "no pipelined pre-copy recorded");
+      float total = 0;
+      for (uint32_t w = 0; w < c->waves_last; ++w) {
+        float m = 0;
+        ck(cudaEventSynchronize(c->wave_hash[w][1]), "event sync");
+        ck(cudaEventElapsedTime(&m, c->wave_hash[w][0], c->wave_hash[w][1]), "elapsed");
+        total += m;
+      }
+      *ms = total;
+      return;
+    }
     for (int t = 0; t < kTimCount; ++t) {
       if (std::strcmp(which, kTimerNames[t]) != 0) continue;
       if (!c->timers[t].used) fail(POS_E_BAD_STATE, "no launch recorded");

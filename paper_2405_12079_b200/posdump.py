@@ -343,6 +343,21 @@ class DumpEngine:
         """Asynchronous pre-copy (pos_precopy); pair with precopy_size()."""
         check(lib().pos_precopy(self.ctx, 1 if exclude_dag_dirty else 0, _s(stream)))
 
+    def precopy_pipelined(self, host_ptr: Optional[int], waves: int = 4, stream=None, copy_stream=None,
+                          exclude_dag_dirty: bool = True, slice_bytes: int = 0) -> list[tuple[int, int]]:
+        """Wave-pipelined pre-copy with D2H of each wave's pack into host_ptr
+        (same offsets as in the cache).  Returns [(offset, size)] per pack."""
+        offs = (C.c_uint64 * 16)()
+        sizes = (C.c_uint64 * 16)()
+        n = C.c_uint32(0)
+        check(lib().pos_precopy_pipelined(self.ctx, 1 if exclude_dag_dirty else 0, waves, _s(stream),
+                                          _s(copy_stream), host_ptr, slice_bytes, offs, sizes, C.byref(n)))
+        packs = [(offs[i], sizes[i]) for i in range(n.value)]
+        if packs:
+            o, z = packs[-1]
+            self.precopy_bytes = o + z
+        return packs
+
     def precopy_size(self) -> int:
         n = C.c_uint64(0)
         check(lib().pos_precopy_size(self.ctx, C.byref(n)))

@@ -411,3 +411,52 @@ def test_c1_full_size_properties(orc):
     eng.hash_chunks()
     assert np.array_equal(eng.digests(), before)
     eng.close()
+
+
+@pytest.mark.parametrize("waves", [1, 3, 16])
+def test_pipelined_precopy_matches_single_pack(orc, waves):
+    """Wave-pipelined pre-copy: per-wave packs, chained in the cache and copied
+    to the same host offsets, carry exactly the single pack's entries and
+    payload; digests/flags/bitmap identical."""
+    cs = 65536
+    sizes = [3 * cs, 10000, 1, 2 * cs + 5, 70001, 5 * cs, 300, cs]
+    p = Proc(orc, sizes, seed0=4000)
+    p.bufs[2].upstream = pd.Upstream(ocrc(orc, p.host[2]), True)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=32 << 20))
+    eng.register_buffers(p.bufs)
+    n = eng.plan_precopy()
+    single = download_cache(eng, 0, n)
+    eng.commit_epoch()
+    p.write(0, 5, 100, 1)
+    p.write(5, 2 * cs, cs, 2)
+    p.write(7, cs - 1, 1, 3)
+    pd.device_synchronize()
+    n1 = eng.plan_precopy()
+    one = download_cache(eng, 0, n1)
+    d1, f1, b1 = eng.digests(), eng.flags(), eng.bitmap()
+    # same epoch again, pipelined (digests identical -> same flags)
+    host = pd.PinnedHost(16 << 20)
+    copy = pd.Stream()
+    packs = eng.precopy_pipelined(host.ptr, waves=waves, copy_stream=copy)
+    copy.synchronize()
+    pd.device_synchronize()
+    assert np.array_equal(eng.digests(), d1) and np.array_equal(eng.flags(), f1)
+    assert np.array_equal(eng.bitmap(), b1)
+    assert 1 <= len(packs) <= waves
+    ents = [pd.parse_pack(host.array[o:o + z]) for o, z in packs]
+    ref = pd.parse_pack(one)
+    for key in ("handle", "chunk", "len", "crc"):
+        assert np.array_equal(np.concatenate([e[key] for e in ents]), ref[key])
+    img = [np.zeros(n, np.uint8) for n in sizes]
+    for o, z in packs:
+        pd.apply_pack_host(host.array[o:o + z], p.handles, img)
+    want = [np.zeros(n, np.uint8) for n in sizes]
+    pd.apply_pack_host(one, p.handles, want)
+    for a, b in zip(img, want):
+        assert np.array_equal(a, b)
+    # the STW delta lands after the last wave pack
+    eng.record_dirty([4])
+    off, m = eng.at_final_stop()
+    assert off == (packs[-1][0] + packs[-1][1] + 255) // 256 * 256
+    del single
+    eng.close()
