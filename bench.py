@@ -333,7 +333,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
-    ckpt, copy, app = pd.Stream(), pd.Stream(), pd.Stream()
+    ckpt, copy, app = pd.Stream(priority=args.ckpt_priority), pd.Stream(), pd.Stream()
     by_handle = {b.handle: b for b in bufs}
 
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
@@ -347,9 +347,15 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         window = wl.window(e)
         launches0 = eng.launches
 
+        # The window's kernels, argument blocks prepared ahead (as an application
+        # would have its launch arguments ready): [dev_ptr, bytes, seed] per write.
+        app_args = [np.array([[by_handle[h].dev_ptr, by_handle[h].size, s & 0xFFFFFFFFFFFFFFFF]
+                              for h, s in k], dtype=np.uint64) for k in window]
+        fill_fn, app_h = pd.lib().pos_fill_batch, int(app)
+
         def run_app():  # the application's own host thread submits the window
-            for k in window:
-                pd.fill_batch([(by_handle[h].dev_ptr, by_handle[h].size, s) for h, s in k], stream=app)
+            for a in app_args:
+                fill_fn(a.ctypes.data, a.shape[0], app_h)
             eng.event_record(2, app)
 
         t0 = time.perf_counter()
@@ -536,7 +542,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
-    ap.add_argument("--waves", type=int, default=4, help="pre-copy pipeline waves (1 = no overlap)")
+    ap.add_argument("--waves", type=int, default=1, help="pre-copy pipeline waves (1 = no overlap)")
+    ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -254,6 +254,9 @@ int pos_host_free_pinned(void* host);
 int pos_memcpy(uint64_t dst, uint64_t src, uint64_t bytes, int kind, void* stream);
 int pos_memset(uint64_t dev_ptr, int value, uint64_t bytes, void* stream);
 int pos_stream_create(void** stream);
+/* priority: 0 = default, 1 = highest the device allows (the dump's kernels
+ * then win SMs over queued application blocks). */
+int pos_stream_create_prio(int priority, void** stream);
 int pos_stream_destroy(void* stream);
 int pos_stream_sync(void* stream);
 int pos_device_sync(void);

@@ -136,6 +136,7 @@ SIGNATURES = {
     "pos_memcpy": [U64, U64, U64, I32, P],
     "pos_memset": [U64, I32, U64, P],
     "pos_stream_create": [C.POINTER(P)],
+    "pos_stream_create_prio": [I32, C.POINTER(P)],
     "pos_stream_destroy": [P],
     "pos_stream_sync": [P],
     "pos_device_sync": [],

@@ -428,7 +428,8 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     uint64_t chunk_size, const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty,
     int exclude_dag, const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* cache,
     uint64_t cache_capacity, uint64_t* cursor, CopyItem* items,
-    uint64_t* result /* [n, total, overflow, n_items, base] */) {
+    uint64_t* result /* [n, total, overflow, n_items, base] */,
+    volatile uint64_t* result_host /* mapped pinned mirror (no DMA queue in between) */) {
   __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
   const int t = threadIdx.x;
   // The pack goes at the running cache cursor (packs of earlier waves end
@@ -478,6 +479,14 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     result[3] = overflow ? 0 : N;  // items for the copy kernel
     result[4] = base;
     if (!overflow) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
+    if (result_host) {
+      result_host[0] = N;
+      result_host[1] = total;
+      result_host[2] = overflow;
+      result_host[3] = overflow ? 0 : N;
+      result_host[4] = base;
+      __threadfence_system();
+    }
   }
   if (overflow) return;
   if (t == 0) {

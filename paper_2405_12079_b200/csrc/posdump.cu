@@ -86,7 +86,7 @@ struct PinnedArray {
     p = nullptr;
     n = 0;
     size_t c = std::max<size_t>(count, 1);
-    ck(cudaHostAlloc((void**)&p, c * sizeof(T), cudaHostAllocDefault), "cudaHostAlloc");
+    ck(cudaHostAlloc((void**)&p, c * sizeof(T), cudaHostAllocMapped), "cudaHostAlloc");
     n = c;
   }
   void release() {
@@ -690,11 +690,10 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
   k_pack_scan<<<1, kScanThreads, 0, s>>>(
       c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
-      c->cache_cap, c->d_cursor.p, c->d_items.p, res);
+      c->cache_cap, c->d_cursor.p, c->d_items.p, res, c->h_scan.p + 8 * slot);
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
   ++c->launches;
-  ck(cudaMemcpyAsync(c->h_scan.p + 8 * slot, res, 5 * 8, cudaMemcpyDeviceToHost, s), "scan result");
   ck(cudaEventRecord(c->scanned[slot], s), "event");
   bool aligned = c->cfg.chunk_size % 16 == 0;
   for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
@@ -1334,6 +1333,17 @@ int pos_stream_create(void** stream) {
     if (!stream) fail(POS_E_INVALID_ARGUMENT, "null argument");
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    *stream = s;
+  });
+}
+
+int pos_stream_create_prio(int priority, void** stream) {
+  return guarded([&] {
+    if (!stream) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    cudaStream_t s;
+    ck(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority ? hi : lo), "cudaStreamCreate");
     *stream = s;
   });
 }

@@ -96,9 +96,9 @@ class PinnedHost:
 
 
 class Stream:
-    def __init__(self):
+    def __init__(self, priority: int = 0):
         s = C.c_void_p(0)
-        check(lib().pos_stream_create(C.byref(s)))
+        check(lib().pos_stream_create_prio(priority, C.byref(s)))
         self.handle = s.value
 
     def __int__(self):
