@@ -329,13 +329,42 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # Landing ring of pinned buffers: the host applies step e's packs out of
     # one buffer while step e+1 DMA-writes the next (DMA into lines the CPU
     # just read costs ~30% of the link).
-    pins = [pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20))) for _ in range(3)]
+    pins = [pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20))) for _ in range(args.ring)]
     host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
     ckpt, copy, app = pd.Stream(priority=args.ckpt_priority), pd.Stream(), pd.Stream()
     by_handle = {b.handle: b for b in bufs}
 
+    class AppThread:
+        """Long-lived application host thread: submits a window of kernels
+        (pos_fill_batch) on the app stream, then records event 2."""
+
+        def __init__(self):
+            self.q, self.done = [], threading.Event()
+            self.go = threading.Event()
+            self.fill, self.h = pd.lib().pos_fill_batch, int(app)
+            threading.Thread(target=self.run, daemon=True).start()
+
+        def run(self):
+            while True:
+                self.go.wait()
+                self.go.clear()
+                for a in self.q:
+                    self.fill(a.ctypes.data, a.shape[0], self.h)
+                eng.event_record(2, app)
+                self.done.set()
+
+        def submit(self, args_list):
+            self.q = args_list
+            self.done.clear()
+            self.go.set()
+
+        def wait(self):
+            self.done.wait()
+
+    app_thread = AppThread()
+    apply_threads = max(1, min(32, len(os.sched_getaffinity(0))))
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
     def checkpoint(e: int, e2e: bool):
         pin = pins[e % len(pins)]
@@ -351,28 +380,22 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # would have its launch arguments ready): [dev_ptr, bytes, seed] per write.
         app_args = [np.array([[by_handle[h].dev_ptr, by_handle[h].size, s & 0xFFFFFFFFFFFFFFFF]
                               for h, s in k], dtype=np.uint64) for k in window]
-        fill_fn, app_h = pd.lib().pos_fill_batch, int(app)
-
-        def run_app():  # the application's own host thread submits the window
-            for a in app_args:
-                fill_fn(a.ctypes.data, a.shape[0], app_h)
-            eng.event_record(2, app)
+        dag_writes = sorted({h for k in window for h, _ in k})
 
         t0 = time.perf_counter()
         eng.event_record(0, ckpt)
         # The window's kernels are in the DAG from submission (their spec write
         # sets, process.hpp:313-344): their buffers are left to the STW pass,
         # as record_dirty's copy cancellation does (cr.hpp:909-918).
-        eng.record_dirty(sorted({h for k in window for h, _ in k}))
-        app_thread = threading.Thread(target=run_app)
-        app_thread.start()
+        eng.record_dirty(dag_writes)
+        app_thread.submit(app_args)  # the application's own host thread
         # waves: hash/O1/compaction of wave k+1 overlaps the D2H of wave k
         packs = eng.precopy_pipelined(pin.ptr, waves=args.waves, stream=ckpt, copy_stream=copy)
         nbytes = eng.precopy_bytes
         eng.event_record(1, ckpt)
         eng.event_record(8, copy)
         # final stop: DAG write sets of the window -> dirty_set_, drain the app
-        app_thread.join()
+        app_thread.wait()
         eng.prepare_final_stop(stream=ckpt)
         eng.stream_wait_event(2, ckpt)
         eng.event_record(3, ckpt)
@@ -387,8 +410,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # clock, always outside the device-timed region
         if not args.no_host_apply:
             for o, z in packs:
-                pd.apply_pack_host(pin.array[o:o + z], handles, host_image, threads=8)
-            pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=8)
+                pd.apply_pack_host(pin.array[o:o + z], handles, host_image, threads=apply_threads)
+            pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=apply_threads)
         t1 = time.perf_counter()
         ms = eng.event_elapsed(0, 5)
         stw = eng.event_elapsed(3, 4)
@@ -401,7 +424,10 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         hash_ms = kms("hash_waves")
         if args.trace:
             marks = {"precopy_enqueued": 1, "app_drained": 2, "stop": 3, "stw_end": 4, "precopy_d2h_end": 8, "end": 5}
-            print(json.dumps({k: round(eng.event_elapsed(0, v), 4) for k, v in marks.items()}), file=sys.stderr)
+            tl = {k: round(eng.event_elapsed(0, v), 4) for k, v in marks.items()}
+            tl.update(eng.timeline(0))
+            tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]
+            print(json.dumps(tl), file=sys.stderr)
         r = {"ms": ms, "stw_ms": stw, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
              "precopy_bytes": sum(z for _, z in packs), "delta_bytes": dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
@@ -543,6 +569,7 @@ def main():
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
     ap.add_argument("--waves", type=int, default=1, help="pre-copy pipeline waves (1 = no overlap)")
+    ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
     args = ap.parse_args()

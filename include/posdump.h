@@ -207,6 +207,9 @@ int pos_event_elapsed(pos_ctx* ctx, uint32_t a, uint32_t b, float* ms);
 /* `stream` waits for event `slot` (cross-stream drain: the STW delta-copy
  * waits for the application stream, cr.hpp:591-597). */
 int pos_stream_wait_event(pos_ctx* ctx, uint32_t slot, void* stream);
+/* Device timeline: for each internal timer (hash, combine, scan, copy, delta,
+ * scatter, d2h) the ms from event `slot` to its begin and end (-1 if unused). */
+int pos_timeline(pos_ctx* ctx, uint32_t slot, float* out14);
 /* Kernels this context has launched (monotone counter). */
 int pos_launch_count(pos_ctx* ctx, uint64_t* out);
 /* Device time of the most recent hash kernel launch (ms). */

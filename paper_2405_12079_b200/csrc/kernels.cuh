@@ -397,22 +397,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
 // O1: whole-buffer CRC = crc32_combine fold of the chunk digests, then the
 // scan_dedup verdict (cr.hpp:419-421) and the finalize_image gate
 // (!dirty_set_, cr.hpp:720).  One thread per buffer; Z^chunk_size from a table.
-__global__ void k_buffer_crc(const DevBuf* bufs, uint32_t nbufs, const uint32_t* digests,
-                             const uint32_t* tcs, const uint8_t* dag_dirty, int dedup,
-                             uint32_t* crc_out, uint8_t* verdict_out) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nbufs) return;
-  const DevBuf b = bufs[i];
+// Whole-buffer CRC of buffer b folded from its chunk digests (crc32_combine
+// with Z^chunk_size from table t, and x^(8*tail) for the short last chunk).
+__device__ __forceinline__ uint32_t fold_buffer_crc(const DevBuf& b, const uint32_t* digests,
+                                                    const uint32_t* t) {
   const uint32_t* d = digests + b.chunk_base;
   uint32_t crc = d[0];
   for (uint32_t c = 1; c < b.nchunks; ++c) {
     bool last = c + 1 == b.nchunks;
-    uint32_t adv = last ? multmodp(b.x8_tail, crc) : adv_small(tcs, crc);
+    uint32_t adv = last ? multmodp(b.x8_tail, crc) : adv_small(t, crc);
     crc = adv ^ d[c];
   }
+  return crc;
+}
+
+__global__ void k_buffer_crc(const DevBuf* bufs, uint32_t nbufs, const uint32_t* digests,
+                             const uint32_t* tcs, const uint8_t* dag_dirty, int dedup, int all,
+                             uint32_t* crc_out, uint8_t* verdict_out) {
+  __shared__ uint32_t t[1024];  // Z^chunk_size
+  for (int k = threadIdx.x; k < 1024; k += blockDim.x) t[k] = __ldg(tcs + k);
+  __syncthreads();
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbufs) return;
+  const DevBuf b = bufs[i];
+  const bool candidate = dedup && (b.flags & kBufHasUpstream);
+  if (!all && !candidate) {  // verdict only: no provenance, no CRC needed (cr.hpp:390)
+    verdict_out[i] = 0;
+    return;
+  }
+  const uint32_t crc = fold_buffer_crc(b, digests, t);
   crc_out[i] = crc;
-  bool ok = dedup && (b.flags & kBufHasUpstream) && crc == b.upstream_crc &&
-            (b.flags & kBufHostUntouched) && !dag_dirty[i];
+  bool ok = candidate && crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
   verdict_out[i] = ok;
 }
 
@@ -429,9 +444,29 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     int exclude_dag, const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* cache,
     uint64_t cache_capacity, uint64_t* cursor, CopyItem* items,
     uint64_t* result /* [n, total, overflow, n_items, base] */,
-    volatile uint64_t* result_host /* mapped pinned mirror (no DMA queue in between) */) {
+    volatile uint64_t* result_host /* mapped pinned mirror (no DMA queue in between) */,
+    uint64_t seq /* written last into result_host[5] */,
+    // fused O1 (k_buffer_crc for buffers [vb0, vb1) with upstream provenance):
+    uint32_t vb0, uint32_t vb1, const uint32_t* tcs, int dedup, uint32_t* crc_out,
+    uint8_t* verdict_out) {
   __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
   const int t = threadIdx.x;
+  if (vb1 > vb0) {
+    uint32_t* tz = reinterpret_cast<uint32_t*>(s_n);  // 8 KiB scratch: Z^chunk_size table
+    for (int k = t; k < 1024; k += kScanThreads) tz[k] = __ldg(tcs + k);
+    __syncthreads();
+    for (uint32_t i = vb0 + t; i < vb1; i += kScanThreads) {
+      const DevBuf& b = bufs[i];
+      bool ok = false;
+      if (dedup && (b.flags & kBufHasUpstream)) {  // no provenance -> no verdict (cr.hpp:390)
+        const uint32_t crc = fold_buffer_crc(b, digests, tz);
+        crc_out[i] = crc;
+        ok = crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
+      }
+      verdict_out[i] = ok;
+    }
+    __syncthreads();
+  }
   // The pack goes at the running cache cursor (packs of earlier waves end
   // there); items are written at [0, N) of `items`.
   const uint64_t base = *cursor;
@@ -485,6 +520,8 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       result_host[2] = overflow;
       result_host[3] = overflow ? 0 : N;
       result_host[4] = base;
+      __threadfence_system();
+      result_host[5] = seq;
       __threadfence_system();
     }
   }

@@ -401,6 +401,13 @@ class DumpEngine:
     def stream_wait_event(self, slot: int, stream=None) -> None:
         check(lib().pos_stream_wait_event(self.ctx, slot, _s(stream)))
 
+    def timeline(self, slot: int = 0) -> dict:
+        """ms from event `slot` to each internal timer's begin/end."""
+        out = (C.c_float * 14)()
+        check(lib().pos_timeline(self.ctx, slot, out))
+        names = ["hash", "combine", "scan", "copy", "delta", "scatter", "d2h"]
+        return {n: (round(out[2 * i], 4), round(out[2 * i + 1], 4)) for i, n in enumerate(names) if out[2 * i] >= 0}
+
     def kernel_ms(self, which: str) -> float:
         ms = C.c_float(0)
         check(lib().pos_last_kernel_ms(self.ctx, which.encode(), C.byref(ms)))
