@@ -210,6 +210,11 @@ def all_max(dist, vals, device):
     return t.cpu().tolist()
 
 
+def aggregate_value(world: int, state_bytes: int, step_ms: float) -> float:
+    """Whole-job GB/s: every rank checkpoints state_bytes; time = max over ranks."""
+    return world * state_bytes / (step_ms * 1e-3) / 1e9
+
+
 def barrier(dist, device):
     if dist is not None:
         if dist.get_backend() == "nccl":
@@ -488,7 +493,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
 
     out = None
     if rank == 0:
-        value = world * total / (step_ms * 1e-3) / 1e9
+        value = aggregate_value(world, total, step_ms)
         cpu = None
         if not args.no_cpu_baseline:
             try:

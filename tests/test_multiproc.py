@@ -1,0 +1,79 @@
+"""CPU, world_size 2 (gloo on 127.0.0.1): the N>1 plumbing of bench.py.
+
+Each GPU checkpoints its own process's buffers (independent
+units, no data-path collective); the only cross-rank traffic is the barrier
+and the max-over-ranks of the step timings.  Covered here: all_max, the
+barrier, the weak-scaling aggregate, and the reference arm under torchrun
+(rank 0 alone runs and prints; the others exit 0).
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bench.barrier(dist, rank)
+    vals = bench.all_max(dist, [float(rank + 1), float(10 - rank), 0.5 * rank], rank)
+    q.put((rank, vals))
+    dist.destroy_process_group()
+
+
+def test_all_max_and_barrier_over_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0] == out[1] == [2.0, 10.0, 0.5]
+
+
+def test_weak_scaling_aggregate():
+    sys.path.insert(0, ROOT)
+    import bench
+    # value = N * state bytes / max step time over ranks
+    assert bench.aggregate_value(world=4, state_bytes=100_000_000, step_ms=1.25) == pytest.approx(320.0)
+
+
+def test_reference_arm_under_torchrun(tmp_path):
+    ref = os.path.join(ROOT, "oracle", "_ref", "libgpucrsim_ref.so")
+    if not os.path.exists(ref):
+        pytest.skip("oracle/_ref not built")
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3",
+           "--ref-sample-bytes", "8000000"]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["cpu_baseline"]["kind"] == "reference"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
