@@ -19,6 +19,7 @@
 #include "gpucrsim/image.hpp"
 #include "gpucrsim/rng.hpp"
 #include "gpucrsim/workload.hpp"
+#include "gpucrsim/scenario.hpp"
 
 #include <sstream>
 
@@ -211,6 +212,28 @@ uint64_t ref_gen_workload(const char* profile, uint64_t total_bytes, uint64_t p5
   std::string s = os.str();
   if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
   return s.size();
+}
+
+// The reference engine end to end: generate a trace (desk profile with
+// total_bytes override, or a fuzz trace when profile == "fuzz"), checkpoint it
+// with checkpoint_at (scenario.hpp:63-78) at default_trigger (mid-trace
+// iteration boundary), mode 1 = StopTheWorld, 3 = DirtyBitCheckpoint; return the
+// POSI bytes of the image (write_image, image.hpp:136-207).
+uint64_t ref_checkpoint_image(const char* profile, uint64_t total_bytes, uint64_t seed, int mode,
+                              uint8_t* out, uint64_t cap) {
+  std::vector<ApiCall> trace;
+  if (std::string(profile) == "fuzz") {
+    trace = gen_fuzz_trace(seed);
+  } else {
+    WorkloadProfile p = profile_by_name(profile, seed);
+    if (total_bytes) p.total_bytes = total_bytes;
+    trace = gen_workload(p);
+  }
+  SimConfig cfg;
+  auto [img, metrics] = checkpoint_at(trace, default_trigger(trace), static_cast<CrMode>(mode), cfg);
+  std::vector<uint8_t> bytes = write_image(img);
+  if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+  return bytes.size();
 }
 
 }  // extern "C"

@@ -51,6 +51,7 @@ _REF = {
     "ref_state_write": (None, [P, U32, U64, P, U64]),
     "ref_state_captured": (None, [P, U32, P]),
     "ref_gen_workload": (U64, [C.c_char_p, U64, U64, U64, U64, P, U64]),
+    "ref_checkpoint_image": (U64, [C.c_char_p, U64, U64, I32, P, U64]),
 }
 
 
