@@ -399,13 +399,14 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         nbytes = eng.precopy_bytes
         eng.event_record(1, ckpt)
         eng.event_record(8, copy)
-        # final stop: DAG write sets of the window -> dirty_set_, drain the app
-        app_thread.wait()
+        # Stage the delta's layout now (write sets known at submission), so the
+        # stop window holds only the gather; then the final stop: hold the app
+        # (its window is fully submitted) and drain it.
         eng.prepare_final_stop(stream=ckpt)
+        app_thread.wait()
         eng.stream_wait_event(2, ckpt)
         eng.event_record(3, ckpt)
-        doff, dbytes = eng.at_final_stop(stream=ckpt)
-        eng.event_record(4, ckpt)
+        doff, dbytes = eng.at_final_stop(stream=ckpt, stw_end_slot=4)  # STW ends after the gather
         copy.wait(ckpt)
         eng.d2h_async(pin.ptr + doff, doff, dbytes, stream=copy)
         eng.event_record(5, copy)
@@ -437,6 +438,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
              "precopy_bytes": sum(z for _, z in packs), "delta_bytes": dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
              "scan_ms": kms("scan"), "delta_ms": kms("delta") if dbytes > 0 else 0.0,
+             "delta_hash_ms": kms("delta_hash") if dbytes > 0 else 0.0,
              "h2d_bytes": len(bufs) + 64 + 16 * (dbytes // CHUNK + 1)}
         eng.commit_epoch()
         return r
@@ -532,7 +534,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                           "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run",
                           "achieved_over": "pre-copy pack D2H window (first wave copy -> last wave byte)"},
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
-                          for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "d2h_ms")},
+                          for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "delta_hash_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": int(statistics.mean(r["h2d_bytes"] for r in e2e_res)),
                     "d2h_bytes_per_step": int(statistics.mean(r["precopy_bytes"] + r["delta_bytes"] + 24

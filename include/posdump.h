@@ -157,10 +157,15 @@ int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, v
 
 /* ---- STW delta-copy --------------------------------------------------- */
 /* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is
- * hashed and copied into the cache as a second POSD pack starting at
- * *pack_offset (256-B aligned, after the pre-copy pack), refreshing their
- * digests.  Asynchronous on `stream`. */
+ * gathered into the cache as a second POSD pack starting at *pack_offset
+ * (256-B aligned, after the pre-copy pack).  The stop-the-world part is a
+ * pure TMA bulk gather; the chunks are hashed afterwards from the gathered
+ * copy (entry crcs + refreshed digests), on the same stream.  Asynchronous. */
 int pos_delta_copy(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes);
+/* Same, recording event `stw_end_slot` (>= 0) right after the gather: the end
+ * of the stop-the-world window. */
+int pos_delta_copy_ex(pos_ctx* ctx, void* stream, int stw_end_slot, uint64_t* pack_offset,
+                      uint64_t* pack_bytes);
 /* Stage the delta pack's header and work list ahead of the stop (the DAG
  * write sets are known at submission, process.hpp:313-344), so the STW window
  * holds only the kernel.  pos_delta_copy re-stages if dirty_set_ or the

@@ -112,6 +112,7 @@ SIGNATURES = {
     "pos_precopy_size": [P, PU64],
     "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
     "pos_delta_copy": [P, P, PU64, PU64],
+    "pos_delta_copy_ex": [P, P, I32, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],
     "pos_cache_info": [P, PU64, PU64],

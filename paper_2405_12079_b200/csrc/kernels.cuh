@@ -1,7 +1,9 @@
 // kernels.cuh -- sm_100a kernels of the buffer-dump hot path.
 //
-//   k_hash_chunks<COPY>  O2 digest + dirty bitmap (COPY=false), or the STW
-//                        delta-copy: digest + gather into a POSD pack (COPY=true)
+//   k_hash_chunks<MODE>  O2 digest + dirty bitmap (kModeHash), digest + gather
+//                        into a POSD pack (kModeCopy), or digest of chunks
+//                        already gathered into a pack (kModeCached: the STW
+//                        delta is a pure bulk gather; its hashing runs after)
 //   k_buffer_crc         O1: whole-buffer CRC folded from chunk digests + verdict
 //   k_pack_scan          deterministic (handle, chunk)-ordered pack layout
 //   k_copy_bulk          TMA bulk copies (cp.async.bulk) staged through smem
@@ -309,10 +311,15 @@ __device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* 
   __syncthreads();
 }
 
-// O2 (COPY=false): every chunk -> digest, dirty flag, bitmap bit.
-// STW delta-copy (COPY=true): every work item -> digest + pack entry + payload.
-template <bool COPY, int kThreads = kHashThreads, int kUnroll = kUnrollDefault>
+enum : int { kModeHash = 0, kModeCopy = 1, kModeCached = 2 };
+
+// kModeHash: every chunk -> digest, dirty flag, bitmap bit.
+// kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
+// kModeCached: every work item's payload, already in the pack -> digest + entry.
+template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault>
 __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
+  constexpr bool COPY = MODE == kModeCopy;
+  constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
   load_hash_tables(smem, p.tables);
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
     const uint32_t seg = p.nseg == 1 ? 0u : (uint32_t)(it % p.nseg);
     uint64_t g, dst_off = 0;
     uint32_t entry = 0;
-    if (COPY) {
+    if (WORK) {
       uint4 w = p.work[item];
       g = w.x;
       entry = w.y;
@@ -343,12 +350,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
     const uint64_t len = last ? b.size - start : p.chunk_size;
     const uint32_t k_len = last ? b.k_tail : p.k_full;
     uint8_t* dst = COPY ? p.pack + p.payload_off + dst_off : nullptr;
+    // kModeCached reads the gathered copy (16-B aligned) instead of the live buffer.
+    const uint64_t src = MODE == kModeCached ? (uint64_t)(p.pack + p.payload_off + dst_off) : b.ptr + start;
     uint32_t crc;
     // Whole chunk (nseg == 1), or this warp's segment: raw register (init 0)
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
-    const uint32_t r = n ? warp_crc32<COPY, kUnroll>(small, p.xinv, lsel, lane, b.ptr + start + lo, n,
+    const uint32_t r = n ? warp_crc32<COPY, kUnroll>(small, p.xinv, lsel, lane, src + lo, n,
                                             p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
                          : 0u;
     if (p.nseg == 1) {
@@ -379,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
     }
     if (lane == 31) {
       p.digest_cur[g] = crc;
-      if (COPY) {
+      if (WORK) {
         uint4* e = reinterpret_cast<uint4*>(p.pack + kPackHeader + (uint64_t)entry * kPackEntry);
         e[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)dst_off,
                           (uint32_t)(dst_off >> 32));

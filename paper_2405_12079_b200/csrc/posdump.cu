@@ -120,7 +120,7 @@ int hash_threads() {
   }
 }
 
-template <bool COPY>
+template <int COPY>
 void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
   switch (hash_cfg()) {
     case kCfg256x16: k_hash_chunks<COPY, 256, 16><<<grid, 256, kHashSmem, s>>>(p); break;
@@ -129,7 +129,7 @@ void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
   }
 }
 
-template <bool COPY>
+template <int COPY>
 void set_hash_smem() {
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
@@ -154,8 +154,9 @@ struct CrcTables {
     ck(cudaMemcpy(tables.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "upload tables");
     ck(cudaMemcpy(xinv.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice), "upload xinv");
     ck(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
-    set_hash_smem<false>();
-    set_hash_smem<true>();
+    set_hash_smem<kModeHash>();
+    set_hash_smem<kModeCopy>();
+    set_hash_smem<kModeCached>();
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
   }
@@ -170,8 +171,10 @@ void require_device(int device) {
   ck(cudaSetDevice(device), "cudaSetDevice");
 }
 
-enum TimerId { kTimHash = 0, kTimCombine, kTimScan, kTimCopy, kTimDelta, kTimScatter, kTimD2H, kTimCount };
-const char* kTimerNames[kTimCount] = {"hash", "combine", "scan", "copy", "delta", "scatter", "d2h"};
+enum TimerId {
+  kTimHash = 0, kTimCombine, kTimScan, kTimCopy, kTimDelta, kTimScatter, kTimD2H, kTimDeltaHash, kTimCount
+};
+const char* kTimerNames[kTimCount] = {"hash", "combine", "scan", "copy", "delta", "scatter", "d2h", "delta_hash"};
 
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -214,6 +217,8 @@ struct pos_ctx {
   bool delta_ready = false;
   uint64_t delta_version = 0, delta_precopy = 0, delta_n = 0, delta_offset = 0, delta_total = 0,
            delta_payload_off = 0;
+  bool delta_aligned = true;
+  DevArray<CopyItem> d_delta_items;
   // O3 cache
   DevArray<uint8_t> cache;
   uint64_t cache_cap = 0;
@@ -277,6 +282,11 @@ void upload_dag_flags(pos_ctx* c, cudaStream_t s) {
 void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
                  bool aligned, cudaStream_t s) {
   int sms = c->crc.sm_count;
+  static const bool force_simt = [] {
+    const char* e = std::getenv("POSDUMP_COPY");
+    return e && !std::strcmp(e, "simt");
+  }();
+  if (force_simt) aligned = false;
   if (aligned) {
     // 3 CTAs/SM fit in smem (64 KiB ring each); one elected thread per CTA.
     int grid = sms * 3;
@@ -396,6 +406,7 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_seg_cnt.release();
   c->cache.release();
   c->d_items.release();
+  c->d_delta_items.release();
   c->d_scan.release();
   c->d_work.release();
   c->d_err.release();
@@ -585,7 +596,7 @@ int pos_hash_chunks(pos_ctx* c, void* stream) {
     set_segments(c, c->n_chunks, p);
     int grid = c->hash_grid(c->n_chunks * p.nseg);
     c->timer_begin(kTimHash, s);
-    launch_hash<false>(grid, s, p);
+    launch_hash<kModeHash>(grid, s, p);
     check_launch("k_hash_chunks");
     c->timer_end(kTimHash, s);
     ++c->launches;
@@ -763,7 +774,7 @@ static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uin
   set_segments(c, hi - lo, p);
   int grid = c->hash_grid((hi - lo) * p.nseg);
   ck(cudaEventRecord(c->wave_hash[wave][0], s), "event");
-  launch_hash<false>(grid, s, p);
+  launch_hash<kModeHash>(grid, s, p);
   check_launch("k_hash_chunks");
   ck(cudaEventRecord(c->wave_hash[wave][1], s), "event");
   ++c->launches;
@@ -862,29 +873,35 @@ int pos_precopy_size(pos_ctx* c, uint64_t* pack_bytes) {
 static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   const uint64_t cs = c->cfg.chunk_size;
   // at_final_stop: every buffer of dirty_set_ in the snapshot, ascending handle.
+  const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
   std::vector<uint4> work;
+  std::vector<CopyItem> items;
   uint64_t payload = 0;
   uint32_t entry = 0;
+  bool aligned = cs % 16 == 0;
   for (uint64_t h : c->dirty_set) {
     uint32_t i = c->index_of.at(h);
     const DevBuf& b = c->hbufs[i];
+    aligned = aligned && (b.ptr % 16 == 0);
     for (uint32_t k = 0; k < b.nchunks; ++k) {
       uint64_t len = k + 1 == b.nchunks ? b.size - (uint64_t)k * cs : cs;
       uint64_t g = c->chunk_base[i] + k;
       work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
+      items.push_back(CopyItem{b.ptr + (uint64_t)k * cs, 0, len, round_up(len, 16)});
+      items.back().dst = payload;  // relative; rebased below
       payload += round_up(len, 16);
     }
   }
   const uint64_t n = work.size();
   const uint64_t payload_off = round_up(kPackHeader + kPackEntry * n, kPackAlign);
   const uint64_t total = payload_off + payload;
-  const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
   if (offset + total > c->cache_cap) fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
-  // Stage the header (+ zero gap up to the payload) and the work list.
-  const uint64_t hdr_bytes = payload_off;
-  const uint64_t work_bytes = n * sizeof(uint4);
+  uint8_t* pack = c->cache.p + offset;
+  for (auto& it : items) it.dst = (uint64_t)pack + payload_off + it.dst;
+  // Stage the header, the work list (for the post-stop hash) and the gather items.
+  const uint64_t work_bytes = n * sizeof(uint4), item_bytes = n * sizeof(CopyItem);
   if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
-  c->h_stage.ensure(hdr_bytes + work_bytes);
+  c->h_stage.ensure(kPackHeader + work_bytes + item_bytes);
   uint8_t* st = c->h_stage.p;
   std::memset(st, 0, kPackHeader);
   uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)n, flags = 1;
@@ -897,14 +914,22 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   std::memcpy(st + 32, &payload, 8);
   std::memcpy(st + 40, &c->epoch, 8);
   std::memcpy(st + 48, &total, 8);
-  if (n) std::memcpy(st + hdr_bytes, work.data(), work_bytes);
-  uint8_t* pack = c->cache.p + offset;
-  // Only the header and the entry gap go up; the kernel writes the entries.
+  if (n) {
+    std::memcpy(st + kPackHeader, work.data(), work_bytes);
+    std::memcpy(st + kPackHeader + work_bytes, items.data(), item_bytes);
+  }
+  // The kernels write the entries and the payload; the header and the gap go up now.
   ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
-  if (hdr_bytes > kPackHeader + kPackEntry * n)
-    ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0, hdr_bytes - kPackHeader - kPackEntry * n, s),
+  if (payload_off > kPackHeader + kPackEntry * n)
+    ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0, payload_off - kPackHeader - kPackEntry * n, s),
        "gap");
-  if (n) ck(cudaMemcpyAsync(c->d_work.p, st + hdr_bytes, work_bytes, cudaMemcpyHostToDevice, s), "work");
+  if (n) {
+    c->d_delta_items.ensure(n);
+    ck(cudaMemcpyAsync(c->d_work.p, st + kPackHeader, work_bytes, cudaMemcpyHostToDevice, s), "work");
+    ck(cudaMemcpyAsync(c->d_delta_items.p, st + kPackHeader + work_bytes, item_bytes,
+                       cudaMemcpyHostToDevice, s),
+       "items");
+  }
   ck(cudaEventRecord(c->stage_free, s), "event");
   c->delta_ready = true;
   c->delta_version = c->dirty_version;
@@ -913,6 +938,7 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   c->delta_offset = offset;
   c->delta_total = total;
   c->delta_payload_off = payload_off;
+  c->delta_aligned = aligned;
 }
 
 static bool delta_current(const pos_ctx* c) {
@@ -930,13 +956,25 @@ int pos_delta_prepare(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t*
 }
 
 int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes) {
+  return pos_delta_copy_ex(c, stream, -1, pack_offset, pack_bytes);
+}
+
+int pos_delta_copy_ex(pos_ctx* c, void* stream, int stw_end_slot, uint64_t* pack_offset,
+                      uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (stw_end_slot >= (int)c->events.size()) fail(POS_E_INVALID_ARGUMENT, "bad event slot");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     cudaStream_t s = S(stream);
     if (!delta_current(c)) delta_prepare(c, s);
     c->delta_ready = false;  // one launch per preparation
     const uint64_t n = c->delta_n, cs = c->cfg.chunk_size;
+    // Stop-the-world part: a pure TMA bulk gather of the flagged buffers.
+    c->timer_begin(kTimDelta, s);
+    if (n) launch_copy(c, c->d_delta_items.p, nullptr, n, c->delta_aligned, s);
+    c->timer_end(kTimDelta, s);
+    if (stw_end_slot >= 0) ck(cudaEventRecord(c->events[stw_end_slot], s), "event");
+    // After the stop: hash the gathered copy -> entry crcs + refreshed digests.
     if (n) {
       HashParams p{};
       p.bufs = c->d_bufs.p;
@@ -952,10 +990,10 @@ int pos_delta_copy(pos_ctx* c, void* stream, uint64_t* pack_offset, uint64_t* pa
       p.payload_off = c->delta_payload_off;
       set_segments(c, n, p);
       int grid = c->hash_grid(n * p.nseg);
-      c->timer_begin(kTimDelta, s);
-      launch_hash<true>(grid, s, p);
-      check_launch("k_hash_chunks<copy>");
-      c->timer_end(kTimDelta, s);
+      c->timer_begin(kTimDeltaHash, s);
+      launch_hash<kModeCached>(grid, s, p);
+      check_launch("k_hash_chunks<cached>");
+      c->timer_end(kTimDeltaHash, s);
       ++c->launches;
     }
     if (pack_offset) *pack_offset = c->delta_offset;
@@ -1098,7 +1136,7 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
       p.seg_bytes = (uint32_t)cs;
       uint64_t blocks = (nc + 15) / 16;
       int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)t.sm_count));
-      launch_hash<false>(grid, s, p);
+      launch_hash<kModeHash>(grid, s, p);
       check_launch("k_hash_chunks");
       k_buffer_crc<<<1, 32, 0, s>>>(db.p, 1, dd.p, dt.p, dz.p, 0, 1, dc.p, dz.p + 1);
       check_launch("k_buffer_crc");
@@ -1183,7 +1221,7 @@ int pos_stream_wait_event(pos_ctx* c, uint32_t slot, void* stream) {
 int pos_timeline(pos_ctx* c, uint32_t slot, float* out) {
   return guarded([&] {
     if (!c || !out || slot >= c->events.size()) fail(POS_E_INVALID_ARGUMENT, "bad argument");
-    for (int t = 0; t < kTimCount; ++t) {
+    for (int t = 0; t < 7; ++t) {
       out[2 * t] = out[2 * t + 1] = -1.f;
       if (!c->timers[t].used) continue;
       ck(cudaEventSynchronize(c->timers[t].b), "event sync");

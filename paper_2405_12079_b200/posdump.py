@@ -365,9 +365,11 @@ class DumpEngine:
         return n.value
 
     # ---- STW delta-copy (at_final_stop, cr.hpp:599-621)
-    def at_final_stop(self, stream=None) -> tuple[int, int]:
+    def at_final_stop(self, stream=None, stw_end_slot: int = -1) -> tuple[int, int]:
+        """STW delta pack: bulk gather (records event stw_end_slot when >= 0),
+        then the post-stop hash of the gathered copy."""
         off, n = C.c_uint64(0), C.c_uint64(0)
-        check(lib().pos_delta_copy(self.ctx, _s(stream), C.byref(off), C.byref(n)))
+        check(lib().pos_delta_copy_ex(self.ctx, _s(stream), stw_end_slot, C.byref(off), C.byref(n)))
         return off.value, n.value
 
     def prepare_final_stop(self, stream=None) -> tuple[int, int]:
