@@ -75,15 +75,13 @@ struct HashParams {
   const uint4* work;         // {g, entry, dst_off lo, dst_off hi}
   uint8_t* pack;             // pack base
   uint64_t payload_off;      // payload offset within the pack
-  // Segmented chunks (nseg > 1): warp unit = (item, segment of seg_bytes);
-  // the last segment to finish folds the segment registers.
+  // Segmented chunks (nseg > 1, divides the warps per CTA): warp unit =
+  // (item, segment of seg_bytes); a CTA-local group of warps folds them.
   uint32_t nseg;
   uint32_t seg_bytes;
   uint64_t item_base;        // hash mode: first global chunk of this launch
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
   const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
-  uint32_t* seg_raw;         // [n_chunks * nseg]
-  uint32_t* seg_cnt;         // [n_chunks], zero between launches
 };
 
 // Hash kernel geometry.
@@ -185,7 +183,7 @@ __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
 // with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
 // which leaves a register that starts at 0 unchanged.  COPY: every loaded
 // vector is also stored at dst (only when src is 16-B aligned).
-template <bool COPY, int kUnroll>
+template <bool COPY, int kUnroll, bool kRoll>
 __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
                                                const uint32_t* xinv, uint32_t lsel, int lane,
                                                uint64_t src, uint64_t len, uint32_t k_len,
@@ -240,7 +238,45 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
     hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
     if (hi) l2_prefetch(reinterpret_cast<const void*>(a0), (uint32_t)hi);
   }
-  if (blk + kUnroll <= full_end) {
+  if (kRoll) {
+    // Rolling pipeline: a ring of kUnroll in-flight steps; the load for step
+    // i + kUnroll is issued the moment step i's registers are read, so the
+    // warp keeps a constant kUnroll x 512 B in flight instead of draining a
+    // whole batch before refilling it.
+    const uint64_t nsteps = full_end - blk;
+    uint4 ring[kUnroll];
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j)
+      if ((uint64_t)j < nsteps) ring[j] = ldg_stream(base + (blk + j) * 32);
+    uint64_t done = 0;
+    while (done + kUnroll <= nsteps) {
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) {
+        const uint4 v = ring[j];
+        const uint64_t nxt = done + kUnroll + j;
+        if (nxt < nsteps) ring[j] = ldg_stream(base + (blk + nxt) * 32);
+        if (vec_copy) stg_stream(dbase + (blk + done + j) * 32, v);
+        c0 = adv512(lsel, c0 ^ v.x);
+        c1 = adv512(lsel, c1 ^ v.y);
+        c2 = adv512(lsel, c2 ^ v.z);
+        c3 = adv512(lsel, c3 ^ v.w);
+      }
+      done += kUnroll;
+    }
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      if (done + j < nsteps) {
+        const uint4 v = ring[j];
+        if (vec_copy) stg_stream(dbase + (blk + done + j) * 32, v);
+        c0 = adv512(lsel, c0 ^ v.x);
+        c1 = adv512(lsel, c1 ^ v.y);
+        c2 = adv512(lsel, c2 ^ v.z);
+        c3 = adv512(lsel, c3 ^ v.w);
+      }
+    }
+    blk = full_end;
+  }
+  if (!kRoll && blk + kUnroll <= full_end) {
     uint4 bufA[kUnroll], bufB[kUnroll];
     load_batch(bufA, blk);
     for (;;) {
@@ -316,7 +352,7 @@ enum : int { kModeHash = 0, kModeCopy = 1, kModeCached = 2 };
 // kModeHash: every chunk -> digest, dirty flag, bitmap bit.
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
-template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault>
+template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault, bool kRoll = false>
 __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;
@@ -325,14 +361,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
   const uint32_t lsel = (uint32_t)lane * 4 | kRepAbs;
-  // Item i goes to CTA i % grid, warp (i / grid) % 16: consecutive items land
-  // on different SMs, so a short list still spreads over the whole chip.
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kThreads / 32);
-  const uint64_t n_units = p.n_items * p.nseg;
-  for (uint64_t it = (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x; it < n_units;
-       it += nwarps) {
-    const uint64_t item = p.nseg == 1 ? it : it / p.nseg;
-    const uint32_t seg = p.nseg == 1 ? 0u : (uint32_t)(it % p.nseg);
+  // nseg == 1: item i goes to CTA i % grid, warp (i / grid) % W, so a short
+  // list still spreads over every SM.  nseg > 1: the nseg segments of a chunk
+  // go to nseg consecutive warps of ONE CTA (a "group"), which fold their
+  // segment registers through shared memory behind a named barrier; groups
+  // are dealt round-robin over CTAs.
+  constexpr int W = kThreads / 32;
+  __shared__ uint32_t s_seg[2][W];
+  const int warp = threadIdx.x >> 5;
+  const uint32_t nseg = p.nseg;
+  const uint32_t G = W / nseg;                       // groups per CTA
+  const uint32_t my_group = warp / nseg, my_seg = warp % nseg;
+  const uint64_t n_units = p.n_items * nseg;
+  uint64_t it, stride;
+  if (nseg == 1) {
+    it = (uint64_t)warp * gridDim.x + blockIdx.x;
+    stride = (uint64_t)gridDim.x * W;
+  } else {
+    it = ((uint64_t)my_group * gridDim.x + blockIdx.x) * nseg + my_seg;
+    stride = (uint64_t)gridDim.x * G * nseg;
+  }
+  for (uint32_t round = 0; it < n_units; it += stride, ++round) {
+    const uint64_t item = nseg == 1 ? it : it / nseg;
+    const uint32_t seg = nseg == 1 ? 0u : my_seg;
     uint64_t g, dst_off = 0;
     uint32_t entry = 0;
     if (WORK) {
@@ -357,34 +408,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
-    const uint32_t r = n ? warp_crc32<COPY, kUnroll>(small, p.xinv, lsel, lane, src + lo, n,
+    const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll>(small, p.xinv, lsel, lane, src + lo, n,
                                             p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
                          : 0u;
-    if (p.nseg == 1) {
+    if (nseg == 1) {
       crc = r;
     } else {
-      const uint32_t raw = r;
-      uint32_t old = 0;
-      if (lane == 31) {
-        p.seg_raw[g * p.nseg + seg] = raw;
-        __threadfence();
-        old = atomicAdd(p.seg_cnt + g, 1u);
-      }
-      old = __shfl_sync(0xffffffffu, old, 31);
-      if (old != p.nseg - 1) continue;  // not the last segment of this chunk
-      __threadfence();
       // raw(chunk) = XOR_s Z^(len - end_s)(raw_s); segments past the tail are empty.
+      uint32_t* slot = s_seg[round & 1] + my_group * nseg;
+      if (lane == 31) slot[seg] = r;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + my_group), "r"(nseg * 32) : "memory");
+      if (seg != 0) continue;  // the group's first warp folds and publishes
       const uint32_t m = (uint32_t)((len - 1) / p.seg_bytes);  // last non-empty segment
       const uint32_t xl = len == p.chunk_size ? p.xseg[1] : p.lastseg[cm.x];
       uint32_t v = 0;
       if ((uint32_t)lane <= m) {
-        v = __ldcg(p.seg_raw + g * p.nseg + lane);
+        v = slot[lane];
         if ((uint32_t)lane < m) v = multmodp(p.xseg[m - 1 - lane], multmodp(xl, v));
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
       crc = v ^ k_len;
-      if (lane == 31) p.seg_cnt[g] = 0;
     }
     if (lane == 31) {
       p.digest_cur[g] = crc;

@@ -99,7 +99,7 @@ struct PinnedArray {
 
 // Hash kernel variants (threads per CTA x warp steps per batch); one CTA per
 // SM either way.  POSDUMP_HASH_CFG selects one for tuning runs.
-enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12 };
+enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12, kCfg512r12, kCfg512r16, kCfg256r24 };
 
 HashCfg hash_cfg() {
   static const HashCfg c = [] {
@@ -107,6 +107,9 @@ HashCfg hash_cfg() {
     if (!e) return kCfg512x8;
     if (!std::strcmp(e, "256x16")) return kCfg256x16;
     if (!std::strcmp(e, "384x12")) return kCfg384x12;
+    if (!std::strcmp(e, "512r12")) return kCfg512r12;
+    if (!std::strcmp(e, "512r16")) return kCfg512r16;
+    if (!std::strcmp(e, "256r24")) return kCfg256r24;
     return kCfg512x8;
   }();
   return c;
@@ -115,6 +118,7 @@ HashCfg hash_cfg() {
 int hash_threads() {
   switch (hash_cfg()) {
     case kCfg256x16: return 256;
+    case kCfg256r24: return 256;
     case kCfg384x12: return 384;
     default: return 512;
   }
@@ -125,6 +129,9 @@ void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
   switch (hash_cfg()) {
     case kCfg256x16: k_hash_chunks<COPY, 256, 16><<<grid, 256, kHashSmem, s>>>(p); break;
     case kCfg384x12: k_hash_chunks<COPY, 384, 12><<<grid, 384, kHashSmem, s>>>(p); break;
+    case kCfg512r12: k_hash_chunks<COPY, 512, 12, true><<<grid, 512, kHashSmem, s>>>(p); break;
+    case kCfg512r16: k_hash_chunks<COPY, 512, 16, true><<<grid, 512, kHashSmem, s>>>(p); break;
+    case kCfg256r24: k_hash_chunks<COPY, 256, 24, true><<<grid, 256, kHashSmem, s>>>(p); break;
     default: k_hash_chunks<COPY, 512, 8><<<grid, 512, kHashSmem, s>>>(p); break;
   }
 }
@@ -134,6 +141,9 @@ void set_hash_smem() {
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 384, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
 }
 
 // Tables shared by every launch on a device: Z^512 (replicated in smem by the
@@ -208,7 +218,7 @@ struct pos_ctx {
   // level L = log2(nseg): x^(8 k cs/2^L) (32 per level) and, per buffer,
   // x^(8 * last segment length of the tail chunk); valid_levels bitmask.
   uint32_t seg_levels = 1;
-  DevArray<uint32_t> d_xseg, d_lastseg, d_seg_raw, d_seg_cnt;
+  DevArray<uint32_t> d_xseg, d_lastseg;
   DevArray<uint64_t> d_result;  // async pre-copy: [n, total, overflow, n_items]
   std::set<uint64_t> dirty_set;
   bool dag_uploaded = false;
@@ -402,8 +412,6 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_xseg.release();
   c->d_lastseg.release();
   c->d_result.release();
-  c->d_seg_raw.release();
-  c->d_seg_cnt.release();
   c->cache.release();
   c->d_items.release();
   c->d_delta_items.release();
@@ -492,10 +500,6 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
       c->d_lastseg.ensure(ls.size());
       ck(cudaMemcpy(c->d_xseg.p, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice), "xseg");
       ck(cudaMemcpy(c->d_lastseg.p, ls.data(), ls.size() * 4, cudaMemcpyHostToDevice), "lastseg");
-      uint32_t nseg = 1u << (c->seg_levels - 1);
-      c->d_seg_raw.ensure(std::max<uint64_t>(g, 1) * nseg);  // enough for any level
-      c->d_seg_cnt.ensure(std::max<uint64_t>(g, 1));
-      ck(cudaMemset(c->d_seg_cnt.p, 0, std::max<uint64_t>(g, 1) * 4), "memset");
     }
     std::vector<uint2> cmap(g);
     for (uint32_t i = 0; i < n; ++i)
@@ -555,22 +559,22 @@ int pos_num_chunks(pos_ctx* c, uint64_t* out) {
 // cannot give every warp of the grid one chunk (measured: splitting a list
 // that already covers half the warps costs more than it balances).
 static void set_segments(const pos_ctx* c, uint64_t items, HashParams& p) {
-  const uint64_t warps = (uint64_t)c->crc.sm_count * (hash_threads() / 32);
+  const uint32_t wpc = (uint32_t)(hash_threads() / 32);  // warps per CTA: nseg must divide it
+  const uint64_t warps = (uint64_t)c->crc.sm_count * wpc;
+  auto ok = [&](int L) { return L < (int)c->seg_levels && wpc % (1u << L) == 0; };
   int L = 0;
   if (items < warps / 2)
-    while (L + 1 < (int)c->seg_levels && (items << L) < warps) ++L;
+    while (ok(L + 1) && (items << L) < warps) ++L;
   if (const char* e = std::getenv("POSDUMP_NSEG")) {  // tuning override
     int want = 0;
     for (unsigned v = (unsigned)std::strtoul(e, nullptr, 10); v > 1; v >>= 1) ++want;
-    if (want < (int)c->seg_levels) L = want;
+    if (ok(want)) L = want;
   }
   const uint32_t nb = (uint32_t)std::max<size_t>(c->bufs.size(), 1);
   p.nseg = 1u << L;
   p.seg_bytes = (uint32_t)(c->cfg.chunk_size >> L);
   p.xseg = c->d_xseg.p + 32 * L;
   p.lastseg = c->d_lastseg.p + (size_t)nb * L;
-  p.seg_raw = c->d_seg_raw.p;
-  p.seg_cnt = c->d_seg_cnt.p;
 }
 
 int pos_hash_chunks(pos_ctx* c, void* stream) {
