@@ -151,6 +151,19 @@ int pos_precopy_size(pos_ctx* ctx, uint64_t* pack_bytes);
  * the hashing of wave k+1.  offsets[] / sizes[] (capacity 16) receive each
  * pack's cache offset and size; returns after the last scan (copies may still
  * be in flight on copy_stream). */
+/* Cache-cycled pre-copy for states larger than the O3 cache (BASELINE
+ * configs 3 and 5): the chunks are cut into waves whose worst-case pack fits
+ * one of two cache regions of region_bytes (0 => half the cache); wave w
+ * hashes/compacts into region w%2 while wave w-1 drains over PCIe into one of
+ * two pinned landing slots owned by the context; `sink` receives each pack
+ * (valid during the call) on the calling thread, in order.  Blocks until the
+ * last pack was handed over.  O1 verdicts are decided in the wave holding a
+ * buffer's last chunk (a dedup candidate larger than a region may ship chunks
+ * it could have skipped; the image is unaffected). */
+typedef void (*pos_pack_sink)(void* user, const uint8_t* pack, uint64_t bytes, uint32_t index);
+int pos_precopy_stream(pos_ctx* ctx, int exclude_dag_dirty, void* ckpt_stream, void* copy_stream,
+                       uint64_t region_bytes, pos_pack_sink sink, void* user, uint64_t* total_bytes,
+                       uint32_t* n_packs);
 int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                           void* copy_stream, void* host_dst, uint64_t slice_bytes,
                           uint64_t* offsets, uint64_t* sizes, uint32_t* n_packs);

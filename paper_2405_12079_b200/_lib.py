@@ -111,6 +111,7 @@ SIGNATURES = {
     "pos_precopy": [P, I32, P],
     "pos_precopy_size": [P, PU64],
     "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
+    "pos_precopy_stream": [P, I32, P, P, U64, P, P, PU64, PU32],
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_delta_copy_ex": [P, P, I32, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
@@ -144,6 +145,9 @@ SIGNATURES = {
     "pos_device_sync": [],
     "pos_stream_wait": [P, P],
 }
+# void (*pos_pack_sink)(void* user, const uint8_t* pack, uint64_t bytes, uint32_t index)
+PACK_SINK = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_uint8), C.c_uint64, C.c_uint32)
+
 _RESTYPE = {"pos_strerror": C.c_char_p, "pos_last_error": C.c_char_p}
 
 

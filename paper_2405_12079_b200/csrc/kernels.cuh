@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     uint64_t seq /* written last into result_host[5] */,
     // fused O1 (k_buffer_crc for buffers [vb0, vb1) with upstream provenance):
     uint32_t vb0, uint32_t vb1, const uint32_t* tcs, int dedup, uint32_t* crc_out,
-    uint8_t* verdict_out) {
+    uint8_t* verdict_out, uint64_t fixed_base /* ~0 = use the cursor */) {
   __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
   const int t = threadIdx.x;
   if (vb1 > vb0) {
@@ -521,8 +521,8 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     __syncthreads();
   }
   // The pack goes at the running cache cursor (packs of earlier waves end
-  // there); items are written at [0, N) of `items`.
-  const uint64_t base = *cursor;
+  // there) or at a fixed region (cache cycling); items are written at [0, N).
+  const uint64_t base = fixed_base != ~0ull ? fixed_base : *cursor;
   uint8_t* pack = cache + base;
   const uint64_t n_chunks = chunk_hi - chunk_lo;
   const uint64_t per = (n_chunks + kScanThreads - 1) / kScanThreads;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     result[2] = overflow;
     result[3] = overflow ? 0 : N;  // items for the copy kernel
     result[4] = base;
-    if (!overflow) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
+    if (!overflow && fixed_base == ~0ull) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
     if (result_host) {
       result_host[0] = N;
       result_host[1] = total;

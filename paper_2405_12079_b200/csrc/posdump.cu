@@ -249,6 +249,9 @@ struct pos_ctx {
   cudaEvent_t wave_hash[kMaxWaves][2] = {};
   uint32_t waves_last = 0;                          // waves of the last pre-copy (hash timing)
   uint64_t scan_seq = 0, slot_seq[kMaxWaves] = {};  // host-mirror sequence numbers
+  // cache-cycled pre-copy (pos_precopy_stream): 2 cache regions, 2 pinned landing slots
+  PinnedArray<uint8_t> h_land[2];
+  cudaEvent_t ev_d2h[2] = {}, ev_copied2[2] = {};
   bool pack_pending = false;
   // timing
   std::vector<cudaEvent_t> events;
@@ -429,6 +432,12 @@ int pos_ctx_destroy(pos_ctx* c) {
     if (c->wave_hash[w][1]) cudaEventDestroy(c->wave_hash[w][1]);
   }
   c->d_cursor.release();
+  c->h_land[0].release();
+  c->h_land[1].release();
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+    if (c->ev_copied2[i]) cudaEventDestroy(c->ev_copied2[i]);
+  }
   for (auto& t : c->timers) {
     if (t.a) cudaEventDestroy(t.a);
     if (t.b) cudaEventDestroy(t.b);
@@ -700,7 +709,7 @@ int pos_clear_dirty(pos_ctx* c) {
 // scan's device-side result, which is mirrored into pinned memory behind
 // event scanned[slot] for pack_result().
 static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
-                        uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0) {
+                        uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0, uint64_t fixed_base = ~0ull) {
   upload_dag_flags(c, s);
   uint64_t* res = c->d_scan.p + 8 * slot;
   c->timer_begin(kTimScan, s);
@@ -708,7 +717,7 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
       c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
       c->cache_cap, c->d_cursor.p, c->d_items.p, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
-      c->d_tcs.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p);
+      c->d_tcs.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base);
   c->slot_seq[slot] = c->scan_seq;
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
@@ -863,6 +872,98 @@ int pos_precopy_pipelined(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, voi
     c->pack_pending = false;
     c->precopy_bytes = end;
     *n_packs = W;
+  });
+}
+
+int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, void* copy_stream,
+                       uint64_t region, pos_pack_sink sink, void* user, uint64_t* total_bytes,
+                       uint32_t* n_packs) {
+  return guarded([&] {
+    if (!c || !sink) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(ckpt_stream), cs = S(copy_stream);
+    if (region == 0) region = c->cache_cap / 2;
+    region = region / kPackAlign * kPackAlign;
+    if (2 * region > c->cache_cap) fail(POS_E_INVALID_ARGUMENT, "two regions must fit the cache");
+    const uint64_t csz = c->cfg.chunk_size;
+    const uint32_t nb = (uint32_t)c->bufs.size();
+    // Waves = chunk ranges whose worst-case pack (every chunk dirty) fits a region.
+    std::vector<uint64_t> cuts(1, 0);
+    uint64_t acc_n = 0, acc_b = 0;
+    for (uint64_t g = 0; g < c->n_chunks; ++g) {
+      uint32_t bi = 0;  // chunk length from the host tables
+      {
+        auto it = std::upper_bound(c->chunk_base.begin(), c->chunk_base.end(), g);
+        bi = (uint32_t)(it - c->chunk_base.begin()) - 1;
+      }
+      const DevBuf& b = c->hbufs[bi];
+      uint32_t k = (uint32_t)(g - c->chunk_base[bi]);
+      uint64_t len = k + 1 == b.nchunks ? b.size - (uint64_t)k * csz : csz;
+      uint64_t nb_ = acc_b + round_up(len, 16), nn = acc_n + 1;
+      if (round_up(kPackHeader + kPackEntry * nn, kPackAlign) + nb_ > region && acc_n > 0) {
+        cuts.push_back(g);
+        acc_n = 1;
+        acc_b = round_up(len, 16);
+      } else {
+        acc_n = nn;
+        acc_b = nb_;
+      }
+      if (round_up(kPackHeader + kPackEntry * acc_n, kPackAlign) + acc_b > region)
+        fail(POS_E_STAGING_EXHAUSTED, "a single chunk exceeds the cache region");
+    }
+    cuts.push_back(c->n_chunks);
+    const uint32_t W = (uint32_t)cuts.size() - 1;
+    // Buffers whose O1 verdict is decided in wave w: last chunk in [cuts[w], cuts[w+1]).
+    auto vb_of = [&](uint64_t g) {  // first buffer whose last chunk >= g
+      uint32_t b = 0;
+      while (b < nb && c->chunk_base[b] + c->hbufs[b].nchunks <= g) ++b;
+      return b;
+    };
+    c->h_land[0].ensure(region);
+    c->h_land[1].ensure(region);
+    if (!c->ev_d2h[0]) {
+      ck(cudaEventCreateWithFlags(&c->ev_d2h[0], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_d2h[1], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_copied2[0], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_copied2[1], cudaEventDisableTiming), "event");
+    }
+    upload_dag_flags(c, s);
+    ck(cudaMemsetAsync(c->d_verdict.p, 0, std::max<uint32_t>(nb, 1), s), "memset verdicts");
+    if (c->n_chunks)
+      ck(cudaMemsetAsync(c->d_bitmap.p, 0, ((c->n_chunks + 31) / 32) * 4, s), "memset bitmap");
+    std::vector<uint64_t> sizes(W, 0);
+    uint64_t total = 0;
+    auto finish = [&](uint32_t w) {  // wave w's bytes are on the host: hand them over
+      ck(cudaEventSynchronize(c->ev_d2h[w & 1]), "d2h sync");
+      sink(user, c->h_land[w & 1].p, sizes[w], w);
+    };
+    c->timer_begin(kTimHash, s);
+    for (uint32_t w = 0; w < W; ++w) {
+      const uint32_t r = w & 1;
+      if (w >= 2) finish(w - 2);  // frees landing slot r and (its D2H done) cache region r
+      hash_range(c, cuts[w], cuts[w + 1], s, w % pos_ctx::kMaxWaves);
+      if (w >= 2) ck(cudaStreamWaitEvent(s, c->ev_d2h[r], 0), "wait region");  // before writing region r
+      const uint32_t slot = w % pos_ctx::kMaxWaves;
+      launch_pack(c, exclude_dag_dirty, s, cuts[w], cuts[w + 1], slot, vb_of(cuts[w]), vb_of(cuts[w + 1]),
+                  (uint64_t)r * region);
+      ck(cudaEventRecord(c->ev_copied2[r], s), "event");
+      PackResult res = pack_result(c, slot);
+      sizes[w] = res.total;
+      total += res.total;
+      ck(cudaStreamWaitEvent(cs, c->ev_copied2[r], 0), "wait copy");
+      for (uint64_t o = 0; o < res.total; o += 8ull << 20)
+        ck(cudaMemcpyAsync(c->h_land[r].p + o, c->cache.p + res.base + o, std::min<uint64_t>(8ull << 20, res.total - o),
+                           cudaMemcpyDeviceToHost, cs),
+           "d2h");
+      ck(cudaEventRecord(c->ev_d2h[r], cs), "event");
+    }
+    c->timer_end(kTimHash, s);
+    for (uint32_t w = W >= 2 ? W - 2 : 0; w < W; ++w) finish(w);
+    c->pack_pending = false;
+    c->precopy_bytes = 0;  // every pack has left the cache
+    c->waves_last = std::min<uint32_t>(W, pos_ctx::kMaxWaves);
+    if (total_bytes) *total_bytes = total;
+    if (n_packs) *n_packs = W;
   });
 }
 

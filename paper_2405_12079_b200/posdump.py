@@ -358,6 +358,21 @@ class DumpEngine:
             self.precopy_bytes = o + z
         return packs
 
+    def precopy_stream(self, sink, region_bytes: int = 0, stream=None, copy_stream=None,
+                       exclude_dag_dirty: bool = True) -> tuple[int, int]:
+        """Cache-cycled pre-copy (pos_precopy_stream) for states larger than the
+        O3 cache: sink(pack: np.ndarray view, index) is called per wave, in
+        order, while the next wave drains.  Returns (total pack bytes, packs)."""
+        def _cb(user, ptr, nbytes, index):
+            arr = np.ctypeslib.as_array(ptr, shape=(nbytes,)) if nbytes else np.zeros(0, np.uint8)
+            sink(arr, index)
+        cb = _lib.PACK_SINK(_cb)
+        total, n = C.c_uint64(0), C.c_uint32(0)
+        check(lib().pos_precopy_stream(self.ctx, 1 if exclude_dag_dirty else 0, _s(stream), _s(copy_stream),
+                                       region_bytes, C.cast(cb, C.c_void_p), None, C.byref(total), C.byref(n)))
+        self.precopy_bytes = 0
+        return total.value, n.value
+
     def precopy_size(self) -> int:
         n = C.c_uint64(0)
         check(lib().pos_precopy_size(self.ctx, C.byref(n)))

@@ -522,3 +522,39 @@ def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode):
     out.cursor, out.next_handle, out.next_base = m["cursor"], m["next_handle"], m["next_base"]
     assert pd.write_image(out) == want
     eng.close()
+
+
+@pytest.mark.parametrize("region", [300_000, 1 << 20])
+def test_cache_cycled_precopy(orc, region):
+    """States larger than the O3 cache (BASELINE configs 3/5): waves cycle two
+    cache regions; the packs handed to the sink carry exactly the single-pack
+    entries/payload, and verdicts of buffers spanning waves still apply."""
+    cs = 65536
+    sizes = [3 * cs, 10000, 1, 2 * cs + 5, 70001, 5 * cs, 300, cs, 9 * cs + 7]
+    p = Proc(orc, sizes, seed0=4500)
+    p.bufs[1].upstream = pd.Upstream(ocrc(orc, p.host[1]), True)  # dedup-ok
+    p.bufs[8].upstream = pd.Upstream(ocrc(orc, p.host[8]), True)  # dedup-ok, spans waves
+    big = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=64 << 20))
+    big.register_buffers(p.bufs)
+    one = download_cache(big, 0, big.plan_precopy())
+    big.close()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=2 * region + 4096))
+    eng.register_buffers(p.bufs)
+    got = []
+    total, n = eng.precopy_stream(lambda arr, i: got.append((i, arr.copy())), region_bytes=region)
+    assert [i for i, _ in got] == list(range(n)) and n >= 2
+    assert total == sum(a.size for _, a in got)
+    ents = [pd.parse_pack(a) for _, a in got]
+    ref = pd.parse_pack(one)
+    # buffer 9 spans waves: its early chunks may ship before its verdict is known
+    keep = [e["handle"] != 9 for e in ents]
+    for key in ("handle", "chunk", "len", "crc"):
+        a = np.concatenate([e[key][k] for e, k in zip(ents, keep)])
+        assert np.array_equal(a, ref[key]), key
+    img = [np.zeros(n_, np.uint8) for n_ in sizes]
+    for _, a in got:
+        pd.apply_pack_host(a, p.handles, img)
+    for i in range(len(sizes)):
+        if i not in (1, 8):
+            assert np.array_equal(img[i], p.host[i])
+    eng.close()
