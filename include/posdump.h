@@ -208,6 +208,17 @@ int pos_pack_apply_host(const uint8_t* pack, uint64_t pack_bytes, const uint64_t
                         uint8_t* const* hosts, const uint64_t* sizes, uint32_t n,
                         uint32_t threads);
 
+/* Streaming restore (start_loads / load_complete / materialize,
+ * cr.hpp:1043-1084): packs held in host memory (the base image's packs, then
+ * the incremental ones -- delta-restore) are validated on the host (all or
+ * nothing, like write_content, buffer.hpp:80), copied H2D through two cache
+ * regions of region_bytes (0 => half the cache) on h2d_stream, and scattered
+ * onto the registered buffers on `stream` in order, so a later pack overrides
+ * an earlier one.  Pageable packs are staged through pinned landing slots with
+ * the host's threads.  Returns when the last scatter finished. */
+int pos_restore_packs(pos_ctx* ctx, const uint8_t* const* packs, const uint64_t* sizes, uint32_t n,
+                      void* h2d_stream, void* stream, uint64_t region_bytes);
+
 /* ---- device crc32 (crc32.hpp:26-34 over device memory) ---------------- */
 int pos_crc32(uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream);
 int pos_crc32_update(uint32_t crc, uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream);

@@ -118,6 +118,7 @@ SIGNATURES = {
     "pos_d2h_async": [P, P, U64, U64, U64, P],
     "pos_cache_info": [P, PU64, PU64],
     "pos_scatter": [P, U64, U64, P],
+    "pos_restore_packs": [P, P, P, U32, P, P, U64],
     "pos_crc32": [U64, U64, PU32, P],
     "pos_crc32_update": [U32, U64, U64, PU32, P],
     "pos_fill": [U64, U64, U64, P],

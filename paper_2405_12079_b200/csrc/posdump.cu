@@ -1173,6 +1173,109 @@ int pos_scatter(pos_ctx* c, uint64_t pack_dev, uint64_t pack_bytes, void* stream
   });
 }
 
+// Host-side validation of a POSD pack against the registered buffers: the
+// checks write_content makes before it copies (buffer.hpp:80) plus the
+// pack's own section bounds.
+static void validate_pack_host(const pos_ctx* c, const uint8_t* pack, uint64_t bytes) {
+  if (bytes < kPackHeader) fail(POS_E_CORRUPT_IMAGE, "pack shorter than its header");
+  uint32_t magic, n;
+  uint64_t cs, payload_off, payload;
+  std::memcpy(&magic, pack, 4);
+  std::memcpy(&cs, pack + 8, 8);
+  std::memcpy(&n, pack + 16, 4);
+  std::memcpy(&payload_off, pack + 24, 8);
+  std::memcpy(&payload, pack + 32, 8);
+  if (magic != kPackMagic) fail(POS_E_CORRUPT_IMAGE, "bad pack magic");
+  if (cs != c->cfg.chunk_size) fail(POS_E_CORRUPT_IMAGE, "pack chunk_size differs from the context");
+  if (kPackHeader + (uint64_t)kPackEntry * n > payload_off || payload_off + payload > bytes)
+    fail(POS_E_CORRUPT_IMAGE, "pack sections exceed its size");
+  for (uint32_t e = 0; e < n; ++e) {
+    const uint8_t* ent = pack + kPackHeader + (uint64_t)e * kPackEntry;
+    uint64_t h, off;
+    uint32_t ch, len;
+    std::memcpy(&h, ent, 8);
+    std::memcpy(&off, ent + 8, 8);
+    std::memcpy(&ch, ent + 16, 4);
+    std::memcpy(&len, ent + 20, 4);
+    auto it = c->index_of.find(h);
+    if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "pack entry for unknown handle");
+    if ((uint64_t)ch * cs + len > c->bufs[it->second].size || off + len > payload)
+      fail(POS_E_INVALID_LOCATOR, "pack entry outside its buffer");
+  }
+}
+
+int pos_restore_packs(pos_ctx* c, const uint8_t* const* packs, const uint64_t* sizes, uint32_t npacks,
+                      void* h2d_stream, void* stream, uint64_t region) {
+  return guarded([&] {
+    if (!c || (npacks && (!packs || !sizes))) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t hs = S(h2d_stream), s = S(stream);
+    if (region == 0) region = c->cache_cap / 2;
+    region = region / kPackAlign * kPackAlign;
+    if (2 * region > c->cache_cap) fail(POS_E_INVALID_ARGUMENT, "two regions must fit the cache");
+    for (uint32_t i = 0; i < npacks; ++i) {  // all-or-nothing: validate before writing
+      if (sizes[i] > region) fail(POS_E_STAGING_EXHAUSTED, "pack larger than a cache region");
+      validate_pack_host(c, packs[i], sizes[i]);
+    }
+    bool aligned = c->cfg.chunk_size % 16 == 0;
+    for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
+    if (!c->ev_d2h[0]) {
+      for (int k = 0; k < 2; ++k) {
+        ck(cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->ev_copied2[k], cudaEventDisableTiming), "event");
+      }
+    }
+    c->h_land[0].ensure(std::min<uint64_t>(region, std::max<uint64_t>(1, *std::max_element(sizes, sizes + std::max<uint32_t>(npacks, 1)))));
+    c->h_land[1].ensure(c->h_land[0].n);
+    bool used[2] = {false, false};
+    c->timer_begin(kTimScatter, s);
+    for (uint32_t i = 0; i < npacks; ++i) {
+      const uint32_t r = i & 1;
+      uint8_t* dev = c->cache.p + (uint64_t)r * region;
+      // region r / landing slot r are free once pack i-2's scatter finished
+      cudaPointerAttributes at{};
+      bool pinned = cudaPointerGetAttributes(&at, packs[i]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      if (used[r]) {
+        if (!pinned) ck(cudaEventSynchronize(c->ev_copied2[r]), "scatter sync");  // landing slot reuse
+        ck(cudaStreamWaitEvent(hs, c->ev_copied2[r], 0), "wait region");           // cache region reuse
+      }
+      const uint8_t* src = packs[i];
+      if (!pinned) {  // stage through the pinned landing slot with the host's threads
+        uint8_t* dst = c->h_land[r].p;
+        const uint64_t n = sizes[i];
+        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        if (n < (8u << 20)) nt = 1;
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nt; ++t)
+          pool.emplace_back([=] {
+            uint64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+            std::memcpy(dst + lo, src + lo, hi - lo);
+          });
+        for (auto& th : pool) th.join();
+        src = dst;
+      }
+      ck(cudaMemcpyAsync(dev, src, sizes[i], cudaMemcpyHostToDevice, hs), "h2d");
+      ck(cudaEventRecord(c->ev_d2h[r], hs), "event");
+      ck(cudaStreamWaitEvent(s, c->ev_d2h[r], 0), "wait h2d");
+      uint32_t ne;
+      std::memcpy(&ne, packs[i] + 16, 4);
+      if (ne) {
+        c->d_items.ensure(std::max<uint64_t>(ne, c->n_chunks));
+        k_pack_items<<<(ne + 255) / 256, 256, 0, s>>>(dev, sizes[i], c->d_bufs.p, (uint32_t)c->bufs.size(),
+                                                     c->cfg.chunk_size, c->d_items.p, c->d_err.p);
+        check_launch("k_pack_items");
+        ++c->launches;
+        launch_copy(c, c->d_items.p, nullptr, ne, aligned, s);
+      }
+      ck(cudaEventRecord(c->ev_copied2[r], s), "event");
+      used[r] = true;
+    }
+    c->timer_end(kTimScatter, s);
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
 static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
   return guarded([&] {
     if (!out) fail(POS_E_INVALID_ARGUMENT, "null argument");

@@ -406,6 +406,17 @@ class DumpEngine:
     def materialize(self, pack_dev_ptr: int, pack_bytes: int, stream=None) -> None:
         check(lib().pos_scatter(self.ctx, pack_dev_ptr, pack_bytes, _s(stream)))
 
+    def restore_packs(self, packs: Sequence[np.ndarray], stream=None, h2d_stream=None,
+                      region_bytes: int = 0) -> None:
+        """Streaming restore of host-resident packs, in order (base image then
+        deltas): H2D through two cache regions + scatter (pos_restore_packs)."""
+        n = len(packs)
+        arrs = [np.ascontiguousarray(p.view(np.uint8)) for p in packs]
+        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
+        sizes = np.array([a.nbytes for a in arrs], dtype=np.uint64)
+        check(lib().pos_restore_packs(self.ctx, ptrs, sizes.ctypes.data, n, _s(h2d_stream), _s(stream),
+                                      region_bytes))
+
     # ---- timing
     def event_record(self, slot: int, stream=None) -> None:
         check(lib().pos_event_record(self.ctx, slot, _s(stream)))

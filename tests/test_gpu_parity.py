@@ -558,3 +558,53 @@ def test_cache_cycled_precopy(orc, region):
         if i not in (1, 8):
             assert np.array_equal(img[i], p.host[i])
     eng.close()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_streaming_restore_with_delta_replay(orc, pinned):
+    """Restore = base image packs, then the incremental packs in order
+    (delta-restore), through two cache regions: the restored buffers equal
+    the live state; a pack naming an unknown handle is rejected before
+    anything is written (all or nothing)."""
+    cs = 65536
+    sizes = [3 * cs, 10000, 1, 2 * cs + 5, 70001, 5 * cs]
+    p = Proc(orc, sizes, seed0=6000)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=2 * 400_000 + 4096))
+    eng.register_buffers(p.bufs)
+    packs = []
+    eng.precopy_stream(lambda a, i: packs.append(a.copy()), region_bytes=400_000)
+    eng.commit_epoch()
+    for e in range(3):  # appends: new bytes at a moving frontier
+        p.write(5, e * cs + 100, 5000, 700 + e)
+        p.write(0, e * 1000, 10, 800 + e)
+        pd.device_synchronize()
+        eng.precopy_stream(lambda a, i: packs.append(a.copy()), region_bytes=400_000)
+        eng.commit_epoch()
+    # fresh device buffers for the restored process (same handles)
+    q = Proc(orc, sizes, seed0=9999)
+    for i in range(len(sizes)):
+        q.zero(i)
+    rest = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=2 * 400_000 + 4096))
+    rest.register_buffers(q.bufs)
+    hostpacks = packs
+    if pinned:
+        hostpacks = []
+        keep = []
+        for a in packs:
+            h = pd.PinnedHost(a.size)
+            h.array[:] = a
+            keep.append(h)
+            hostpacks.append(h.array)
+    rest.restore_packs(hostpacks, region_bytes=400_000)
+    for i in range(len(sizes)):
+        assert np.array_equal(q.read(i), p.host[i]), i
+    bad = packs[-1].copy()
+    if pd.parse_pack(bad)["n_entries"]:
+        bad[64:72] = np.frombuffer(np.uint64(424242).tobytes(), np.uint8)
+        before = [q.read(i) for i in range(len(sizes))]
+        with pytest.raises(pd.SimError) as e:
+            rest.restore_packs([packs[0], bad], region_bytes=400_000)
+        assert e.value.errc == "InvalidLocator"
+        assert all(np.array_equal(q.read(i), b) for i, b in enumerate(before))
+    eng.close()
+    rest.close()
