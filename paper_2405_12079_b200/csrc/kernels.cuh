@@ -82,6 +82,11 @@ struct HashParams {
   uint64_t item_base;        // hash mode: first global chunk of this launch
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
   const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
+  // > 0: before hashing its unit, a warp asks L2 for the unit's first
+  // pf_bytes with TMA bulk prefetches (16 KiB per lane), so a single-round
+  // launch (every warp holds one chunk) has the whole list in flight at once.
+  uint32_t pf_bytes;
+  uint32_t pad2;
 };
 
 // Hash kernel geometry.
@@ -408,6 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
+    if (p.pf_bytes && n) {
+      const uint64_t pa = (src + lo + 15) & ~15ull;
+      const uint64_t pe = (src + lo + (n < p.pf_bytes ? n : p.pf_bytes)) & ~15ull;
+      for (uint64_t q = pa + (uint64_t)lane * 16384; q < pe; q += 32 * 16384)
+        l2_prefetch(reinterpret_cast<const void*>(q), (uint32_t)(pe - q < 16384 ? pe - q : 16384));
+    }
     const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll>(small, p.xinv, lsel, lane, src + lo, n,
                                             p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
                          : 0u;

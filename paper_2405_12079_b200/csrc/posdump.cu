@@ -584,6 +584,11 @@ static void set_segments(const pos_ctx* c, uint64_t items, HashParams& p) {
   p.seg_bytes = (uint32_t)(c->cfg.chunk_size >> L);
   p.xseg = c->d_xseg.p + 32 * L;
   p.lastseg = c->d_lastseg.p + (size_t)nb * L;
+  p.pf_bytes = 0;
+  if (const char* e = std::getenv("POSDUMP_PF")) {  // tuning: L2 prefetch of single-round units
+    uint64_t v = std::strtoull(e, nullptr, 10);
+    if (v && (items << L) <= warps) p.pf_bytes = (uint32_t)std::min<uint64_t>(v, p.seg_bytes);
+  }
 }
 
 int pos_hash_chunks(pos_ctx* c, void* stream) {
