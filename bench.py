@@ -349,11 +349,28 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # Landing ring of pinned buffers: the host applies step e's packs out of
     # one buffer while step e+1 DMA-writes the next (DMA into lines the CPU
     # just read costs ~30% of the link).
-    pins = [pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20))) for _ in range(args.ring)]
-    host_image = [np.zeros(b.size, np.uint8) for b in bufs]
+    direct = args.mode == "direct"
+    if direct:
+        # The checkpoint image itself is pinned + mapped: k_copy_host stores
+        # every shipped chunk at its place (chunk_copied, cr.hpp:499-501).
+        img_offs, o = [], 0
+        for b in bufs:
+            img_offs.append(o)
+            o += (b.size + 255) // 256 * 256
+        img_pin = pd.PinnedHost(max(o, 1))
+        img_pin.array[:] = 0
+        host_image = [img_pin.array[a:a + b.size] for a, b in zip(img_offs, bufs)]
+        eng.register_image(host_image)
+        pins = []
+    else:
+        pins = [pd.PinnedHost(min(cache_cap, 2 * total + (64 << 20))) for _ in range(args.ring)]
+        host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
-    ckpt, copy, app = pd.Stream(priority=args.ckpt_priority), pd.Stream(), pd.Stream()
+    # direct mode: the drain kernel (k_copy_host) must win SM slots over queued
+    # application blocks too, so its stream shares the dump's priority
+    ckpt, app = pd.Stream(priority=args.ckpt_priority), pd.Stream()
+    copy = pd.Stream(priority=args.ckpt_priority if args.mode == "direct" else 0)
     by_handle = {b.handle: b for b in bufs}
 
     class AppThread:
@@ -387,7 +404,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     apply_threads = max(1, min(32, len(os.sched_getaffinity(0))))
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
     def checkpoint(e: int, e2e: bool):
-        pin = pins[e % len(pins)]
+        pin = pins[e % len(pins)] if pins else None
         for h, o, n, seed in wl.epoch_writes(e):  # untimed application iteration
             b = by_handle[h]
             pd.fill_bytes(b.dev_ptr + o, n, seed)
@@ -403,15 +420,17 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         dag_writes = sorted({h for k in window for h, _ in k})
 
         t0 = time.perf_counter()
-        eng.event_record(0, ckpt)
         # The window's kernels are in the DAG from submission (their spec write
         # sets, process.hpp:313-344): their buffers are left to the STW pass,
         # as record_dirty's copy cancellation does (cr.hpp:909-918).
         eng.record_dirty(dag_writes)
         app_thread.submit(app_args)  # the application's own host thread
-        # waves: hash/O1/compaction of wave k+1 overlaps the D2H of wave k
-        packs = eng.precopy_pipelined(pin.ptr, waves=args.waves, stream=ckpt, copy_stream=copy)
-        nbytes = eng.precopy_bytes
+        eng.event_record(0, ckpt)  # device clock starts with the dump's first operation
+        if direct:  # hash -> O1 -> scan per wave; chunks stored into the image on `copy`
+            eng.precopy_direct(waves=args.waves, stream=ckpt, drain_stream=copy)
+            packs = []
+        else:  # waves: hash/O1/compaction of wave k+1 overlaps the D2H of wave k
+            packs = eng.precopy_pipelined(pin.ptr, waves=args.waves, stream=ckpt, copy_stream=copy)
         eng.event_record(1, ckpt)
         eng.event_record(8, copy)
         # Stage the delta's layout now (write sets known at submission), so the
@@ -423,13 +442,19 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         eng.event_record(3, ckpt)
         doff, dbytes = eng.at_final_stop(stream=ckpt, stw_end_slot=4)  # STW ends after the gather
         copy.wait(ckpt)
-        eng.d2h_async(pin.ptr + doff, doff, dbytes, stream=copy)
+        if direct:
+            eng.delta_drain(stream=copy)
+        else:
+            eng.d2h_async(pin.ptr + doff, doff, dbytes, stream=copy)
         eng.event_record(5, copy)
         copy.synchronize()
         ckpt.synchronize()
+        if direct:
+            _, pre_payload = eng.precopy_direct_result()
+            dpay = sum(by_handle[h].size for h in dag_writes)
         # host image = the checkpoint target (captured_); inside the e2e wall
         # clock, always outside the device-timed region
-        if not args.no_host_apply:
+        if not args.no_host_apply and not direct:
             for o, z in packs:
                 pd.apply_pack_host(pin.array[o:o + z], handles, host_image, threads=apply_threads)
             pd.apply_pack_host(pin.array[doff:doff + dbytes], handles, host_image, threads=apply_threads)
@@ -450,11 +475,12 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]
             print(json.dumps(tl), file=sys.stderr)
         r = {"ms": ms, "stw_ms": stw, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
-             "precopy_bytes": sum(z for _, z in packs), "delta_bytes": dbytes, "launches": eng.launches - launches0 + len(window),
+             "precopy_bytes": pre_payload if direct else sum(z for _, z in packs),
+             "delta_bytes": dpay if direct else dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
              "scan_ms": kms("scan"), "delta_ms": kms("delta") if dbytes > 0 else 0.0,
              "delta_hash_ms": kms("delta_hash") if dbytes > 0 else 0.0,
-             "h2d_bytes": len(bufs) + 64 + 16 * (dbytes // CHUNK + 1)}
+             "h2d_bytes": len(bufs) + 64 + (48 if direct else 16) * (dbytes // CHUNK + 1)}
         eng.commit_epoch()
         return r
 
@@ -488,7 +514,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     step_ms, stw_ms, e2e_ms = all_max(dist, [step_ms, stw_ms, e2e_ms], local)
 
     # host-link peak: best of 5 plain pinned D2H copies of 256 MiB (CUDA events)
-    pin = pins[0]
+    pin = pins[0] if pins else pd.PinnedHost(256 << 20)
     link_n = min(flush.nbytes, pin.nbytes)
     link_peak = 0.0
     for _ in range(5):
@@ -683,6 +709,8 @@ def main():
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
     ap.add_argument("--waves", type=int, default=1, help="pre-copy pipeline waves (1 = no overlap)")
+    ap.add_argument("--mode", choices=["pack", "direct"], default="direct",
+                    help="pack: POSD pack D2H by the copy engine + host apply; direct: SM stores into the pinned image")
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)

@@ -128,6 +128,22 @@ int pos_read_buffer_crcs(pos_ctx* ctx, uint32_t* crcs, uint8_t* verdicts, uint32
 int pos_record_dirty(pos_ctx* ctx, const uint64_t* handles, uint32_t n);
 int pos_clear_dirty(pos_ctx* ctx);
 
+/* ---- H2D provenance (note_h2d_provenance, process.hpp:505-522) ---------- */
+/* The application's host-to-device copy of [dst, dst+bytes) from host_src
+ * (enqueued here on `stream` when do_copy != 0; otherwise the caller already
+ * enqueued it on `stream`), followed on the device by the provenance update
+ * of the buffer containing dst: a whole-buffer copy hashes the buffer's
+ * chunks and folds them into Upstream::crc (k_hash_chunks + k_note_upstream,
+ * no host round trip), sets has_upstream / host_untouched; a partial copy
+ * drops the provenance (process.hpp:510-513).  Either way the buffer becomes
+ * written_since_ckpt.  No containing buffer: only the copy.  The crc reaches
+ * the host lazily (pos_read_upstream). */
+int pos_h2d_provenance(pos_ctx* ctx, uint64_t dst, const void* host_src, uint64_t bytes, int do_copy,
+                       void* stream);
+/* GpuBuffer::upstream (buffer.hpp:37) of a registered buffer: waits for a
+ * pending pos_h2d_provenance. */
+int pos_read_upstream(pos_ctx* ctx, uint64_t handle, uint32_t* has_upstream, uint32_t* crc);
+
 /* ---- O3: compaction into the on-device cache ---------------------------- */
 /* Packs every flagged chunk of every non-dedup buffer (and, when
  * exclude_dag_dirty, outside dirty_set_: chunk_copied abandons those,
@@ -167,6 +183,30 @@ int pos_precopy_stream(pos_ctx* ctx, int exclude_dag_dirty, void* ckpt_stream, v
 int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                           void* copy_stream, void* host_dst, uint64_t slice_bytes,
                           uint64_t* offsets, uint64_t* sizes, uint32_t* n_packs);
+
+/* ---- direct pre-copy into the host image (zero-copy chunk_copied) ------ */
+/* The checkpoint target's image of captured_ (cr.hpp:499-501, the byte
+ * vectors chunk_copied writes at ci * chunk_size): hosts[i] / sizes[i] is the
+ * host copy of registered buffer i (ascending handle; sizes must match).
+ * Pinned memory is used as is; pageable ranges are pinned and mapped here
+ * (and unpinned at pos_ctx_destroy).  Re-register after pos_register_buffers. */
+int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n);
+/* Pre-copy straight into the registered image: per wave (<= 16 groups of
+ * whole buffers) hash -> O1 -> scan on ckpt_stream, then every eligible chunk
+ * is stored by SMs over PCIe into its place in the image on drain_stream
+ * (k_copy_host, zero copy) -- no compaction pass, no host round trip, no
+ * host-side apply.  The cache keeps an index-only POSD pack per wave (header
+ * + entries, flag 2).  Asynchronous: returns after enqueueing. */
+int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
+                       void* drain_stream);
+/* Chunks and payload bytes the last pos_precopy_direct shipped, and the end
+ * of its index packs in the cache (waits for the scans only). */
+int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_bytes,
+                              uint64_t* index_bytes);
+/* After pos_delta_copy with an image registered: the delta pack's payload
+ * (already in the cache -- the stop is over) stored into the image on
+ * `stream` by k_copy_host. */
+int pos_delta_drain(pos_ctx* ctx, void* stream);
 
 /* ---- STW delta-copy --------------------------------------------------- */
 /* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is

@@ -112,6 +112,12 @@ SIGNATURES = {
     "pos_precopy_size": [P, PU64],
     "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
     "pos_precopy_stream": [P, I32, P, P, U64, P, P, PU64, PU32],
+    "pos_register_image": [P, P, P, U32],
+    "pos_h2d_provenance": [P, U64, P, U64, I32, P],
+    "pos_read_upstream": [P, U64, PU32, PU32],
+    "pos_precopy_direct": [P, I32, U32, P, P],
+    "pos_precopy_direct_result": [P, PU64, PU64, PU64],
+    "pos_delta_drain": [P, P],
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_delta_copy_ex": [P, P, I32, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],

@@ -33,7 +33,8 @@ struct DevBuf {              // one registered allocation (GpuBuffer, buffer.hpp
   uint32_t x8_tail;          // x^(8 * last chunk length) mod P
   uint32_t flags;            // kBuf* bits
   uint32_t upstream_crc;     // Upstream::crc
-  uint32_t pad[3];
+  uint32_t pad;
+  uint64_t image;            // device-visible address of the buffer's host image (0: none)
 };
 static_assert(sizeof(DevBuf) == 64, "DevBuf layout");
 
@@ -55,6 +56,8 @@ constexpr uint32_t kPackHeader = 64;
 constexpr uint32_t kPackEntry = 32;
 constexpr uint32_t kPackAlign = 256;
 constexpr uint32_t kPackMagic = 0x44534F50u;  // "POSD"
+constexpr uint32_t kPackFlagDelta = 1u;        // STW delta pack
+constexpr uint32_t kPackFlagDirect = 2u;       // index only: payload went straight to the host image
 
 struct HashParams {
   const DevBuf* bufs;
@@ -451,178 +454,341 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
       } else if (p.flags) {
         const bool dirty = !p.prev_valid || p.digest_prev[g] != crc;
         p.flags[g] = dirty;
-        if (dirty) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
+        if (dirty && p.bitmap) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
       }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// O1: whole-buffer CRC = crc32_combine fold of the chunk digests, then the
-// scan_dedup verdict (cr.hpp:419-421) and the finalize_image gate
-// (!dirty_set_, cr.hpp:720).  One thread per buffer; Z^chunk_size from a table.
-// Whole-buffer CRC of buffer b folded from its chunk digests (crc32_combine
-// with Z^chunk_size from table t, and x^(8*tail) for the short last chunk).
-__device__ __forceinline__ uint32_t fold_buffer_crc(const DevBuf& b, const uint32_t* digests,
-                                                    const uint32_t* t) {
+// Whole-buffer CRC by one warp (O1, note_h2d_provenance): lanes fold
+// right-aligned runs of `per` full chunks with Z^chunk_size (table tz in
+// smem) -- only a prefix of lanes can be short, and a short run's left
+// neighbours are empty (crc 0), so every right operand of the lane tree is a
+// whole subtree of per * 2^k chunks and is shifted in with x^(8 cs per 2^k)
+// (xfold = x^(8 cs per), squared per level).  The last (possibly short)
+// chunk is appended with x^(8 tail).  Returns the crc on every lane.
+__device__ __forceinline__ uint32_t warp_fold_buffer(const DevBuf& b, const uint32_t* digests,
+                                                     const uint32_t* tz, uint32_t xfold, int lane) {
   const uint32_t* d = digests + b.chunk_base;
-  uint32_t crc = d[0];
-  for (uint32_t c = 1; c < b.nchunks; ++c) {
-    bool last = c + 1 == b.nchunks;
-    uint32_t adv = last ? multmodp(b.x8_tail, crc) : adv_small(t, crc);
-    crc = adv ^ d[c];
+  const uint32_t nfull = b.nchunks - 1;
+  if (nfull == 0) return d[0];
+  uint32_t crc = 0;
+  if (nfull <= 32) {
+    // Short buffer: one coalesced load, then a shuffle-fed Z^cs chain
+    // (~40 cycles per chunk; the lane tree's multmodp levels cost more).
+    const uint32_t v = (uint32_t)lane < nfull ? d[lane] : 0u;
+    for (uint32_t c = 0; c < nfull; ++c) crc = adv_small(tz, crc) ^ __shfl_sync(0xffffffffu, v, c);
+  } else {
+    const uint32_t per = (nfull + 31) / 32;
+    const int64_t hi = (int64_t)nfull - (int64_t)per * (31 - lane);
+    const int64_t lo = hi - per;
+#pragma unroll 4
+    for (int64_t c = lo < 0 ? 0 : lo; c < hi; ++c) crc = adv_small(tz, crc) ^ d[c];
+    uint32_t x = xfold;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, crc, 1 << k);
+      if ((lane & ((2 << k) - 1)) == 0) crc = multmodp(x, crc) ^ o;
+      x = multmodp(x, x);
+    }
+    crc = __shfl_sync(0xffffffffu, crc, 0);
   }
-  return crc;
+  return multmodp(b.x8_tail, crc) ^ d[nfull];
 }
 
+// O1: whole-buffer CRC (crc32_combine fold of the chunk digests, one warp
+// per buffer), then the scan_dedup verdict (cr.hpp:419-421) and the
+// finalize_image gate (!dirty_set_, cr.hpp:720).
 __global__ void k_buffer_crc(const DevBuf* bufs, uint32_t nbufs, const uint32_t* digests,
-                             const uint32_t* tcs, const uint8_t* dag_dirty, int dedup, int all,
-                             uint32_t* crc_out, uint8_t* verdict_out) {
+                             const uint32_t* tcs, const uint32_t* xfold, const uint8_t* dag_dirty, int dedup,
+                             int all, uint32_t* crc_out, uint8_t* verdict_out) {
   __shared__ uint32_t t[1024];  // Z^chunk_size
-  for (int k = threadIdx.x; k < 1024; k += blockDim.x) t[k] = __ldg(tcs + k);
+  for (int q = threadIdx.x; q < 1024; q += blockDim.x) t[q] = __ldg(tcs + q);
   __syncthreads();
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (i >= nbufs) return;
   const DevBuf b = bufs[i];
   const bool candidate = dedup && (b.flags & kBufHasUpstream);
   if (!all && !candidate) {  // verdict only: no provenance, no CRC needed (cr.hpp:390)
-    verdict_out[i] = 0;
+    if (lane == 0) verdict_out[i] = 0;
     return;
   }
-  const uint32_t crc = fold_buffer_crc(b, digests, t);
-  crc_out[i] = crc;
-  bool ok = candidate && crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
-  verdict_out[i] = ok;
+  const uint32_t crc = warp_fold_buffer(b, digests, t, xfold[i], lane);
+  if (lane == 0) {
+    crc_out[i] = crc;
+    verdict_out[i] = candidate && crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
+  }
+}
+
+// note_h2d_provenance (process.hpp:505-522) on the device: after a
+// whole-buffer H2D (whole != 0) the buffer's chunk digests (just hashed into
+// `digests`) fold into Upstream::crc, which lands in the device buffer table
+// and in a mapped host mirror; a partial H2D drops the provenance
+// (process.hpp:510-513).  Either way the buffer is written_since_ckpt.
+// One warp.
+__global__ void k_note_upstream(DevBuf* bufs, uint32_t i, const uint32_t* digests, const uint32_t* tcs,
+                                const uint32_t* xfold, int whole, volatile uint32_t* mirror) {
+  __shared__ uint32_t tz[1024];
+  for (int q = threadIdx.x; q < 1024; q += blockDim.x) tz[q] = __ldg(tcs + q);
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  DevBuf& b = bufs[i];
+  if (!whole) {
+    if (lane == 0) b.flags = (b.flags & ~(kBufHasUpstream | kBufHostUntouched)) | kBufWrittenSinceCkpt;
+    return;
+  }
+  const DevBuf snap = b;
+  const uint32_t crc = warp_fold_buffer(snap, digests, tz, xfold[i], lane);
+  if (lane == 0) {
+    b.upstream_crc = crc;
+    b.flags |= kBufHasUpstream | kBufHostUntouched | kBufWrittenSinceCkpt;
+    mirror[i] = crc;
+    __threadfence_system();
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Pack layout: one CTA scans the eligible-chunk flags in global chunk order
-// (= ascending (handle, chunk), since buffers are registered by ascending
-// handle), writes the POSD header + entries and one CopyItem per entry.
+// Pack layout: one CTA scans the eligible-chunk flags of [chunk_lo, chunk_hi)
+// in global chunk order (= ascending (handle, chunk), since buffers are
+// registered by ascending handle), writes the POSD header + entries and one
+// CopyItem per entry.
 // eligible = flag && !verdict_ok(buffer) && !(exclude_dag && dag_dirty(buffer)).
+//
+// Rounds of 32 chunks aligned to bitmap words: lane l of a round holds chunk
+// 32k + l, so loads are coalesced, the dirty-bitmap word is one ballot and a
+// lane's rank among the round's entries is a popc.  Each warp owns a
+// contiguous range of rounds; two block barriers join the warp totals.
+// Bitmap word k is written by the launch holding its last existing chunk
+// (earlier launches' flags are final by then), so waves need no memset.
 constexpr int kScanThreads = 1024;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kScanKeep = 4;  // rounds per warp kept in registers between the passes
 
 __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     const DevBuf* bufs, const uint2* chunk_map, uint64_t chunk_lo, uint64_t chunk_hi,
     uint64_t chunk_size, const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty,
     int exclude_dag, const uint32_t* digests, uint64_t epoch, uint32_t pack_flags, uint8_t* cache,
     uint64_t cache_capacity, uint64_t* cursor, CopyItem* items,
-    uint64_t* result /* [n, total, overflow, n_items, base] */,
+    uint64_t* result /* [n, total, overflow, n_items, base, -, payload] */,
     volatile uint64_t* result_host /* mapped pinned mirror (no DMA queue in between) */,
     uint64_t seq /* written last into result_host[5] */,
-    // fused O1 (k_buffer_crc for buffers [vb0, vb1) with upstream provenance):
-    uint32_t vb0, uint32_t vb1, const uint32_t* tcs, int dedup, uint32_t* crc_out,
-    uint8_t* verdict_out, uint64_t fixed_base /* ~0 = use the cursor */) {
-  __shared__ uint64_t s_n[kScanThreads], s_b[kScanThreads];
-  const int t = threadIdx.x;
+    // fused O1 (whole-buffer CRC + verdict for buffers [vb0, vb1) with upstream provenance):
+    uint32_t vb0, uint32_t vb1, const uint32_t* tcs, const uint32_t* xfold, int dedup, uint32_t* crc_out,
+    uint8_t* verdict_out, uint64_t fixed_base /* ~0 = at *cursor; cursor (if set) is advanced */,
+    int direct /* items target DevBuf::image; the pack keeps header + entries only */,
+    uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total) {
+  __shared__ uint32_t tz[1024];  // Z^chunk_size
+  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_tot[3];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
   if (vb1 > vb0) {
-    uint32_t* tz = reinterpret_cast<uint32_t*>(s_n);  // 8 KiB scratch: Z^chunk_size table
-    for (int k = t; k < 1024; k += kScanThreads) tz[k] = __ldg(tcs + k);
+    // Candidates (upstream provenance) into a smem list in one parallel pass,
+    // then one warp per candidate: no warp walks buffers it has nothing to do for.
+    __shared__ uint32_t s_cand[kScanThreads];
+    __shared__ uint32_t s_ncand;
+    if (t == 0) s_ncand = 0;
+    for (int q = t; q < 1024; q += kScanThreads) tz[q] = __ldg(tcs + q);
     __syncthreads();
     for (uint32_t i = vb0 + t; i < vb1; i += kScanThreads) {
-      const DevBuf& b = bufs[i];
-      bool ok = false;
-      if (dedup && (b.flags & kBufHasUpstream)) {  // no provenance -> no verdict (cr.hpp:390)
-        const uint32_t crc = fold_buffer_crc(b, digests, tz);
-        crc_out[i] = crc;
-        ok = crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
+      const bool cand = dedup && (bufs[i].flags & kBufHasUpstream);
+      if (cand) {
+        const uint32_t slot = atomicAdd(&s_ncand, 1u);
+        if (slot < kScanThreads) s_cand[slot] = i;
+        else verdict_out[i] = 2;  // list full: folded by the walk below
+      } else {
+        verdict_out[i] = 0;  // no provenance -> no verdict (cr.hpp:390)
       }
-      verdict_out[i] = ok;
     }
     __syncthreads();
+    const uint32_t nc = s_ncand < kScanThreads ? s_ncand : kScanThreads;
+    for (uint32_t q = warp; q < nc; q += kScanWarps) {
+      const uint32_t i = s_cand[q];
+      const DevBuf b = bufs[i];
+      const uint32_t crc = warp_fold_buffer(b, digests, tz, xfold[i], lane);
+      if (lane == 0) {
+        crc_out[i] = crc;
+        verdict_out[i] = crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
+      }
+    }
+    if (s_ncand > kScanThreads) {  // more candidates than list slots: walk the rest
+      __syncthreads();
+      for (uint32_t i = vb0 + warp; i < vb1; i += kScanWarps) {
+        if (verdict_out[i] != 2) continue;
+        const DevBuf b = bufs[i];
+        const uint32_t crc = warp_fold_buffer(b, digests, tz, xfold[i], lane);
+        __syncwarp();
+        if (lane == 0) {
+          crc_out[i] = crc;
+          verdict_out[i] = crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
+        }
+      }
+    }
+    __syncthreads();  // verdicts are read below
   }
-  // The pack goes at the running cache cursor (packs of earlier waves end
-  // there) or at a fixed region (cache cycling); items are written at [0, N).
   const uint64_t base = fixed_base != ~0ull ? fixed_base : *cursor;
   uint8_t* pack = cache + base;
-  const uint64_t n_chunks = chunk_hi - chunk_lo;
-  const uint64_t per = (n_chunks + kScanThreads - 1) / kScanThreads;
-  const uint64_t lo = chunk_lo + ((uint64_t)t * per < n_chunks ? (uint64_t)t * per : n_chunks);
-  const uint64_t hi = lo + per < chunk_hi ? lo + per : chunk_hi;
-  auto chunk_len = [&](uint2 cm) -> uint64_t {
-    const DevBuf& b = bufs[cm.x];
-    uint64_t start = (uint64_t)cm.y * chunk_size;
-    return cm.y + 1 == b.nchunks ? b.size - start : chunk_size;
+  const uint64_t w0 = chunk_lo >> 5, w1 = (chunk_hi + 31) >> 5;
+  const uint64_t per_w = (w1 - w0 + kScanWarps - 1) / kScanWarps;
+  const uint64_t r0 = w0 + (uint64_t)warp * per_w < w1 ? w0 + (uint64_t)warp * per_w : w1;
+  const uint64_t r1 = r0 + per_w < w1 ? r0 + per_w : w1;
+
+  struct Lane {
+    uint2 cm;
+    uint32_t mask;  // ballot of eligible lanes
+    uint64_t len;   // this lane's chunk length (0 if not eligible)
   };
-  auto eligible = [&](uint64_t g, uint2 cm) -> bool {
-    return flags[g] && !verdict[cm.x] && !(exclude_dag && dag_dirty[cm.x]);
+  auto look = [&](uint64_t k, bool with_bitmap) -> Lane {
+    const uint64_t g = 32 * k + lane;
+    const bool in = g >= chunk_lo && g < chunk_hi;
+    Lane L{make_uint2(0, 0), 0u, 0};
+    uint8_t f = 0;
+    if (in) {
+      L.cm = chunk_map[g];
+      f = flags[g];
+    }
+    bool el = false;
+    if (in && f) {
+      el = !verdict[L.cm.x] && !(exclude_dag && dag_dirty[L.cm.x]);
+      if (el) {
+        const DevBuf& b = bufs[L.cm.x];
+        L.len = L.cm.y + 1 == b.nchunks ? b.size - (uint64_t)L.cm.y * chunk_size : chunk_size;
+      }
+    }
+    L.mask = __ballot_sync(0xffffffffu, el);
+    if (with_bitmap && bitmap) {
+      const uint64_t last = (32 * k + 31 < n_total ? 32 * k + 31 : n_total - 1);
+      if (last >= chunk_lo && last < chunk_hi) {  // this launch owns word k
+        const uint32_t fb = in ? f : (g < n_total ? flags[g] : 0);
+        const uint32_t word = __ballot_sync(0xffffffffu, fb != 0);
+        if (lane == 0) bitmap[k] = word;
+      }
+    }
+    return L;
   };
-  uint64_t n = 0, bytes = 0;
-  for (uint64_t g = lo; g < hi; ++g) {
-    uint2 cm = chunk_map[g];
-    if (eligible(g, cm)) {
-      ++n;
-      bytes += (chunk_len(cm) + 15) & ~15ull;
+  auto padded = [&](uint64_t len) { return direct ? len : (len + 15) & ~15ull; };
+  auto warp_sum = [&](uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  // Pass 1: per-warp totals (entries, padded payload bytes).
+  Lane keep[kScanKeep];
+  uint64_t wn = 0, wb = 0;
+  auto count = [&](const Lane& L) {
+    wn += __popc(L.mask);
+    wb += warp_sum(L.len ? (L.len + 15) & ~15ull : 0);
+  };
+#pragma unroll
+  for (int j = 0; j < kScanKeep; ++j) {  // fixed indices: `keep` stays in registers
+    keep[j] = Lane{make_uint2(0, 0), 0u, 0};
+    if (r0 + j < r1) {
+      keep[j] = look(r0 + j, true);
+      count(keep[j]);
     }
   }
-  s_n[t] = n;
-  s_b[t] = bytes;
+  for (uint64_t k = r0 + kScanKeep; k < r1; ++k) count(look(k, true));
+  if (lane == 0) {
+    s_wn[warp] = wn;
+    s_wb[warp] = wb;
+  }
   __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {  // inclusive Hillis-Steele
-    uint64_t an = t >= off ? s_n[t - off] : 0, ab = t >= off ? s_b[t - off] : 0;
-    __syncthreads();
-    s_n[t] += an;
-    s_b[t] += ab;
-    __syncthreads();
-  }
-  const uint64_t N = s_n[kScanThreads - 1], B = s_b[kScanThreads - 1];
-  const uint64_t payload_off =
-      (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
-  const uint64_t total = payload_off + B;
-  const bool overflow = base + total > cache_capacity;
-  __syncthreads();  // every thread has read *cursor
-  if (t == 0) {
-    result[0] = N;
-    result[1] = total;
-    result[2] = overflow;
-    result[3] = overflow ? 0 : N;  // items for the copy kernel
-    result[4] = base;
-    if (!overflow && fixed_base == ~0ull) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
-    if (result_host) {
-      result_host[0] = N;
-      result_host[1] = total;
-      result_host[2] = overflow;
-      result_host[3] = overflow ? 0 : N;
-      result_host[4] = base;
-      __threadfence_system();
-      result_host[5] = seq;
-      __threadfence_system();
+  if (warp == 0) {  // exclusive scan of the warp totals
+    uint64_t n = s_wn[lane], b = s_wb[lane];
+    uint64_t in_n = n, in_b = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t an = __shfl_up_sync(0xffffffffu, in_n, o), ab = __shfl_up_sync(0xffffffffu, in_b, o);
+      if (lane >= o) {
+        in_n += an;
+        in_b += ab;
+      }
+    }
+    s_wn[lane] = in_n - n;
+    s_wb[lane] = in_b - b;
+    const uint64_t N = __shfl_sync(0xffffffffu, in_n, 31), B = __shfl_sync(0xffffffffu, in_b, 31);
+    if (lane == 0) {
+      const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
+      // Direct: entries keep the offsets a payload would have, but nothing is
+      // stored behind them (header payload_bytes = 0, kPackFlagDirect).
+      const uint64_t total = direct ? kPackHeader + kPackEntry * N : payload_off + B;
+      const bool overflow = base + total > cache_capacity;
+      result[0] = N;
+      result[1] = total;
+      result[2] = overflow;
+      result[3] = overflow ? 0 : N;  // items for the copy kernel
+      result[4] = base;
+      result[6] = B;
+      if (!overflow && cursor) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
+      if (result_host) {
+        result_host[0] = N;
+        result_host[1] = total;
+        result_host[2] = overflow;
+        result_host[3] = overflow ? 0 : N;
+        result_host[4] = base;
+        result_host[6] = B;
+        __threadfence_system();
+        result_host[5] = seq;
+        __threadfence_system();
+      }
+      s_tot[0] = N;
+      s_tot[1] = B;
+      s_tot[2] = overflow;
     }
   }
-  if (overflow) return;
+  __syncthreads();
+  const uint64_t N = s_tot[0], B = s_tot[1];
+  if (s_tot[2]) return;
+  const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
   if (t == 0) {
     uint32_t* h = reinterpret_cast<uint32_t*>(pack);
     h[0] = kPackMagic;
     h[1] = 1;
     *reinterpret_cast<uint64_t*>(pack + 8) = chunk_size;
     h[4] = (uint32_t)N;
-    h[5] = pack_flags;
-    *reinterpret_cast<uint64_t*>(pack + 24) = payload_off;
-    *reinterpret_cast<uint64_t*>(pack + 32) = B;
+    h[5] = pack_flags | (direct ? kPackFlagDirect : 0u);
+    *reinterpret_cast<uint64_t*>(pack + 24) = direct ? kPackHeader + kPackEntry * N : payload_off;
+    *reinterpret_cast<uint64_t*>(pack + 32) = direct ? 0 : B;
     *reinterpret_cast<uint64_t*>(pack + 40) = epoch;
-    *reinterpret_cast<uint64_t*>(pack + 48) = total;
+    *reinterpret_cast<uint64_t*>(pack + 48) = direct ? kPackHeader + kPackEntry * N : payload_off + B;
     *reinterpret_cast<uint64_t*>(pack + 56) = 0;
   }
-  for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
-  uint64_t e = s_n[t] - n, off = s_b[t] - bytes;
-  for (uint64_t g = lo; g < hi; ++g) {
-    uint2 cm = chunk_map[g];
-    if (!eligible(g, cm)) continue;
-    const DevBuf& b = bufs[cm.x];
-    uint64_t len = chunk_len(cm);
-    uint4* ent = reinterpret_cast<uint4*>(pack + kPackHeader + e * kPackEntry);
-    ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)off,
-                        (uint32_t)(off >> 32));
-    ent[1] = make_uint4(cm.y, (uint32_t)len, digests[g], 0u);
-    CopyItem ci;
-    ci.src = b.ptr + (uint64_t)cm.y * chunk_size;
-    ci.dst = (uint64_t)pack + payload_off + off;
-    ci.len = len;
-    ci.padded = (len + 15) & ~15ull;
-    items[e] = ci;
-    ++e;
-    off += ci.padded;
-  }
+  if (!direct)
+    for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
+  // Pass 2: entries + copy items at the warp's base.
+  uint64_t e = s_wn[warp], off = s_wb[warp];
+  auto emit = [&](uint64_t k, const Lane& L) {
+    const uint64_t pl = L.len ? (L.len + 15) & ~15ull : 0;
+    uint64_t incl = pl;  // inclusive prefix of the round's padded lengths
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    if (L.mask >> lane & 1) {
+      const uint64_t my_e = e + __popc(L.mask & lt);
+      const uint64_t my_off = off + incl - pl;
+      const DevBuf& b = bufs[L.cm.x];
+      const uint64_t g = 32 * k + lane;
+      uint4* ent = reinterpret_cast<uint4*>(pack + kPackHeader + my_e * kPackEntry);
+      ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)my_off,
+                          (uint32_t)(my_off >> 32));
+      ent[1] = make_uint4(L.cm.y, (uint32_t)L.len, digests[g], 0u);
+      CopyItem ci;
+      ci.src = b.ptr + (uint64_t)L.cm.y * chunk_size;
+      ci.dst = direct ? b.image + (uint64_t)L.cm.y * chunk_size : (uint64_t)pack + payload_off + my_off;
+      ci.len = L.len;
+      ci.padded = padded(L.len);
+      items[my_e] = ci;
+    }
+    e += __popc(L.mask);
+    off += __shfl_sync(0xffffffffu, incl, 31);
+  };
+#pragma unroll
+  for (int j = 0; j < kScanKeep; ++j)
+    if (r0 + j < r1) emit(r0 + j, keep[j]);
+  for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k, false));
 }
 
 // ---------------------------------------------------------------------------
@@ -762,6 +928,43 @@ __global__ void k_copy_simt(const CopyItem* items, const uint64_t* n_items_dev, 
     const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
     uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
     for (uint64_t k = lane; k < c.padded; k += 32) d[k] = k < c.len ? s[k] : 0;
+  }
+}
+
+// Zero-copy drain into the host image (mapped pinned memory): a handful of
+// small CTAs -- no shared memory, few registers -- so they co-reside with the
+// hash kernel's one-CTA-per-SM launch and with application blocks.  Each warp
+// streams one item at a time: kHostUnroll 16-B loads per lane in flight, then
+// the same number of 16-B stores, which leave the SM as posted PCIe writes
+// (the link, ~53 GB/s for SM stores, is the bound; 8 CTAs saturate it).
+// Items whose src/dst are not both 16-B aligned, and item tails, go by byte.
+constexpr int kHostCopyThreads = 128;
+constexpr int kHostCopyCtas = 16;
+constexpr int kHostUnroll = 4;
+
+__global__ void __launch_bounds__(kHostCopyThreads) k_copy_host(const CopyItem* items,
+                                                               const uint64_t* n_items_dev,
+                                                               uint64_t n_items_host) {
+  const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (kHostCopyThreads / 32);
+  for (uint64_t i = (uint64_t)blockIdx.x * (kHostCopyThreads / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+    const CopyItem c = items[i];
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
+    uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
+    uint64_t body = ((c.src | c.dst) & 15) == 0 ? c.len & ~15ull : 0;
+    constexpr uint64_t kStep = 32 * 16 * kHostUnroll;
+    uint64_t o = 0;
+    for (; o + kStep <= body; o += kStep) {
+      uint4 v[kHostUnroll];
+#pragma unroll
+      for (int u = 0; u < kHostUnroll; ++u) v[u] = ldg_stream(s + o + (u * 32 + lane) * 16);
+#pragma unroll
+      for (int u = 0; u < kHostUnroll; ++u) *reinterpret_cast<uint4*>(d + o + (u * 32 + lane) * 16) = v[u];
+    }
+    for (uint64_t q = o + lane * 16; q + 16 <= body; q += 32 * 16)
+      *reinterpret_cast<uint4*>(d + q) = ldg_stream(s + q);
+    for (uint64_t q = body + lane; q < c.padded; q += 32) d[q] = q < c.len ? s[q] : 0;
   }
 }
 

@@ -201,6 +201,13 @@ struct pos_ctx {
   std::vector<uint64_t> chunk_base;  // per buffer
   std::vector<DevBuf> hbufs;
   std::map<uint64_t, uint32_t> index_of;
+  std::map<uint64_t, uint32_t> by_ptr;  // device base -> buffer index (find_containing)
+  // note_h2d_provenance on the device (pos_h2d_provenance)
+  DevArray<uint32_t> d_prov;            // chunk digests of the H2D'd buffer
+  PinnedArray<uint32_t> h_up;           // mapped mirror of Upstream::crc per buffer
+  cudaEvent_t ev_prov = nullptr;
+  bool prov_pending = false;
+  std::vector<uint32_t> prov_bufs;      // buffers whose crc is still on its way
   uint64_t n_chunks = 0;
   DevArray<DevBuf> d_bufs;
   DevArray<uint2> d_chunk_map;
@@ -214,6 +221,7 @@ struct pos_ctx {
   DevArray<uint8_t> d_verdict;
   DevArray<uint8_t> d_dag_dirty;
   DevArray<uint32_t> d_tcs;  // Z^chunk_size
+  DevArray<uint32_t> d_xfold;  // per buffer: x^(8 cs ceil((nchunks-1)/32)) (warp_fold_buffer)
   // chunk segmentation (parallelism for short chunk lists)
   // level L = log2(nseg): x^(8 k cs/2^L) (32 per level) and, per buffer,
   // x^(8 * last segment length of the tail chunk); valid_levels bitmask.
@@ -228,7 +236,17 @@ struct pos_ctx {
   uint64_t delta_version = 0, delta_precopy = 0, delta_n = 0, delta_offset = 0, delta_total = 0,
            delta_payload_off = 0;
   bool delta_aligned = true;
+  bool delta_drain = false;  // drain items staged with the delta
   DevArray<CopyItem> d_delta_items;
+  // host image (pos_register_image): device-visible address per buffer, and
+  // the host ranges this context pinned itself (unpinned at destroy)
+  bool image_ready = false;
+  std::vector<void*> image_pinned;
+  DevArray<CopyItem> d_drain_items;  // STW delta pack payload -> host image
+  uint64_t drain_n = 0;              // items of the last delta copy (pos_delta_drain)
+  bool drain_pending = false;
+  bool direct_pending = false;       // a pos_precopy_direct awaits pos_precopy_direct_result
+  uint32_t direct_waves = 0;
   // O3 cache
   DevArray<uint8_t> cache;
   uint64_t cache_cap = 0;
@@ -241,6 +259,8 @@ struct pos_ctx {
   PinnedArray<uint8_t> h_stage;  // delta header + work list upload
   PinnedArray<uint8_t> h_dag;
   cudaEvent_t stage_free = nullptr;
+  cudaEvent_t ev_dag = nullptr;  // DAG flags uploaded on a side stream
+  bool dag_side = false;
   // Pre-copy packs: one per wave, chained at a device-side cache cursor.
   static constexpr uint32_t kMaxWaves = 16;
   DevArray<uint64_t> d_cursor;                     // [1]
@@ -281,14 +301,23 @@ void check_launch(const char* what) {
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
-void upload_dag_flags(pos_ctx* c, cudaStream_t s) {
-  if (c->dag_uploaded) return;
+// Per-buffer DAG-dirty flags (dirty_set_) to the device.  With a side
+// stream the copy runs there (concurrently with the first hash) and `s`
+// waits for it only where a consumer is enqueued (upload_dag_flags(c, s)).
+void upload_dag_flags(pos_ctx* c, cudaStream_t s, cudaStream_t side = nullptr) {
+  if (c->dag_uploaded) {
+    if (c->dag_side && !side) ck(cudaStreamWaitEvent(s, c->ev_dag, 0), "wait dag");
+    return;
+  }
   uint32_t nb = (uint32_t)c->bufs.size();
   c->h_dag.ensure(nb);
   if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
   for (uint32_t i = 0; i < nb; ++i) c->h_dag.p[i] = c->dirty_set.count(c->bufs[i].handle) ? 1 : 0;
-  ck(cudaMemcpyAsync(c->d_dag_dirty.p, c->h_dag.p, nb, cudaMemcpyHostToDevice, s), "dag upload");
-  ck(cudaEventRecord(c->stage_free, s), "event");
+  cudaStream_t us = side ? side : s;
+  ck(cudaMemcpyAsync(c->d_dag_dirty.p, c->h_dag.p, nb, cudaMemcpyHostToDevice, us), "dag upload");
+  ck(cudaEventRecord(c->stage_free, us), "event");
+  c->dag_side = side != nullptr;
+  if (side) ck(cudaEventRecord(c->ev_dag, side), "event");
   c->dag_uploaded = true;
 }
 
@@ -309,6 +338,20 @@ void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint6
     k_copy_simt<<<sms * 4, 256, 0, s>>>(items, n_dev, n_host);
   }
   check_launch("copy");
+  ++c->launches;
+}
+
+void launch_copy_host(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
+                      cudaStream_t s) {
+  static const int ctas = [] {
+    const char* e = std::getenv("POSDUMP_HOST_CTAS");  // tuning override
+    int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : kHostCopyCtas;
+  }();
+  int grid = ctas;
+  if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (n_host + 3) / 4));
+  k_copy_host<<<grid, kHostCopyThreads, 0, s>>>(items, n_dev, n_host);
+  check_launch("k_copy_host");
   ++c->launches;
 }
 
@@ -376,6 +419,7 @@ int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
       c->d_err.ensure(1);
       c->h_scan.ensure(8 * pos_ctx::kMaxWaves);
       ck(cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_dag, cudaEventDisableTiming), "event");
       for (uint32_t w = 0; w < pos_ctx::kMaxWaves; ++w) {
         ck(cudaEventCreateWithFlags(&c->scanned[w], cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->copied[w], cudaEventDisableTiming), "event");
@@ -412,12 +456,18 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_verdict.release();
   c->d_dag_dirty.release();
   c->d_tcs.release();
+  c->d_xfold.release();
+  c->d_prov.release();
+  c->h_up.release();
+  if (c->ev_prov) cudaEventDestroy(c->ev_prov);
   c->d_xseg.release();
   c->d_lastseg.release();
   c->d_result.release();
   c->cache.release();
   c->d_items.release();
   c->d_delta_items.release();
+  c->d_drain_items.release();
+  for (void* h : c->image_pinned) cudaHostUnregister(h);
   c->d_scan.release();
   c->d_work.release();
   c->d_err.release();
@@ -425,6 +475,7 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->h_stage.release();
   c->h_dag.release();
   if (c->stage_free) cudaEventDestroy(c->stage_free);
+  if (c->ev_dag) cudaEventDestroy(c->ev_dag);
   for (uint32_t w = 0; w < pos_ctx::kMaxWaves; ++w) {
     if (c->scanned[w]) cudaEventDestroy(c->scanned[w]);
     if (c->copied[w]) cudaEventDestroy(c->copied[w]);
@@ -463,6 +514,9 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
     c->hbufs.assign(n, DevBuf{});
     c->chunk_base.assign(n, 0);
     c->index_of.clear();
+    c->by_ptr.clear();
+    c->prov_pending = false;
+    c->prov_bufs.clear();
     uint64_t g = 0;
     for (uint32_t i = 0; i < n; ++i) {
       const auto& d = v[i];
@@ -482,6 +536,7 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
       b.upstream_crc = d.upstream_crc;
       c->chunk_base[i] = g;
       c->index_of[d.handle] = i;
+      c->by_ptr[d.dev_ptr] = i;
       g += nc;
     }
     if (g > 0xFFFFFFFFull) fail(POS_E_INVALID_ARGUMENT, "more than 2^32 chunks");
@@ -509,6 +564,12 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
       c->d_lastseg.ensure(ls.size());
       ck(cudaMemcpy(c->d_xseg.p, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice), "xseg");
       ck(cudaMemcpy(c->d_lastseg.p, ls.data(), ls.size() * 4, cudaMemcpyHostToDevice), "lastseg");
+    }
+    {
+      std::vector<uint32_t> xf(std::max<uint32_t>(n, 1), 0);
+      for (uint32_t i = 0; i < n; ++i) xf[i] = x8nmodp(cs * (uint64_t)((c->hbufs[i].nchunks - 1 + 31) / 32));
+      c->d_xfold.ensure(xf.size());
+      ck(cudaMemcpy(c->d_xfold.p, xf.data(), xf.size() * 4, cudaMemcpyHostToDevice), "xfold");
     }
     std::vector<uint2> cmap(g);
     for (uint32_t i = 0; i < n; ++i)
@@ -539,9 +600,93 @@ int pos_register_buffers(pos_ctx* c, const pos_buffer_desc* bufs, uint32_t n) {
   });
 }
 
+static void set_segments(const pos_ctx* c, uint64_t items, HashParams& p);
+
+// Upstream CRCs computed on the device (pos_h2d_provenance) into the host
+// copy of the buffer table, before the host uploads any of it again.
+static void sync_provenance(pos_ctx* c) {
+  if (!c->prov_pending) return;
+  ck(cudaEventSynchronize(c->ev_prov), "provenance sync");
+  for (uint32_t i : c->prov_bufs)
+    if (c->hbufs[i].flags & kBufHasUpstream) {
+      c->hbufs[i].upstream_crc = c->h_up.p[i];
+      c->bufs[i].upstream_crc = c->h_up.p[i];
+    }
+  c->prov_bufs.clear();
+  c->prov_pending = false;
+}
+
+int pos_h2d_provenance(pos_ctx* c, uint64_t dst, const void* src, uint64_t bytes, int do_copy, void* stream) {
+  return guarded([&] {
+    if (!c || (do_copy && bytes && !src)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    if (do_copy && bytes)
+      ck(cudaMemcpyAsync((void*)dst, src, bytes, cudaMemcpyHostToDevice, s), "h2d");
+    // find_containing(dst) (buffer.hpp:160-170); no buffer -> no provenance
+    auto it = c->by_ptr.upper_bound(dst);
+    if (it == c->by_ptr.begin()) return;
+    --it;
+    const uint32_t i = it->second;
+    DevBuf& b = c->hbufs[i];
+    if (dst >= b.ptr + b.size) return;
+    const bool whole = b.ptr == dst && b.size == bytes;
+    if (!c->ev_prov) ck(cudaEventCreateWithFlags(&c->ev_prov, cudaEventDisableTiming), "event");
+    c->h_up.ensure(c->bufs.size());
+    if (whole) {  // chunk digests of the fresh content -> fold on the device
+      c->d_prov.ensure(std::max<uint64_t>(c->n_chunks, 1));
+      HashParams p{};
+      p.bufs = c->d_bufs.p;
+      p.chunk_map = c->d_chunk_map.p;
+      p.n_items = b.nchunks;
+      p.item_base = b.chunk_base;
+      p.chunk_size = c->cfg.chunk_size;
+      p.k_full = zeros_crc(c->cfg.chunk_size);
+      p.tables = c->crc.tables.p;
+      p.xinv = c->crc.xinv.p;
+      p.digest_cur = c->d_prov.p;  // indexed by global chunk
+      set_segments(c, b.nchunks, p);
+      launch_hash<kModeHash>(c->hash_grid(b.nchunks * p.nseg), s, p);
+      check_launch("k_hash_chunks<provenance>");
+      ++c->launches;
+    }
+    k_note_upstream<<<1, 32, 0, s>>>(c->d_bufs.p, i, c->d_prov.p, c->d_tcs.p, c->d_xfold.p, whole ? 1 : 0,
+                                     c->h_up.p);
+    check_launch("k_note_upstream");
+    ++c->launches;
+    ck(cudaEventRecord(c->ev_prov, s), "event");
+    b.flags |= kBufWrittenSinceCkpt;
+    c->bufs[i].written_since_ckpt = 1;
+    if (whole) {
+      b.flags |= kBufHasUpstream | kBufHostUntouched;
+      c->bufs[i].has_upstream = 1;
+      c->bufs[i].host_untouched = 1;
+      c->prov_bufs.push_back(i);
+      c->prov_pending = true;
+    } else {  // process.hpp:510-513
+      b.flags &= ~(kBufHasUpstream | kBufHostUntouched);
+      c->bufs[i].has_upstream = 0;
+      c->bufs[i].host_untouched = 0;
+    }
+  });
+}
+
+int pos_read_upstream(pos_ctx* c, uint64_t handle, uint32_t* has_upstream, uint32_t* crc) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    auto it = c->index_of.find(handle);
+    if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "unknown handle");
+    sync_provenance(c);
+    const pos_buffer_desc& d = c->bufs[it->second];
+    if (has_upstream) *has_upstream = d.has_upstream;
+    if (crc) *crc = d.upstream_crc;
+  });
+}
+
 int pos_update_buffer(pos_ctx* c, const pos_buffer_desc* d) {
   return guarded([&] {
     if (!c || !d) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    sync_provenance(c);
     auto it = c->index_of.find(d->handle);
     if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "unknown handle");
     uint32_t i = it->second;
@@ -666,9 +811,9 @@ int pos_buffer_crc(pos_ctx* c, void* stream) {
     if (!nb) return;
     upload_dag_flags(c, s);
     c->timer_begin(kTimCombine, s);
-    k_buffer_crc<<<(nb + 127) / 128, 128, 0, s>>>(c->d_bufs.p, nb, c->d_digest[c->cur].p, c->d_tcs.p,
-                                                 c->d_dag_dirty.p, c->cfg.dedup, 1, c->d_buf_crc.p,
-                                                 c->d_verdict.p);
+    k_buffer_crc<<<(nb + 7) / 8, 256, 0, s>>>(c->d_bufs.p, nb, c->d_digest[c->cur].p, c->d_tcs.p,
+                                             c->d_xfold.p, c->d_dag_dirty.p, c->cfg.dedup, 1, c->d_buf_crc.p,
+                                             c->d_verdict.p);
     check_launch("k_buffer_crc");
     c->timer_end(kTimCombine, s);
     ++c->launches;
@@ -714,31 +859,46 @@ int pos_clear_dirty(pos_ctx* c) {
 // scan's device-side result, which is mirrored into pinned memory behind
 // event scanned[slot] for pack_result().
 static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
-                        uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0, uint64_t fixed_base = ~0ull) {
+                        uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0, uint64_t fixed_base = ~0ull,
+                        cudaStream_t direct_stream = nullptr, bool direct = false, bool chain_start = false) {
   upload_dag_flags(c, s);
+  // Packs chain at the device-side cursor; the first of a chain starts at 0
+  // (no memset), a fixed-region pack (cache cycling) leaves the cursor alone.
+  uint64_t* cursor = c->d_cursor.p;
+  if (chain_start) fixed_base = 0;
+  else if (fixed_base != ~0ull) cursor = nullptr;
   uint64_t* res = c->d_scan.p + 8 * slot;
   c->timer_begin(kTimScan, s);
   k_pack_scan<<<1, kScanThreads, 0, s>>>(
       c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
-      c->cache_cap, c->d_cursor.p, c->d_items.p, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
-      c->d_tcs.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base);
+      c->cache_cap, cursor, c->d_items.p + lo, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
+      c->d_tcs.p, c->d_xfold.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base, direct ? 1 : 0,
+      c->d_bitmap.p, c->n_chunks);
   c->slot_seq[slot] = c->scan_seq;
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
   ++c->launches;
   ck(cudaEventRecord(c->scanned[slot], s), "event");
+  if (direct) {  // chunks go straight to the host image from the drain stream
+    ck(cudaStreamWaitEvent(direct_stream, c->scanned[slot], 0), "wait scan");
+    if (slot == 0) c->timer_begin(kTimD2H, direct_stream);
+    launch_copy_host(c, c->d_items.p + lo, res + 3, 0, direct_stream);
+    ck(cudaEventRecord(c->copied[slot], direct_stream), "event");
+    c->pack_pending = true;
+    return;
+  }
   bool aligned = c->cfg.chunk_size % 16 == 0;
   for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
   c->timer_begin(kTimCopy, s);
-  launch_copy(c, c->d_items.p, res + 3, 0, aligned, s);
+  launch_copy(c, c->d_items.p + lo, res + 3, 0, aligned, s);
   c->timer_end(kTimCopy, s);
   ck(cudaEventRecord(c->copied[slot], s), "event");
   c->pack_pending = true;
 }
 
 struct PackResult {
-  uint64_t base, total, n;
+  uint64_t base, total, n, payload;
 };
 
 static PackResult pack_result(pos_ctx* c, uint32_t slot) {
@@ -758,7 +918,7 @@ static PackResult pack_result(pos_ctx* c, uint32_t slot) {
                                       std::to_string(r[4]) + " exceeds the cache of " +
                                       std::to_string(c->cache_cap) + " B");
   }
-  return PackResult{r[4], r[1], r[0]};
+  return PackResult{r[4], r[1], r[0], r[6]};
 }
 
 static uint64_t pack_size(pos_ctx* c) {
@@ -767,10 +927,6 @@ static uint64_t pack_size(pos_ctx* c) {
   c->pack_pending = false;
   c->precopy_bytes = r.total;
   return r.total;
-}
-
-static void reset_cursor(pos_ctx* c, cudaStream_t s) {
-  ck(cudaMemsetAsync(c->d_cursor.p, 0, 8, s), "cursor");
 }
 
 static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uint32_t wave) {
@@ -787,7 +943,7 @@ static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uin
   p.digest_cur = c->d_digest[c->cur].p;
   p.digest_prev = c->d_digest[c->cur ^ 1].p;
   p.flags = c->d_flags.p;
-  p.bitmap = c->d_bitmap.p;
+  p.bitmap = nullptr;  // the wave's k_pack_scan writes its bitmap words (one ballot per word)
   p.prev_valid = c->prev_valid ? 1 : 0;
   set_segments(c, hi - lo, p);
   int grid = c->hash_grid((hi - lo) * p.nseg);
@@ -803,8 +959,7 @@ int pos_compact(pos_ctx* c, int exclude_dag_dirty, void* stream, uint64_t* pack_
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
-    reset_cursor(c, S(stream));
-    launch_pack(c, exclude_dag_dirty, S(stream), 0, c->n_chunks, 0);
+    launch_pack(c, exclude_dag_dirty, S(stream), 0, c->n_chunks, 0, 0, 0, ~0ull, nullptr, false, true);
     uint64_t total = pack_size(c);
     if (pack_bytes) *pack_bytes = total;
   });
@@ -819,8 +974,7 @@ int pos_precopy(pos_ctx* c, int exclude_dag_dirty, void* stream) {
     if (rc != POS_OK) throw Fail{rc};
     rc = pos_buffer_crc(c, stream);
     if (rc != POS_OK) throw Fail{rc};
-    reset_cursor(c, s);
-    launch_pack(c, exclude_dag_dirty, s, 0, c->n_chunks, 0);
+    launch_pack(c, exclude_dag_dirty, s, 0, c->n_chunks, 0, 0, 0, ~0ull, nullptr, false, true);
   });
 }
 
@@ -845,15 +999,13 @@ int pos_precopy_pipelined(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, voi
     bb.push_back(nb);
     W = (uint32_t)bb.size() - 1;
     auto chunk_of = [&](uint32_t b) { return b < nb ? c->chunk_base[b] : c->n_chunks; };
-    reset_cursor(c, s);
-    upload_dag_flags(c, s);
-    if (c->n_chunks)
-      ck(cudaMemsetAsync(c->d_bitmap.p, 0, ((c->n_chunks + 31) / 32) * 4, s), "memset bitmap");
+    upload_dag_flags(c, s, cs);  // on the copy stream, under the first hash
     c->timer_begin(kTimHash, s);
     for (uint32_t w = 0; w < W; ++w) {
       hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
       // O1 verdicts fused into the scan: one launch less on the critical path
-      launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1]);
+      launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1], ~0ull,
+                  nullptr, false, w == 0);
     }
     c->timer_end(kTimHash, s);
     c->waves_last = W;
@@ -934,8 +1086,6 @@ int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, voi
     }
     upload_dag_flags(c, s);
     ck(cudaMemsetAsync(c->d_verdict.p, 0, std::max<uint32_t>(nb, 1), s), "memset verdicts");
-    if (c->n_chunks)
-      ck(cudaMemsetAsync(c->d_bitmap.p, 0, ((c->n_chunks + 31) / 32) * 4, s), "memset bitmap");
     std::vector<uint64_t> sizes(W, 0);
     uint64_t total = 0;
     auto finish = [&](uint32_t w) {  // wave w's bytes are on the host: hand them over
@@ -972,6 +1122,105 @@ int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, voi
   });
 }
 
+int pos_register_image(pos_ctx* c, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n) {
+  return guarded([&] {
+    if (!c || (!hosts && n) || (!sizes && n)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (n != c->bufs.size()) fail(POS_E_INVALID_ARGUMENT, "one image range per registered buffer");
+    sync_provenance(c);
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!hosts[i] || sizes[i] != c->bufs[i].size)
+        fail(POS_E_INVALID_ARGUMENT, "image range " + std::to_string(i) + " does not match its buffer");
+      cudaPointerAttributes a{};
+      cudaError_t e = cudaPointerGetAttributes(&a, hosts[i]);
+      if (e != cudaSuccess) cudaGetLastError();
+      if (e != cudaSuccess || a.type != cudaMemoryTypeHost) {  // pageable: pin + map it
+        ck(cudaHostRegister(hosts[i], sizes[i], cudaHostRegisterMapped | cudaHostRegisterPortable),
+           "cudaHostRegister(image)");
+        c->image_pinned.push_back(hosts[i]);
+      }
+      void* dev = nullptr;
+      ck(cudaHostGetDevicePointer(&dev, hosts[i], 0), "cudaHostGetDevicePointer(image)");
+      c->hbufs[i].image = (uint64_t)dev;
+    }
+    if (n) ck(cudaMemcpy(c->d_bufs.p, c->hbufs.data(), n * sizeof(DevBuf), cudaMemcpyHostToDevice), "bufs");
+    c->image_ready = n > 0;
+    c->delta_ready = false;  // re-stage the delta with drain items
+  });
+}
+
+int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
+                       void* drain_stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->image_ready) fail(POS_E_BAD_STATE, "no host image registered (pos_register_image)");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(ckpt_stream), ds = S(drain_stream);
+    if (s == ds) fail(POS_E_INVALID_ARGUMENT, "the drain needs its own stream");
+    const uint32_t nb = (uint32_t)c->bufs.size();
+    uint32_t W = std::max<uint32_t>(1, std::min<uint32_t>(waves, pos_ctx::kMaxWaves));
+    W = std::min<uint32_t>(W, std::max<uint32_t>(nb, 1));
+    std::vector<uint32_t> bb(1, 0);  // waves of whole buffers (O1), ~equal chunk counts
+    for (uint32_t w = 1; w < W; ++w) {
+      uint64_t target = c->n_chunks * w / W;
+      uint32_t b = bb.back();
+      while (b < nb && c->chunk_base[b] < target) ++b;
+      if (b > bb.back() && b < nb) bb.push_back(b);
+    }
+    bb.push_back(nb);
+    W = (uint32_t)bb.size() - 1;
+    auto chunk_of = [&](uint32_t b) { return b < nb ? c->chunk_base[b] : c->n_chunks; };
+    // The index packs' worst case (every chunk shipped) is reserved up front,
+    // so the STW delta's place in the cache is known without waiting.
+    uint64_t reserve = 0;
+    for (uint32_t w = 0; w < W; ++w)
+      reserve += round_up(kPackHeader + kPackEntry * (chunk_of(bb[w + 1]) - chunk_of(bb[w])), kPackAlign);
+    if (reserve > c->cache_cap) fail(POS_E_STAGING_EXHAUSTED, "index packs exceed the cache");
+    upload_dag_flags(c, s, ds);  // on the drain stream, under the first hash
+    c->timer_begin(kTimHash, s);
+    for (uint32_t w = 0; w < W; ++w) {
+      hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
+      launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1], ~0ull,
+                  ds, true, w == 0);
+    }
+    c->timer_end(kTimHash, s);
+    c->timer_end(kTimD2H, ds);
+    c->waves_last = W;
+    c->direct_waves = W;
+    c->direct_pending = true;
+    c->pack_pending = false;
+    c->precopy_bytes = reserve;
+  });
+}
+
+int pos_precopy_direct_result(pos_ctx* c, uint64_t* chunks, uint64_t* payload_bytes, uint64_t* index_bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->direct_pending) fail(POS_E_BAD_STATE, "no direct pre-copy in flight");
+    uint64_t n = 0, pay = 0, end = 0;
+    for (uint32_t w = 0; w < c->direct_waves; ++w) {
+      PackResult r = pack_result(c, w);
+      n += r.n;
+      pay += r.payload;
+      end = r.base + round_up(r.total, kPackAlign);
+    }
+    c->direct_pending = false;  // the index packs stay in [0, end) of the cache
+    if (chunks) *chunks = n;
+    if (payload_bytes) *payload_bytes = pay;
+    if (index_bytes) *index_bytes = end;
+  });
+}
+
+int pos_delta_drain(pos_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->drain_pending) fail(POS_E_BAD_STATE, "no STW delta to drain (pos_delta_copy with an image)");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    c->drain_pending = false;
+    if (c->drain_n) launch_copy_host(c, c->d_drain_items.p, nullptr, c->drain_n, S(stream));
+  });
+}
+
 int pos_precopy_size(pos_ctx* c, uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
@@ -986,6 +1235,7 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   const uint64_t offset = round_up(c->precopy_bytes, kPackAlign);
   std::vector<uint4> work;
   std::vector<CopyItem> items;
+  std::vector<uint2> where;  // (buffer index, chunk) per entry
   uint64_t payload = 0;
   uint32_t entry = 0;
   bool aligned = cs % 16 == 0;
@@ -999,6 +1249,7 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
       work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
       items.push_back(CopyItem{b.ptr + (uint64_t)k * cs, 0, len, round_up(len, 16)});
       items.back().dst = payload;  // relative; rebased below
+      where.push_back(make_uint2(i, k));
       payload += round_up(len, 16);
     }
   }
@@ -1010,8 +1261,9 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   for (auto& it : items) it.dst = (uint64_t)pack + payload_off + it.dst;
   // Stage the header, the work list (for the post-stop hash) and the gather items.
   const uint64_t work_bytes = n * sizeof(uint4), item_bytes = n * sizeof(CopyItem);
+  const uint64_t drain_bytes = c->image_ready ? item_bytes : 0;
   if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
-  c->h_stage.ensure(kPackHeader + work_bytes + item_bytes);
+  c->h_stage.ensure(kPackHeader + work_bytes + item_bytes + drain_bytes);
   uint8_t* st = c->h_stage.p;
   std::memset(st, 0, kPackHeader);
   uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)n, flags = 1;
@@ -1027,6 +1279,13 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   if (n) {
     std::memcpy(st + kPackHeader, work.data(), work_bytes);
     std::memcpy(st + kPackHeader + work_bytes, items.data(), item_bytes);
+    if (drain_bytes) {  // after the stop: gathered payload -> host image (chunk_copied, cr.hpp:499-501)
+      CopyItem* d = reinterpret_cast<CopyItem*>(st + kPackHeader + work_bytes + item_bytes);
+      for (uint64_t e = 0; e < n; ++e) {
+        const uint2 cm = where[e];
+        d[e] = CopyItem{items[e].dst, c->hbufs[cm.x].image + (uint64_t)cm.y * cs, items[e].len, items[e].len};
+      }
+    }
   }
   // The kernels write the entries and the payload; the header and the gap go up now.
   ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
@@ -1039,6 +1298,12 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
     ck(cudaMemcpyAsync(c->d_delta_items.p, st + kPackHeader + work_bytes, item_bytes,
                        cudaMemcpyHostToDevice, s),
        "items");
+    if (drain_bytes) {
+      c->d_drain_items.ensure(n);
+      ck(cudaMemcpyAsync(c->d_drain_items.p, st + kPackHeader + work_bytes + item_bytes, drain_bytes,
+                         cudaMemcpyHostToDevice, s),
+         "drain items");
+    }
   }
   ck(cudaEventRecord(c->stage_free, s), "event");
   c->delta_ready = true;
@@ -1049,6 +1314,7 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   c->delta_total = total;
   c->delta_payload_off = payload_off;
   c->delta_aligned = aligned;
+  c->delta_drain = c->image_ready;
 }
 
 static bool delta_current(const pos_ctx* c) {
@@ -1078,6 +1344,8 @@ int pos_delta_copy_ex(pos_ctx* c, void* stream, int stw_end_slot, uint64_t* pack
     cudaStream_t s = S(stream);
     if (!delta_current(c)) delta_prepare(c, s);
     c->delta_ready = false;  // one launch per preparation
+    c->drain_pending = c->delta_drain;
+    c->drain_n = c->delta_drain ? c->delta_n : 0;
     const uint64_t n = c->delta_n, cs = c->cfg.chunk_size;
     // Stop-the-world part: a pure TMA bulk gather of the flagged buffers.
     c->timer_begin(kTimDelta, s);
@@ -1318,7 +1586,7 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
     dm.ensure(nc);
     dd.ensure(nc);
     dt.ensure(1024);
-    dc.ensure(1);
+    dc.ensure(2);  // [crc out, xfold]
     dz.ensure(2);
     auto cleanup = [&] {
       db.release();
@@ -1333,6 +1601,9 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
       ck(cudaMemcpyAsync(dm.p, cmap.data(), nc * 8, cudaMemcpyHostToDevice, s), "h2d");
       ck(cudaMemcpyAsync(dt.p, tcs.data(), 4096, cudaMemcpyHostToDevice, s), "h2d");
       ck(cudaMemsetAsync(dz.p, 0, 2, s), "memset");
+      static thread_local uint32_t xf;  // pageable source: cudaMemcpyAsync stages it before returning
+      xf = x8nmodp(cs * ((nc - 1 + 31) / 32));
+      ck(cudaMemcpyAsync(dc.p + 1, &xf, 4, cudaMemcpyHostToDevice, s), "h2d");
       HashParams p{};
       p.bufs = db.p;
       p.chunk_map = dm.p;
@@ -1351,7 +1622,7 @@ static int crc_range(uint32_t* out, uint64_t ptr, uint64_t n, cudaStream_t s) {
       int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)t.sm_count));
       launch_hash<kModeHash>(grid, s, p);
       check_launch("k_hash_chunks");
-      k_buffer_crc<<<1, 32, 0, s>>>(db.p, 1, dd.p, dt.p, dz.p, 0, 1, dc.p, dz.p + 1);
+      k_buffer_crc<<<1, 32, 0, s>>>(db.p, 1, dd.p, dt.p, dc.p + 1, dz.p, 0, 1, dc.p, dz.p + 1);
       check_launch("k_buffer_crc");
       uint32_t r = 0;
       ck(cudaMemcpyAsync(&r, dc.p, 4, cudaMemcpyDeviceToHost, s), "d2h");

@@ -373,6 +373,56 @@ class DumpEngine:
         self.precopy_bytes = 0
         return total.value, n.value
 
+    # ---- H2D provenance (note_h2d_provenance, process.hpp:505-522)
+    def h2d_provenance(self, dst: int, host: Optional[np.ndarray] = None, nbytes: Optional[int] = None,
+                       stream=None) -> None:
+        """H2D of `host` into device address dst (skipped when host is None:
+        the caller enqueued it on `stream`), then Upstream::crc on the device."""
+        if host is not None:
+            host = np.ascontiguousarray(host).view(np.uint8).reshape(-1)
+            nbytes = host.nbytes if nbytes is None else nbytes
+            check(lib().pos_h2d_provenance(self.ctx, dst, host.ctypes.data, nbytes, 1, _s(stream)))
+            self._h2d_keep = host  # pageable sources are staged by the call; pinned must stay alive
+        else:
+            check(lib().pos_h2d_provenance(self.ctx, dst, None, nbytes or 0, 0, _s(stream)))
+
+    def upstream(self, handle: int) -> Optional[int]:
+        """Upstream::crc of a buffer, or None without provenance."""
+        has, crc = C.c_uint32(0), C.c_uint32(0)
+        check(lib().pos_read_upstream(self.ctx, handle, C.byref(has), C.byref(crc)))
+        return crc.value if has.value else None
+
+    # ---- direct pre-copy into a registered host image (zero-copy chunk_copied)
+    def register_image(self, hosts: Sequence[np.ndarray]) -> None:
+        """hosts[i]: the host image of registered buffer i (uint8, its size);
+        pinned memory is used as is, pageable arrays are pinned here."""
+        arrs = list(hosts)
+        if any(a.dtype != np.uint8 or not a.flags.c_contiguous for a in arrs):
+            raise SimError(10, "image ranges must be contiguous uint8 arrays")  # InvalidArgument
+        n = len(arrs)
+        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
+        sizes = np.array([a.size for a in arrs], dtype=np.uint64)
+        check(lib().pos_register_image(self.ctx, ptrs, sizes.ctypes.data, n))
+        self._image = arrs  # keep the memory alive
+
+    def precopy_direct(self, waves: int = 1, stream=None, drain_stream=None,
+                       exclude_dag_dirty: bool = True) -> None:
+        """Pre-copy straight into the registered image (pos_precopy_direct);
+        asynchronous -- pair with precopy_direct_result()."""
+        check(lib().pos_precopy_direct(self.ctx, 1 if exclude_dag_dirty else 0, waves, _s(stream),
+                                       _s(drain_stream)))
+
+    def precopy_direct_result(self) -> tuple[int, int]:
+        """(chunks, payload bytes) shipped by the last direct pre-copy."""
+        n, pay, idx = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_precopy_direct_result(self.ctx, C.byref(n), C.byref(pay), C.byref(idx)))
+        self.precopy_bytes = idx.value
+        return n.value, pay.value
+
+    def delta_drain(self, stream=None) -> None:
+        """STW delta payload (in the cache) -> host image (pos_delta_drain)."""
+        check(lib().pos_delta_drain(self.ctx, _s(stream)))
+
     def precopy_size(self) -> int:
         n = C.c_uint64(0)
         check(lib().pos_precopy_size(self.ctx, C.byref(n)))

@@ -608,3 +608,152 @@ def test_streaming_restore_with_delta_replay(orc, pinned):
         assert all(np.array_equal(q.read(i), b) for i, b in enumerate(before))
     eng.close()
     rest.close()
+
+
+@pytest.mark.parametrize("cs,waves,offsets,pageable", [
+    (65536, 1, None, False),
+    (65536, 3, None, True),          # pageable image: pinned + mapped by the context
+    (4096, 2, [0, 5, 0, 3], False),  # unaligned buffers: byte path of k_copy_host
+    (1000, 1, None, False),          # chunk_size not a multiple of 16
+])
+def test_direct_precopy_into_image(orc, cs, waves, offsets, pageable):
+    """Direct mode (pos_precopy_direct + pos_delta_drain): every shipped chunk
+    lands at its place in the registered host image (chunk_copied,
+    cr.hpp:499-501) -- epoch 0 ships everything, epoch 1 exactly the dirty
+    chunks outside dirty_set_ plus the STW delta of dirty_set_; the image then
+    equals the device, untouched image bytes are never written, and the index
+    packs carry the oracle pack's entries."""
+    sizes = [1 << 20, 300000, 65536 + 7, 12345]
+    p = Proc(orc, sizes, seed0=4100, offsets=offsets)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=16 << 20))
+    eng.register_buffers(p.bufs)
+    if pageable:
+        image = [np.zeros(n, np.uint8) for n in sizes]
+    else:
+        pin = pd.PinnedHost(sum((n + 255) // 256 * 256 for n in sizes))
+        pin.array[:] = 0
+        image, o = [], 0
+        for n in sizes:
+            image.append(pin.array[o:o + n])
+            o += (n + 255) // 256 * 256
+    eng.register_image(image)
+    ckpt, drain = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=waves, stream=ckpt, drain_stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    nch, pay = eng.precopy_direct_result()
+    assert nch == sum((n + cs - 1) // cs for n in sizes)
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i]), f"epoch 0 buffer {i}"
+    d0 = eng.digests()
+    eng.commit_epoch()
+    # epoch 1: sparse rewrites; buffer 3 is DAG-dirty (left to the STW delta)
+    p.write(0, 3 * cs + 5, 100, 77)
+    p.write(1, 0, 10, 78)
+    p.write(3, 7, 20, 79)
+    pd.device_synchronize()
+    flags = np.concatenate([odigests(orc, h, cs) for h in p.host]) != d0
+    marker = image[2].copy()
+    eng.record_dirty([4])
+    eng.precopy_direct(waves=waves, stream=ckpt, drain_stream=drain)
+    p.write(3, 100, 50, 80)  # written during the pre-copy window
+    pd.device_synchronize()
+    off, n = eng.at_final_stop(stream=ckpt)
+    drain.wait(ckpt)
+    eng.delta_drain(stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    nch, pay = eng.precopy_direct_result()
+    bounds = np.cumsum([0] + [(s + cs - 1) // cs for s in sizes])
+    want = flags.copy()
+    want[bounds[3]:bounds[4]] = False  # DAG-dirty buffer: not in the pre-copy
+    assert nch == int(want.sum())
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i]), f"epoch 1 buffer {i}"
+    assert np.array_equal(image[2], marker)
+    # index pack (cache offset 0, first wave): POSD header with the direct
+    # flag; one wave -> its entries are the oracle pack's entries byte for byte
+    idx = download_cache(eng, 0, 64)
+    assert idx[:4].tobytes() == b"POSD" and (int(idx[20:24].view(np.uint32)[0]) & 2)
+    if waves == 1:
+        ne = int(idx[16:20].view(np.uint32)[0])
+        assert ne == nch
+        ours = download_cache(eng, 0, 64 + 32 * ne)[64:]
+        ref = opack(orc, list(zip(p.handles, p.host)), cs, want.astype(np.uint8), 1)
+        assert np.array_equal(ours, ref[64:64 + 32 * ne])
+    eng.close()
+
+
+@pytest.mark.parametrize("cs", [4096, 1000])
+def test_h2d_provenance_on_device(orc, cs):
+    """note_h2d_provenance (process.hpp:505-522) on the device, after
+    test_api.cpp:76-98: a whole-buffer H2D records Upstream::crc ==
+    crc32(payload) -- lane-tree fold for buffers past 33 chunks, shuffle chain
+    below -- and the next pre-copy dedups the buffer (O1, cr.hpp:416-425);
+    a partial H2D drops the provenance; an address outside every buffer is a
+    plain copy."""
+    sizes = [cs * 1, cs * 2 + 1, cs * 33, cs * 34 - 5, cs * 100 + 17, 7]
+    p = Proc(orc, sizes, seed0=5200)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=8 << 20))
+    eng.register_buffers(p.bufs)
+    s = pd.Stream()
+    payloads = [mb(orc, 9000 + i, n) for i, n in enumerate(sizes)]
+    for i, b in enumerate(p.bufs):
+        eng.h2d_provenance(b.dev_ptr, payloads[i], stream=s)
+        p.host[i][:] = payloads[i]
+    s.synchronize()
+    for i, b in enumerate(p.bufs):
+        assert np.array_equal(p.read(i), payloads[i])
+        assert eng.upstream(b.handle) == ocrc(orc, payloads[i]), f"buffer {i}"
+    # O1 at the next pre-copy: every buffer dedups, the pack is empty
+    n = eng.plan_precopy()
+    crcs, ver = eng.buffer_crcs()
+    assert [int(c) for c in crcs] == [ocrc(orc, h) for h in p.host]
+    assert all(ver), ver
+    assert n == 256  # header only: no entries, payload at the 256-B aligned offset
+    # partial H2D into buffer 2 drops its provenance (process.hpp:510-513)
+    part = mb(orc, 9100, 100)
+    eng.h2d_provenance(p.bufs[2].dev_ptr + 5, part, stream=s)
+    s.synchronize()
+    assert eng.upstream(p.bufs[2].handle) is None
+    eng.commit_epoch()
+    eng.plan_precopy()
+    _, ver = eng.buffer_crcs()
+    assert not ver[2] and all(ver[i] for i in range(len(sizes)) if i != 2)
+    eng.close()
+
+
+def test_o1_verdicts_many_candidates(orc):
+    """O1 with more provenance candidates (1500) than the scan's candidate
+    list (1024 slots): the overflow walk must give the same verdicts
+    (crc == Upstream::crc, cr.hpp:419-421) -- every other buffer carries a
+    wrong crc."""
+    n, size, cs = 1500, 100, 64
+    mem = pd.DeviceMemory(n * 128)
+    host = [mb(orc, 7000 + i, size) for i in range(n)]
+    bufs = []
+    for i in range(n):
+        mem.upload(host[i], offset=i * 128)
+        crc = ocrc(orc, host[i]) ^ (i & 1)
+        bufs.append(pd.GpuBuffer(handle=i + 1, dev_ptr=mem.ptr + i * 128, size=size,
+                                 upstream=pd.Upstream(crc, True)))
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
+    eng.register_buffers(bufs)
+    s, d = pd.Stream(), pd.Stream()
+    pin = pd.PinnedHost(n * 128)
+    pin.array[:] = 0
+    img = [pin.array[i * 128:i * 128 + size] for i in range(n)]
+    eng.register_image(img)
+    eng.precopy_direct(waves=1, stream=s, drain_stream=d)
+    d.synchronize()
+    s.synchronize()
+    nch, _ = eng.precopy_direct_result()
+    crcs, ver = eng.buffer_crcs()
+    assert [int(c) for c in crcs] == [ocrc(orc, h) for h in host]
+    assert [bool(v) for v in ver] == [i % 2 == 0 for i in range(n)]
+    assert nch == (n // 2) * ((size + cs - 1) // cs)  # only the non-dedup buffers ship
+    for i in range(n):
+        want = host[i] if i % 2 else np.zeros(size, np.uint8)
+        assert np.array_equal(img[i], want)
+    eng.close()
