@@ -96,6 +96,18 @@ class Workload:
             self.phases = []
             self.desc = (f"Llama-3 8B bf16 training state (params bf16 + fp32 master + Adam m,v; "
                          f"{len(self.sizes)} buffers, {sum(self.sizes)} B), Adam step rewrites all")
+        elif name == "c4":
+            # LLM inference KV cache: 32 layers x {K, V} paged tensors, 40 GB;
+            # 16-token blocks of 8 KV heads x 128 dims bf16 = 32 KiB per block
+            # per tensor; 256 sequences each append one block per epoch (one
+            # 16-token decode burst) at ring-allocated block slots.
+            self.sizes = [625_000_000] * 64
+            self.params = set()
+            self.phases = []
+            self.block, self.seqs = 32768, 256
+            self.nblocks = self.sizes[0] // self.block
+            self.desc = ("LLM inference KV cache (32 layers x K/V paged, 40 GB, 32 KiB blocks), 256 sequences "
+                         "append one block each per epoch (1.3% of the state)")
         elif name == "c1":
             self.sizes = [16 << 20] * 64
             self.params = set()
@@ -107,6 +119,13 @@ class Workload:
         self.n_iter = max(1, len(self.phases) // 2)
 
     def epoch_writes(self, e: int):
+        if self.name == "c4":  # append-only: block slots (e * S + s) mod nblocks
+            out = []
+            for s in range(self.seqs):
+                blk = (e * self.seqs + s) % self.nblocks
+                for h in range(1, len(self.sizes) + 1):
+                    out.append((h, blk * self.block, self.block, mix64(mix64(e, s), h)))
+            return out
         if self.name == "c3":  # the optimizer step rewrites every tensor
             return [(h, 0, n, mix64(e, h)) for h, n in enumerate(self.sizes, start=1)]
         if self.name == "c1":
@@ -128,7 +147,7 @@ class Workload:
     def window(self, e: int):
         """Kernels of the next iteration's compute phase (stream 1 and 2
         kernels are serialised on one app stream)."""
-        if self.name in ("c1", "c3"):
+        if self.name in ("c1", "c3", "c4"):
             return []
         it = (e + 1) % self.n_iter
         ph = self.phases[2 * it]
@@ -405,9 +424,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
     def checkpoint(e: int, e2e: bool):
         pin = pins[e % len(pins)] if pins else None
-        for h, o, n, seed in wl.epoch_writes(e):  # untimed application iteration
-            b = by_handle[h]
-            pd.fill_bytes(b.dev_ptr + o, n, seed)
+        # untimed application iteration
+        pd.fill_batch([(by_handle[h].dev_ptr + o, n, seed) for h, o, n, seed in wl.epoch_writes(e)])
         pd.check(pd.lib().pos_memset(flush.ptr, e & 0xFF, flush.nbytes, None))  # flush L2
         pd.device_synchronize()
         window = wl.window(e)
@@ -501,10 +519,10 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     for _ in range(max(3, min(args.steps, 10))):
         e2e_res.append(checkpoint(e, True))
         e += 1
-    # verify the host image against the device (bit-exact)
-    dev_bytes = mem.download()
-    ok = args.no_host_apply or all(np.array_equal(img, dev_bytes[b.dev_ptr - mem.ptr:b.dev_ptr - mem.ptr + b.size])
-             for b, img in zip(bufs, host_image))
+    # verify the host image against the device (bit-exact), buffer by buffer
+    ok = args.no_host_apply or all(np.array_equal(img, mem.download(b.size, offset=b.dev_ptr - mem.ptr))
+                                   for b, img in zip(bufs, host_image))
+    restore = restore_measure(eng, pd, wl, bufs, host_image, mem, e) if (wl.name == "c4" and direct) else None
 
     step_ms = sum(r["ms"] for r in res) / len(res)
     stw_ms = statistics.median(r["stw_ms"] for r in res)
@@ -582,11 +600,71 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                                                               for r in e2e_res)),
                     "how": "host wall clock around DumpEngine calls incl. pinned D2H and host-side pack apply into the image"},
             "image_parity": bool(ok),
+            **({"restore": restore} if restore else {}),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
     eng.close()
     return out
+
+
+def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
+    """KV-cache failover (BASELINE config 4): the device state is lost
+    (zeroed), the checkpoint image is loaded back on demand (pos_restore_image_*:
+    loads in buffer order, one layer's K gated first as the first replayed
+    decode kernel would), then a delta pack of the next decode burst is
+    replayed with the scatter kernel (delta-restore).  Checks: digests after
+    the restore == the checkpoint's digests (every chunk), and the scattered
+    delta == the live writes."""
+    from paper_2405_12079_b200.posdump import D2H  # noqa: F401
+    eng.hash_chunks()  # the state as of the last checkpoint (nothing written since)
+    digests_ckpt = eng.digests()
+    total = sum(b.size for b in bufs)
+    for b in bufs:
+        pd.check(pd.lib().pos_memset(b.dev_ptr, 0, b.size, None))
+    pd.device_synchronize()
+    h2d, app = pd.Stream(), pd.Stream(priority=1)
+    order = [b.handle for b in bufs]
+    gate_h = bufs[len(bufs) // 2].handle  # a layer in the middle of the load order
+    eng.event_record(10, h2d)
+    t0 = time.perf_counter()
+    eng.restore_image_begin(host_image, order=order, h2d_stream=h2d)
+    eng.restore_gate(gate_h, stream=app)
+    eng.event_record(11, app)
+    eng.restore_image_wait()
+    eng.event_record(12, h2d)
+    t1 = time.perf_counter()
+    restore_ms = eng.event_elapsed(10, 12)
+    gate_ms = eng.event_elapsed(10, 11)
+    eng.hash_chunks()
+    restored_ok = bool(np.array_equal(eng.digests(), digests_ckpt))
+    # delta-restore replay: the next burst's appends as a POSD pack (pack mode),
+    # scattered back onto the restored state
+    eng.commit_epoch()
+    writes = wl.epoch_writes(e)
+    by_handle = {b.handle: b for b in bufs}
+    pd.fill_batch([(by_handle[h].dev_ptr + o, n, s) for h, o, n, s in writes])
+    pd.device_synchronize()
+    pack_bytes = eng.plan_precopy()
+    cache_ptr, _ = eng.cache()
+    want = [mem.download(n, offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in writes[:64]]
+    for h, o, n, _ in writes:
+        pd.check(pd.lib().pos_memset(by_handle[h].dev_ptr + o, 0, n, None))
+    pd.device_synchronize()
+    eng.materialize(cache_ptr, pack_bytes)
+    pd.device_synchronize()
+    scatter_ms = eng.kernel_ms("scatter")
+    got = [mem.download(n, offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in writes[:64]]
+    delta_ok = all(np.array_equal(a, b) for a, b in zip(want, got))
+    payload = sum(n for _, _, n, _ in writes)
+    peak = measured_peaks().get("hbm_gbs", FALLBACK_HBM)
+    sc = 2 * payload / (scatter_ms * 1e-3) / 1e9
+    return {"bytes": total, "ms": round(restore_ms, 3), "gbps": round(total / (restore_ms * 1e-3) / 1e9, 2),
+            "wall_ms": round((t1 - t0) * 1e3, 3), "bound": "pcie (H2D, copy engine)",
+            "first_gated_buffer_ms": round(gate_ms, 3), "digests_match_checkpoint": restored_ok,
+            "delta_replay": {"pack_bytes": pack_bytes, "payload_bytes": payload, "scatter_ms": round(scatter_ms, 4),
+                             "scatter_gbps": round(sc, 1), "roofline_frac": round(sc / peak, 4),
+                             "alg_bytes": "2 x payload (read pack, write buffers)", "bit_exact": bool(delta_ok)}}
 
 
 def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
@@ -704,7 +782,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3"], default="c2")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")

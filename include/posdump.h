@@ -208,6 +208,20 @@ int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_
  * `stream` by k_copy_host. */
 int pos_delta_drain(pos_ctx* ctx, void* stream);
 
+/* ---- CoW staging (gate_cow / stage_buffers, cr.hpp:806-888) ------------- */
+/* A kernel about to overwrite buffers of the snapshot before this epoch's
+ * pre-copy has saved them: every chunk of those buffers (in the snapshot,
+ * not staged yet) is copied -- and hashed while copying -- into a staging
+ * POSD pack (flag 4) at the top of the cache, on `stream` (the application's
+ * stream: its next kernel runs after the copy, stream order).  The buffers
+ * keep the staged digests and are left out of this epoch's pre-copy; the
+ * staged pack is part of the checkpoint.  POS_E_STAGING_EXHAUSTED when the
+ * free cache cannot hold it (the reference then delays the kernel,
+ * cr.hpp:837); POS_E_BAD_STATE once the epoch's pre-copy has started.  The
+ * staging is released by pos_commit_epoch. */
+int pos_stage_buffers(pos_ctx* ctx, const uint64_t* handles, uint32_t n, void* stream,
+                      uint64_t* pack_offset, uint64_t* pack_bytes);
+
 /* ---- STW delta-copy --------------------------------------------------- */
 /* at_final_stop (cr.hpp:599-621): every chunk of the buffers in dirty_set_ is
  * gathered into the cache as a second POSD pack starting at *pack_offset
@@ -258,6 +272,25 @@ int pos_pack_apply_host(const uint8_t* pack, uint64_t pack_bytes, const uint64_t
  * the host's threads.  Returns when the last scatter finished. */
 int pos_restore_packs(pos_ctx* ctx, const uint8_t* const* packs, const uint64_t* sizes, uint32_t n,
                       void* h2d_stream, void* stream, uint64_t region_bytes);
+
+/* On-demand restore of a flat host image (restore(), cr.hpp:167-204:
+ * start_loads / enqueue_load / gate_restore, cr.hpp:1043-1143): hosts[i] is
+ * the image of registered buffer i (the direct pre-copy's image, or any host
+ * copy).  A loader thread feeds H2D slices of slice_bytes (0 => 8 MiB) on
+ * h2d_stream in `order` (topo_order_buffers, dag.hpp:141-202; the rest by
+ * handle), at most 4 slices ahead, and records a ready event per buffer.
+ * Returns at once. */
+int pos_restore_image_begin(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n,
+                            const uint64_t* order, uint32_t norder, uint64_t slice_bytes, void* h2d_stream);
+/* bump_front (engines.hpp:86-93): the buffer's remaining slices go next. */
+int pos_restore_want(pos_ctx* ctx, uint64_t handle);
+/* gate_restore for one buffer of a kernel about to be enqueued on `stream`:
+ * bumps it, waits (host) until its last slice is issued, then makes
+ * `stream` wait (device) for it to land.  No restore running: no-op. */
+int pos_restore_gate(pos_ctx* ctx, uint64_t handle, void* stream);
+int pos_restore_ready(pos_ctx* ctx, uint64_t handle, int* ready);
+/* All buffers loaded (check_all_loaded, cr.hpp:1091-1096); ends the restore. */
+int pos_restore_image_wait(pos_ctx* ctx);
 
 /* ---- device crc32 (crc32.hpp:26-34 over device memory) ---------------- */
 int pos_crc32(uint64_t dev_ptr, uint64_t n, uint32_t* out, void* stream);

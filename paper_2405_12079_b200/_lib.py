@@ -119,12 +119,18 @@ SIGNATURES = {
     "pos_precopy_direct_result": [P, PU64, PU64, PU64],
     "pos_delta_drain": [P, P],
     "pos_delta_copy": [P, P, PU64, PU64],
+    "pos_stage_buffers": [P, P, U32, P, PU64, PU64],
     "pos_delta_copy_ex": [P, P, I32, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],
     "pos_cache_info": [P, PU64, PU64],
     "pos_scatter": [P, U64, U64, P],
     "pos_restore_packs": [P, P, P, U32, P, P, U64],
+    "pos_restore_image_begin": [P, P, P, U32, P, U32, U64, P],
+    "pos_restore_want": [P, U64],
+    "pos_restore_gate": [P, U64, P],
+    "pos_restore_ready": [P, U64, C.POINTER(C.c_int)],
+    "pos_restore_image_wait": [P],
     "pos_crc32": [U64, U64, PU32, P],
     "pos_crc32_update": [U32, U64, U64, PU32, P],
     "pos_fill": [U64, U64, U64, P],

@@ -42,6 +42,7 @@ enum : uint32_t {
   kBufHasUpstream = 1u,
   kBufHostUntouched = 2u,
   kBufWrittenSinceCkpt = 8u,
+  kBufStaged = 16u,  // CoW-staged this epoch: its snapshot is the staged pack
 };
 
 struct CopyItem {            // one contiguous copy: chunk -> pack, or pack -> chunk
@@ -58,6 +59,7 @@ constexpr uint32_t kPackAlign = 256;
 constexpr uint32_t kPackMagic = 0x44534F50u;  // "POSD"
 constexpr uint32_t kPackFlagDelta = 1u;        // STW delta pack
 constexpr uint32_t kPackFlagDirect = 2u;       // index only: payload went straight to the host image
+constexpr uint32_t kPackFlagStaged = 4u;       // CoW staging pack (stage_buffers)
 
 struct HashParams {
   const DevBuf* bufs;
@@ -445,12 +447,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
       crc = v ^ k_len;
     }
     if (lane == 31) {
-      p.digest_cur[g] = crc;
+      // a CoW-staged buffer keeps the digest of its staged snapshot (pre-copy hash only)
+      const bool staged = !WORK && p.flags && (b.flags & kBufStaged);
+      if (!staged) p.digest_cur[g] = crc;
       if (WORK) {
         uint4* e = reinterpret_cast<uint4*>(p.pack + kPackHeader + (uint64_t)entry * kPackEntry);
         e[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)dst_off,
                           (uint32_t)(dst_off >> 32));
         e[1] = make_uint4(cm.y, (uint32_t)len, crc, 0u);
+      } else if (staged) {
+        p.flags[g] = 0;  // its snapshot is in the staging pack: nothing to ship
       } else if (p.flags) {
         const bool dirty = !p.prev_valid || p.digest_prev[g] != crc;
         p.flags[g] = dirty;
@@ -935,14 +941,16 @@ __global__ void k_copy_simt(const CopyItem* items, const uint64_t* n_items_dev, 
 // small CTAs -- no shared memory, few registers -- so they co-reside with the
 // hash kernel's one-CTA-per-SM launch and with application blocks.  Each warp
 // streams one item at a time: kHostUnroll 16-B loads per lane in flight, then
-// the same number of 16-B stores, which leave the SM as posted PCIe writes
+// the same number of 16-B stores, which leave the SM as posted PCIe writes.
+// <= 32 registers (launch bounds): 4 warps fit beside the hash kernel's
+// 16 x 120-register warps, so the drain runs while later waves hash
 // (the link, ~53 GB/s for SM stores, is the bound; 8 CTAs saturate it).
 // Items whose src/dst are not both 16-B aligned, and item tails, go by byte.
 constexpr int kHostCopyThreads = 128;
 constexpr int kHostCopyCtas = 16;
 constexpr int kHostUnroll = 4;
 
-__global__ void __launch_bounds__(kHostCopyThreads) k_copy_host(const CopyItem* items,
+__global__ void __launch_bounds__(kHostCopyThreads, 16) k_copy_host(const CopyItem* items,
                                                                const uint64_t* n_items_dev,
                                                                uint64_t n_items_host) {
   const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
@@ -952,17 +960,19 @@ __global__ void __launch_bounds__(kHostCopyThreads) k_copy_host(const CopyItem* 
     const CopyItem c = items[i];
     const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
     uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
-    uint64_t body = ((c.src | c.dst) & 15) == 0 ? c.len & ~15ull : 0;
-    constexpr uint64_t kStep = 32 * 16 * kHostUnroll;
-    uint64_t o = 0;
-    for (; o + kStep <= body; o += kStep) {
+    const uint64_t body = ((c.src | c.dst) & 15) == 0 ? c.len & ~15ull : 0;
+    constexpr uint32_t kStep = 32 * 16 * kHostUnroll;
+    const uint4* sp = reinterpret_cast<const uint4*>(s) + lane;
+    uint4* dp = reinterpret_cast<uint4*>(d) + lane;
+    const uint4* const se = reinterpret_cast<const uint4*>(s + body / kStep * kStep);
+    for (; sp < se; sp += 32 * kHostUnroll, dp += 32 * kHostUnroll) {
       uint4 v[kHostUnroll];
 #pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) v[u] = ldg_stream(s + o + (u * 32 + lane) * 16);
+      for (int u = 0; u < kHostUnroll; ++u) v[u] = ldg_stream(sp + u * 32);
 #pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) *reinterpret_cast<uint4*>(d + o + (u * 32 + lane) * 16) = v[u];
+      for (int u = 0; u < kHostUnroll; ++u) dp[u * 32] = v[u];
     }
-    for (uint64_t q = o + lane * 16; q + 16 <= body; q += 32 * 16)
+    for (uint64_t q = body / kStep * kStep + lane * 16; q + 16 <= body; q += 32 * 16)
       *reinterpret_cast<uint4*>(d + q) = ldg_stream(s + q);
     for (uint64_t q = body + lane; q < c.padded; q += 32) d[q] = q < c.len ? s[q] : 0;
   }

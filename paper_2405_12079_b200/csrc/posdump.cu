@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -193,8 +195,34 @@ struct Timer {
 
 }  // namespace
 
+// On-demand restore of a flat host image (start_loads / enqueue_load /
+// gate_restore / bump_front, cr.hpp:1043-1143, engines.hpp:63-93): a loader
+// thread feeds the copy engine H2D slices from a priority queue of buffers,
+// keeping only kLoadWindow slices in flight so a wanted buffer jumps ahead
+// within ~kLoadWindow * slice of link time; each buffer's last slice records
+// its ready event, which gates kernels on the device (cudaStreamWaitEvent).
+struct Loader {
+  static constexpr int kLoadWindow = 4;
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<uint32_t> queue;         // buffer indices with bytes left to issue; front = next
+  std::vector<uint64_t> issued;       // bytes issued per buffer
+  std::vector<uint8_t> state;         // 0 queued, 1 ready event recorded, 2 not part of the image
+  std::vector<cudaEvent_t> ready;     // per buffer
+  std::vector<const uint8_t*> src;    // host image per buffer
+  cudaEvent_t ring[kLoadWindow] = {};
+  std::vector<void*> pinned_here;     // ranges the loader pinned (unpinned at the end)
+  cudaStream_t stream = nullptr;
+  uint64_t slice = 8ull << 20;
+  int device = 0;
+  bool running = false, failed = false;
+  std::string error;
+};
+
 struct pos_ctx {
   pos_config cfg{};
+  Loader* loader = nullptr;
   CrcTables crc;
   // Buffer set (ascending handle).
   std::vector<pos_buffer_desc> bufs;
@@ -250,10 +278,14 @@ struct pos_ctx {
   // O3 cache
   DevArray<uint8_t> cache;
   uint64_t cache_cap = 0;
+  // CoW staging (pos_stage_buffers): packs grow down from the top of the cache
+  uint64_t staging_used = 0;
+  std::vector<uint32_t> staged;  // buffer indices staged this epoch
   uint64_t precopy_bytes = 0;
   DevArray<CopyItem> d_items;
   DevArray<uint64_t> d_scan;     // [n, total, overflow]
   DevArray<uint4> d_work;
+  DevArray<uint4> d_stage_work;  // CoW staging work list
   DevArray<uint32_t> d_err;
   PinnedArray<uint64_t> h_scan;
   PinnedArray<uint8_t> h_stage;  // delta header + work list upload
@@ -441,8 +473,11 @@ int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
   });
 }
 
+static void loader_finish(pos_ctx* c);
+
 int pos_ctx_destroy(pos_ctx* c) {
   if (!c) return POS_OK;
+  loader_finish(c);
   cudaDeviceSynchronize();
   c->crc.tables.release();
   c->crc.xinv.release();
@@ -470,6 +505,7 @@ int pos_ctx_destroy(pos_ctx* c) {
   for (void* h : c->image_pinned) cudaHostUnregister(h);
   c->d_scan.release();
   c->d_work.release();
+  c->d_stage_work.release();
   c->d_err.release();
   c->h_scan.release();
   c->h_stage.release();
@@ -769,6 +805,15 @@ int pos_hash_chunks(pos_ctx* c, void* stream) {
 int pos_commit_epoch(pos_ctx* c) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->staged.empty()) {  // the staged snapshots were part of this checkpoint
+      ck(cudaDeviceSynchronize(), "sync");
+      for (uint32_t i : c->staged) {
+        c->hbufs[i].flags &= ~kBufStaged;
+        ck(cudaMemcpy(c->d_bufs.p + i, &c->hbufs[i], sizeof(DevBuf), cudaMemcpyHostToDevice), "unstage");
+      }
+      c->staged.clear();
+    }
+    c->staging_used = 0;
     c->cur ^= 1;
     c->prev_valid = true;
     ++c->epoch;
@@ -872,7 +917,7 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
   k_pack_scan<<<1, kScanThreads, 0, s>>>(
       c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p,
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
-      c->cache_cap, cursor, c->d_items.p + lo, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
+      c->cache_cap - c->staging_used, cursor, c->d_items.p + lo, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
       c->d_tcs.p, c->d_xfold.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base, direct ? 1 : 0,
       c->d_bitmap.p, c->n_chunks);
   c->slot_seq[slot] = c->scan_seq;
@@ -1175,7 +1220,7 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
     uint64_t reserve = 0;
     for (uint32_t w = 0; w < W; ++w)
       reserve += round_up(kPackHeader + kPackEntry * (chunk_of(bb[w + 1]) - chunk_of(bb[w])), kPackAlign);
-    if (reserve > c->cache_cap) fail(POS_E_STAGING_EXHAUSTED, "index packs exceed the cache");
+    if (reserve > c->cache_cap - c->staging_used) fail(POS_E_STAGING_EXHAUSTED, "index packs exceed the cache");
     upload_dag_flags(c, s, ds);  // on the drain stream, under the first hash
     c->timer_begin(kTimHash, s);
     for (uint32_t w = 0; w < W; ++w) {
@@ -1221,6 +1266,103 @@ int pos_delta_drain(pos_ctx* c, void* stream) {
   });
 }
 
+int pos_stage_buffers(pos_ctx* c, const uint64_t* handles, uint32_t n, void* stream, uint64_t* pack_offset,
+                      uint64_t* pack_bytes) {
+  return guarded([&] {
+    if (!c || (n && !handles)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (c->pack_pending || c->direct_pending || c->precopy_bytes)
+      fail(POS_E_BAD_STATE, "stage before this epoch's pre-copy (its packs may already hold the buffers)");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    cudaStream_t s = S(stream);
+    const uint64_t cs = c->cfg.chunk_size;
+    // conflicts in the snapshot, ascending handle, not staged yet (gate_cow, cr.hpp:822-826)
+    std::set<uint32_t> idx;
+    for (uint32_t j = 0; j < n; ++j) {
+      auto it = c->index_of.find(handles[j]);
+      if (it == c->index_of.end()) continue;
+      if (c->hbufs[it->second].flags & kBufStaged) continue;
+      idx.insert(it->second);
+    }
+    std::vector<uint4> work;
+    uint64_t payload = 0;
+    uint32_t entry = 0;
+    for (uint32_t i : idx) {
+      const DevBuf& b = c->hbufs[i];
+      for (uint32_t q = 0; q < b.nchunks; ++q) {
+        const uint64_t len = q + 1 == b.nchunks ? b.size - (uint64_t)q * cs : cs;
+        const uint64_t g = c->chunk_base[i] + q;
+        work.push_back(make_uint4((uint32_t)g, entry++, (uint32_t)payload, (uint32_t)(payload >> 32)));
+        payload += round_up(len, 16);
+      }
+    }
+    const uint64_t ne = work.size();
+    const uint64_t payload_off = round_up(kPackHeader + kPackEntry * ne, kPackAlign);
+    const uint64_t total = payload_off + payload;
+    const uint64_t span = round_up(total, kPackAlign);
+    // stage_buffers: staging_used_ + bytes <= staging_capacity() (cr.hpp:860)
+    if (c->staging_used + span > c->cache_cap)
+      fail(POS_E_STAGING_EXHAUSTED, "staging " + std::to_string(total) + " B exceeds the free cache");
+    if (pack_offset) *pack_offset = 0;
+    if (pack_bytes) *pack_bytes = 0;
+    if (!ne) return;
+    const uint64_t offset = c->cache_cap - c->staging_used - span;
+    uint8_t* pack = c->cache.p + offset;
+    const uint64_t work_bytes = ne * sizeof(uint4);
+    if (c->stage_free) ck(cudaEventSynchronize(c->stage_free), "stage sync");
+    c->h_stage.ensure(kPackHeader + work_bytes + idx.size() * sizeof(DevBuf));
+    uint8_t* st = c->h_stage.p;
+    std::memset(st, 0, kPackHeader);
+    uint32_t magic = kPackMagic, ver = 1, nn = (uint32_t)ne, flags = kPackFlagStaged;
+    std::memcpy(st + 0, &magic, 4);
+    std::memcpy(st + 4, &ver, 4);
+    std::memcpy(st + 8, &cs, 8);
+    std::memcpy(st + 16, &nn, 4);
+    std::memcpy(st + 20, &flags, 4);
+    std::memcpy(st + 24, &payload_off, 8);
+    std::memcpy(st + 32, &payload, 8);
+    std::memcpy(st + 40, &c->epoch, 8);
+    std::memcpy(st + 48, &total, 8);
+    std::memcpy(st + kPackHeader, work.data(), work_bytes);
+    ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "staging header");
+    if (payload_off > kPackHeader + kPackEntry * ne)
+      ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * ne, 0, payload_off - kPackHeader - kPackEntry * ne, s),
+         "gap");
+    c->d_stage_work.ensure(ne);  // own array: the delta's work list may be staged concurrently
+    ck(cudaMemcpyAsync(c->d_stage_work.p, st + kPackHeader, work_bytes, cudaMemcpyHostToDevice, s), "work");
+    // the buffers become kBufStaged: the pre-copy hash keeps their staged digests
+    DevBuf* upd = reinterpret_cast<DevBuf*>(st + kPackHeader + work_bytes);
+    uint32_t u = 0;
+    for (uint32_t i : idx) {
+      c->hbufs[i].flags |= kBufStaged;
+      upd[u] = c->hbufs[i];
+      ck(cudaMemcpyAsync(c->d_bufs.p + i, upd + u, sizeof(DevBuf), cudaMemcpyHostToDevice, s), "stage flag");
+      ++u;
+      c->staged.push_back(i);
+    }
+    ck(cudaEventRecord(c->stage_free, s), "event");
+    // hash while copying: staged digests + entries + payload (the stop-point bytes)
+    HashParams p{};
+    p.bufs = c->d_bufs.p;
+    p.chunk_map = c->d_chunk_map.p;
+    p.n_items = ne;
+    p.chunk_size = cs;
+    p.k_full = zeros_crc(cs);
+    p.tables = c->crc.tables.p;
+    p.xinv = c->crc.xinv.p;
+    p.digest_cur = c->d_digest[c->cur].p;
+    p.work = c->d_stage_work.p;
+    p.pack = pack;
+    p.payload_off = payload_off;
+    set_segments(c, ne, p);
+    launch_hash<kModeCopy>(c->hash_grid(ne * p.nseg), s, p);
+    check_launch("k_hash_chunks<copy>");
+    ++c->launches;
+    c->staging_used += span;
+    if (pack_offset) *pack_offset = offset;
+    if (pack_bytes) *pack_bytes = total;
+  });
+}
+
 int pos_precopy_size(pos_ctx* c, uint64_t* pack_bytes) {
   return guarded([&] {
     if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
@@ -1256,7 +1398,8 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
   const uint64_t n = work.size();
   const uint64_t payload_off = round_up(kPackHeader + kPackEntry * n, kPackAlign);
   const uint64_t total = payload_off + payload;
-  if (offset + total > c->cache_cap) fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
+  if (offset + total > c->cache_cap - c->staging_used)
+    fail(POS_E_STAGING_EXHAUSTED, "delta pack exceeds the cache");
   uint8_t* pack = c->cache.p + offset;
   for (auto& it : items) it.dst = (uint64_t)pack + payload_off + it.dst;
   // Stage the header, the work list (for the post-stop hash) and the gather items.
@@ -1425,7 +1568,6 @@ int pos_scatter(pos_ctx* c, uint64_t pack_dev, uint64_t pack_bytes, void* stream
     if (!n) return;
     c->d_items.ensure(std::max<uint64_t>(n, c->n_chunks));
     ck(cudaMemsetAsync(c->d_err.p, 0, 4, s), "memset");
-    c->timer_begin(kTimScatter, s);
     k_pack_items<<<(n + 255) / 256, 256, 0, s>>>((const uint8_t*)pack_dev, pack_bytes, c->d_bufs.p,
                                                 (uint32_t)c->bufs.size(), c->cfg.chunk_size,
                                                 c->d_items.p, c->d_err.p);
@@ -1441,6 +1583,7 @@ int pos_scatter(pos_ctx* c, uint64_t pack_dev, uint64_t pack_bytes, void* stream
     // construction); the <16 B remainder is written byte-exact.
     bool aligned = c->cfg.chunk_size % 16 == 0 && payload_off % 16 == 0 && pack_dev % 16 == 0;
     for (const auto& b : c->bufs) aligned = aligned && (b.dev_ptr % 16 == 0);
+    c->timer_begin(kTimScatter, s);  // the HBM-bound part (validation above is a host round trip)
     launch_copy(c, c->d_items.p, nullptr, n, aligned, s);
     c->timer_end(kTimScatter, s);
   });
@@ -1546,6 +1689,185 @@ int pos_restore_packs(pos_ctx* c, const uint8_t* const* packs, const uint64_t* s
     }
     c->timer_end(kTimScatter, s);
     ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+// ---- on-demand restore of a flat host image --------------------------------
+
+static void loader_run(pos_ctx* c) {
+  Loader& L = *c->loader;
+  cudaSetDevice(L.device);
+  uint64_t k = 0;  // slices issued
+  for (;;) {
+    uint32_t b;
+    uint64_t off, n;
+    {
+      std::unique_lock<std::mutex> lk(L.mu);
+      if (L.queue.empty() || L.failed) break;
+      b = L.queue.front();
+      off = L.issued[b];
+      n = std::min<uint64_t>(L.slice, c->bufs[b].size - off);
+      L.issued[b] = off + n;
+    }
+    // flow control: slice k reuses the ring event of slice k - kLoadWindow
+    cudaEvent_t& ev = L.ring[k % Loader::kLoadWindow];
+    cudaError_t e = cudaSuccess;
+    if (k >= (uint64_t)Loader::kLoadWindow) e = cudaEventSynchronize(ev);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((void*)(c->bufs[b].dev_ptr + off), L.src[b] + off, n, cudaMemcpyHostToDevice, L.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, L.stream);
+    ++k;
+    std::lock_guard<std::mutex> lk(L.mu);
+    if (e != cudaSuccess) {
+      L.failed = true;
+      L.error = cudaGetErrorString(e);
+      L.cv.notify_all();
+      break;
+    }
+    if (L.issued[b] == c->bufs[b].size) {  // last slice of b: its ready event
+      cudaEventRecord(L.ready[b], L.stream);
+      L.state[b] = 1;
+      auto it = std::find(L.queue.begin(), L.queue.end(), b);
+      if (it != L.queue.end()) L.queue.erase(it);
+      L.cv.notify_all();
+    }
+  }
+  std::lock_guard<std::mutex> lk(L.mu);
+  L.running = false;
+  L.cv.notify_all();
+}
+
+static void loader_finish(pos_ctx* c) {
+  if (!c->loader) return;
+  Loader* L = c->loader;
+  if (L->th.joinable()) L->th.join();
+  if (L->stream) cudaStreamSynchronize(L->stream);
+  for (auto e : L->ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : L->ring)
+    if (e) cudaEventDestroy(e);
+  for (void* h : L->pinned_here) cudaHostUnregister(h);
+  delete L;
+  c->loader = nullptr;
+}
+
+int pos_restore_image_begin(pos_ctx* c, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n,
+                            const uint64_t* order, uint32_t norder, uint64_t slice_bytes, void* h2d_stream) {
+  return guarded([&] {
+    if (!c || (n && (!hosts || !sizes)) || (norder && !order)) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (n != c->bufs.size()) fail(POS_E_INVALID_ARGUMENT, "one image range per registered buffer");
+    if (c->loader) fail(POS_E_BAD_STATE, "a restore is already running (pos_restore_image_wait)");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    auto* L = new Loader();
+    c->loader = L;
+    L->device = c->cfg.device;
+    L->stream = S(h2d_stream);
+    if (slice_bytes) L->slice = slice_bytes;
+    L->issued.assign(n, 0);
+    L->state.assign(n, 2);
+    L->ready.assign(n, nullptr);
+    L->src.assign(hosts, hosts + n);
+    for (int i = 0; i < Loader::kLoadWindow; ++i)
+      ck(cudaEventCreateWithFlags(&L->ring[i], cudaEventDisableTiming), "event");
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!hosts[i] || sizes[i] != c->bufs[i].size)
+        fail(POS_E_INVALID_ARGUMENT, "image range " + std::to_string(i) + " does not match its buffer");
+      cudaPointerAttributes a{};
+      cudaError_t e = cudaPointerGetAttributes(&a, hosts[i]);
+      if (e != cudaSuccess) cudaGetLastError();
+      if (e != cudaSuccess || a.type != cudaMemoryTypeHost) {
+        ck(cudaHostRegister(hosts[i], sizes[i], cudaHostRegisterPortable), "cudaHostRegister(restore image)");
+        L->pinned_here.push_back(hosts[i]);
+      }
+      ck(cudaEventCreateWithFlags(&L->ready[i], cudaEventDisableTiming), "event");
+    }
+    // load order: `order` first (topo_order_buffers, dag.hpp:141-202), then
+    // the rest by handle; unknown handles in `order` are ignored
+    std::vector<uint8_t> seen(n, 0);
+    for (uint32_t j = 0; j < norder; ++j) {
+      auto it = c->index_of.find(order[j]);
+      if (it == c->index_of.end() || seen[it->second]) continue;
+      seen[it->second] = 1;
+      L->queue.push_back(it->second);
+      L->state[it->second] = 0;
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      if (!seen[i]) {
+        L->queue.push_back(i);
+        L->state[i] = 0;
+      }
+    L->running = true;
+    L->th = std::thread(loader_run, c);
+  });
+}
+
+// bump_front (engines.hpp:86-93): the buffer's remaining slices go next.
+static uint32_t loader_want(pos_ctx* c, uint64_t handle) {
+  Loader& L = *c->loader;
+  auto it = c->index_of.find(handle);
+  if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "unknown handle");
+  const uint32_t b = it->second;
+  std::lock_guard<std::mutex> lk(L.mu);
+  if (L.state[b] == 0) {
+    auto q = std::find(L.queue.begin(), L.queue.end(), b);
+    if (q != L.queue.end() && q != L.queue.begin()) {
+      L.queue.erase(q);
+      L.queue.push_front(b);
+    }
+  }
+  return b;
+}
+
+int pos_restore_want(pos_ctx* c, uint64_t handle) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->loader) fail(POS_E_BAD_STATE, "no restore running");
+    loader_want(c, handle);
+  });
+}
+
+int pos_restore_gate(pos_ctx* c, uint64_t handle, void* stream) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->loader) return;  // nothing being restored: every buffer is ready
+    const uint32_t b = loader_want(c, handle);
+    Loader& L = *c->loader;
+    std::unique_lock<std::mutex> lk(L.mu);
+    // host waits only until the last slice is ISSUED; the device waits for it to land
+    L.cv.wait(lk, [&] { return L.state[b] != 0 || L.failed; });
+    if (L.failed) fail(POS_E_CUDA, "restore loader: " + L.error);
+    ck(cudaStreamWaitEvent(S(stream), L.ready[b], 0), "gate wait");
+  });
+}
+
+int pos_restore_ready(pos_ctx* c, uint64_t handle, int* ready) {
+  return guarded([&] {
+    if (!c || !ready) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->loader) {
+      *ready = 1;
+      return;
+    }
+    auto it = c->index_of.find(handle);
+    if (it == c->index_of.end()) fail(POS_E_INVALID_LOCATOR, "unknown handle");
+    Loader& L = *c->loader;
+    std::lock_guard<std::mutex> lk(L.mu);
+    *ready = L.state[it->second] == 1 && cudaEventQuery(L.ready[it->second]) == cudaSuccess;
+    cudaGetLastError();
+  });
+}
+
+int pos_restore_image_wait(pos_ctx* c) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->loader) return;
+    std::string err;
+    {
+      Loader& L = *c->loader;
+      if (L.th.joinable()) L.th.join();
+      if (L.failed) err = L.error;
+    }
+    loader_finish(c);
+    if (!err.empty()) fail(POS_E_CUDA, "restore loader: " + err);
   });
 }
 

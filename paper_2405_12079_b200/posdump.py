@@ -429,6 +429,16 @@ class DumpEngine:
         self.precopy_bytes = n.value
         return n.value
 
+    # ---- CoW staging (gate_cow / stage_buffers, cr.hpp:806-888)
+    def stage_buffers(self, handles: Iterable[int], stream=None) -> tuple[int, int]:
+        """Stage whole buffers (stop-point bytes) into a staging pack before a
+        kernel overwrites them; returns (cache offset, pack bytes)."""
+        hs = np.array(sorted(set(handles)), dtype=np.uint64)
+        off, n = C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_stage_buffers(self.ctx, hs.ctypes.data if hs.size else None, hs.size, _s(stream),
+                                      C.byref(off), C.byref(n)))
+        return off.value, n.value
+
     # ---- STW delta-copy (at_final_stop, cr.hpp:599-621)
     def at_final_stop(self, stream=None, stw_end_slot: int = -1) -> tuple[int, int]:
         """STW delta pack: bulk gather (records event stw_end_slot when >= 0),
@@ -466,6 +476,34 @@ class DumpEngine:
         sizes = np.array([a.nbytes for a in arrs], dtype=np.uint64)
         check(lib().pos_restore_packs(self.ctx, ptrs, sizes.ctypes.data, n, _s(h2d_stream), _s(stream),
                                       region_bytes))
+
+    # ---- on-demand restore of a flat host image (restore / gate_restore, cr.hpp:167-204, 1043-1143)
+    def restore_image_begin(self, hosts: Sequence[np.ndarray], order: Sequence[int] = (), slice_bytes: int = 0,
+                            h2d_stream=None) -> None:
+        arrs = [np.ascontiguousarray(h).view(np.uint8).reshape(-1) for h in hosts]
+        n = len(arrs)
+        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
+        sizes = np.array([a.size for a in arrs], dtype=np.uint64)
+        order_a = np.array(list(order), dtype=np.uint64)
+        self._restore_keep = arrs
+        check(lib().pos_restore_image_begin(self.ctx, ptrs, sizes.ctypes.data, n,
+                                            order_a.ctypes.data if order_a.size else None, order_a.size,
+                                            slice_bytes, _s(h2d_stream)))
+
+    def restore_want(self, handle: int) -> None:
+        check(lib().pos_restore_want(self.ctx, handle))
+
+    def restore_gate(self, handle: int, stream=None) -> None:
+        check(lib().pos_restore_gate(self.ctx, handle, _s(stream)))
+
+    def restore_ready(self, handle: int) -> bool:
+        r = C.c_int(0)
+        check(lib().pos_restore_ready(self.ctx, handle, C.byref(r)))
+        return bool(r.value)
+
+    def restore_image_wait(self) -> None:
+        check(lib().pos_restore_image_wait(self.ctx))
+        self._restore_keep = None
 
     # ---- timing
     def event_record(self, slot: int, stream=None) -> None:

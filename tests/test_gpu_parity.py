@@ -757,3 +757,92 @@ def test_o1_verdicts_many_candidates(orc):
         want = host[i] if i % 2 else np.zeros(size, np.uint8)
         assert np.array_equal(img[i], want)
     eng.close()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_ondemand_restore_from_image(orc, pinned):
+    """On-demand restore (restore / start_loads / gate_restore, cr.hpp:167-204,
+    1043-1143) of a flat host image: loads follow `order`, a gated buffer is
+    resident before a kernel enqueued behind the gate reads it (the device
+    waits on the buffer's ready event), and every buffer ends byte-exact."""
+    sizes = [3 << 20, 1 << 20, 700001, 12345, 5 << 20]
+    p = Proc(orc, sizes, seed0=6100)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=8 << 20))
+    eng.register_buffers(p.bufs)
+    if pinned:
+        pin = pd.PinnedHost(sum((n + 255) // 256 * 256 for n in sizes))
+        image, o = [], 0
+        for h in p.host:
+            image.append(pin.array[o:o + h.size])
+            image[-1][:] = h
+            o += (h.size + 255) // 256 * 256
+    else:
+        image = [h.copy() for h in p.host]
+    for i in range(len(sizes)):
+        p.zero(i)
+    pd.device_synchronize()
+    h2d, app = pd.Stream(), pd.Stream()
+    eng.restore_image_begin(image, order=[5, 4, 3, 2, 1], slice_bytes=256 << 10, h2d_stream=h2d)
+    # a "kernel" of the application touching buffer 1 (last in the load order)
+    eng.restore_gate(1, stream=app)
+    out = pd.DeviceMemory(sizes[0])
+    pd.check(pd.lib().pos_memcpy(out.ptr, p.bufs[0].dev_ptr, sizes[0], 3, int(app)))
+    app.synchronize()
+    assert np.array_equal(out.download(), p.host[0])
+    with pytest.raises(pd.SimError) as ei:
+        eng.restore_want(99)
+    assert ei.value.errc == "InvalidLocator"
+    eng.restore_image_wait()
+    for i in range(len(sizes)):
+        assert np.array_equal(p.read(i), p.host[i]), f"buffer {i}"
+    assert eng.restore_ready(1)  # no restore running: everything is ready
+    eng.close()
+
+
+@pytest.mark.parametrize("cs", [65536, 1000])
+def test_cow_staging_keeps_prewrite_bytes(orc, cs):
+    """CoW gate staging (stage_buffers, cr.hpp:858-888; after test_cr.cpp:
+    106-127): a writer lands on buffer `a` before the epoch's pre-copy saved
+    it; staging copies a's stop-point bytes into a staging pack, the kernel
+    then overwrites the live buffer, and the checkpoint (pre-copy pack +
+    staging pack) holds the pre-write payload while the other buffers ship
+    normally.  The next epoch sees `a` as dirty against its staged digest.
+    Staging more than the cache holds is StagingExhausted."""
+    sizes = [1 << 20, 300001, 70000]
+    p = Proc(orc, sizes, seed0=6600)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=3 << 20))
+    eng.register_buffers(p.bufs)
+    app = pd.Stream()
+    snap = [h.copy() for h in p.host]
+    off, n = eng.stage_buffers([1, 99], stream=app)  # unknown handle 99: not in the snapshot
+    assert n > 0 and off + n <= 3 << 20
+    # the kernel the gate let through, on the same (application) stream
+    pd.fill_bytes(p.bufs[0].dev_ptr + 5, 4000, 4242, stream=app)
+    p.host[0][5:4005] = mb(orc, 4242, 4000)
+    pd.device_synchronize()
+    m = eng.plan_precopy()
+    image = [np.zeros(s, np.uint8) for s in sizes]
+    pd.apply_pack_host(download_cache(eng, 0, m), p.handles, image)
+    staged = download_cache(eng, off, n)
+    assert int(staged[20:24].view(np.uint32)[0]) == 4  # staging pack flag
+    pd.apply_pack_host(staged, p.handles, image)
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], snap[i]), f"buffer {i}"
+    # the staging pack's entries carry the stop-point chunk crcs
+    ent = pd.parse_pack(staged)
+    assert list(ent["crc"]) == list(odigests(orc, snap[0], cs))
+    eng.commit_epoch()
+    # next epoch: `a` differs from its staged digest -> its written chunk ships
+    m = eng.plan_precopy()
+    ents = pd.parse_pack(download_cache(eng, 0, m))
+    assert set(int(h) for h in ents["handle"]) == {1}
+    assert set(int(c) for c in ents["chunk"]) == set(range(5 // cs, (5 + 4000 - 1) // cs + 1))
+    eng.commit_epoch()
+    eng.close()
+    small = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    small.register_buffers(p.bufs)
+    assert small.stage_buffers([3], stream=app)[1] > 0  # 70 KB fits
+    with pytest.raises(pd.SimError) as ei:
+        small.stage_buffers([1], stream=app)  # 1 MiB + header does not
+    assert ei.value.errc == "StagingExhausted"
+    small.close()
