@@ -587,7 +587,10 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": round(hash_ms, 5),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                         "note": ("dominant HBM kernel; the step's largest kernel by time is the drain "
+                                  "(k_copy_host in direct mode, ~87% of kernel time in the ncu launch list), "
+                                  "which is host-link bound: see host_link")},
             "host_link": {"bound": "pcie", "achieved": round(d2h_achieved, 2), "peak": round(link_peak, 2),
                           "unit": "GB/s", "frac": round(d2h_achieved / link_peak, 4),
                           "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run",

@@ -180,6 +180,19 @@ typedef void (*pos_pack_sink)(void* user, const uint8_t* pack, uint64_t bytes, u
 int pos_precopy_stream(pos_ctx* ctx, int exclude_dag_dirty, void* ckpt_stream, void* copy_stream,
                        uint64_t region_bytes, pos_pack_sink sink, void* user, uint64_t* total_bytes,
                        uint32_t* n_packs);
+/* NVLink peer-GPU cache for pos_precopy_stream (BASELINE config 5): `bytes`
+ * of device memory on peer_device hold whole cache regions; each wave's pack
+ * moves there by cudaMemcpyPeerAsync, freeing the local region at NVLink
+ * speed, and the peer's copy engine drains the slots to the host (its own
+ * PCIe link).  The snapshot is captured when the last wave sits in a slot.
+ * bytes == 0 detaches.  peer_device may equal the context's device (a D2D
+ * slot pool; single-GPU boxes).  POS_E_OUT_OF_DEVICE_MEMORY if it cannot be
+ * allocated. */
+int pos_peer_cache_attach(pos_ctx* ctx, int peer_device, uint64_t bytes);
+/* Of the last pos_precopy_stream through the peer cache: ms from its start
+ * until every pack was in the peer (capture) and until the last byte reached
+ * the host (total; -1 when the peer is another device). */
+int pos_peer_cache_stats(pos_ctx* ctx, float* capture_ms, float* total_ms);
 int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                           void* copy_stream, void* host_dst, uint64_t slice_bytes,
                           uint64_t* offsets, uint64_t* sizes, uint32_t* n_packs);

@@ -221,6 +221,56 @@ class DumpEngine {
     check(pos_scatter(ctx_, reinterpret_cast<uint64_t>(pack_dev), bytes, stream));
   }
 
+  // chunk_copied straight into the target's captured_ (cr.hpp:499-501): the
+  // image of each snapshot buffer (ascending handle), then the direct pre-copy.
+  void register_image(const std::vector<uint8_t*>& hosts) {
+    std::vector<uint64_t> sizes;
+    for (const auto& b : bufs_) sizes.push_back(b.size);
+    if (hosts.size() != bufs_.size()) throw SimError(Errc::InvalidArgument, "one image per buffer");
+    check(pos_register_image(ctx_, hosts.data(), sizes.data(), static_cast<uint32_t>(hosts.size())));
+  }
+  void plan_precopy_direct(uint32_t waves, void* ckpt_stream, void* drain_stream) {
+    check(pos_precopy_direct(ctx_, 1, waves, ckpt_stream, drain_stream));
+  }
+  // (chunks, payload bytes) the last direct pre-copy shipped.
+  std::pair<uint64_t, uint64_t> direct_result() {
+    uint64_t n = 0, pay = 0, idx = 0;
+    check(pos_precopy_direct_result(ctx_, &n, &pay, &idx));
+    return {n, pay};
+  }
+  void drain_final_stop(void* stream) { check(pos_delta_drain(ctx_, stream)); }
+
+  // note_h2d_provenance (process.hpp:505-522) with the copy itself.
+  void h2d(void* dst_dev, const void* host_src, uint64_t bytes, void* stream = nullptr) {
+    check(pos_h2d_provenance(ctx_, reinterpret_cast<uint64_t>(dst_dev), host_src, bytes, 1, stream));
+  }
+  std::optional<uint32_t> upstream_crc(BufferHandle h) {
+    uint32_t has = 0, crc = 0;
+    check(pos_read_upstream(ctx_, h, &has, &crc));
+    return has ? std::optional<uint32_t>(crc) : std::nullopt;
+  }
+
+  // gate_cow -> stage_buffers (cr.hpp:806-888): stop-point bytes of the
+  // conflicting writers into a staging pack, on the writer's stream.
+  PackRef stage_buffers(const std::vector<BufferHandle>& conflicts, void* app_stream) {
+    PackRef r;
+    check(pos_stage_buffers(ctx_, conflicts.data(), static_cast<uint32_t>(conflicts.size()), app_stream,
+                            &r.offset, &r.bytes));
+    return r;
+  }
+
+  // restore (cr.hpp:167-204) from a flat image: start_loads in `order`,
+  // gate_restore per kernel buffer, all_loaded.
+  void restore_begin(const std::vector<uint8_t*>& hosts, const std::vector<BufferHandle>& order,
+                     void* h2d_stream) {
+    std::vector<uint64_t> sizes;
+    for (const auto& b : bufs_) sizes.push_back(b.size);
+    check(pos_restore_image_begin(ctx_, hosts.data(), sizes.data(), static_cast<uint32_t>(hosts.size()),
+                                  order.data(), static_cast<uint32_t>(order.size()), 0, h2d_stream));
+  }
+  void gate_restore(BufferHandle h, void* stream) { check(pos_restore_gate(ctx_, h, stream)); }
+  void restore_wait() { check(pos_restore_image_wait(ctx_)); }
+
   // finalize_image's written_since_ckpt = false (cr.hpp:745): next epoch compares here.
   void end_checkpoint_session() {
     check(pos_commit_epoch(ctx_));

@@ -113,6 +113,8 @@ SIGNATURES = {
     "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
     "pos_precopy_stream": [P, I32, P, P, U64, P, P, PU64, PU32],
     "pos_register_image": [P, P, P, U32],
+    "pos_peer_cache_attach": [P, I32, U64],
+    "pos_peer_cache_stats": [P, C.POINTER(C.c_float), C.POINTER(C.c_float)],
     "pos_h2d_provenance": [P, U64, P, U64, I32, P],
     "pos_read_upstream": [P, U64, PU32, PU32],
     "pos_precopy_direct": [P, I32, U32, P, P],

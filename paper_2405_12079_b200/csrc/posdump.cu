@@ -10,6 +10,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -220,9 +221,25 @@ struct Loader {
   std::string error;
 };
 
+// NVLink peer-GPU cache (BASELINE config 5): packs of the
+// cache-cycled pre-copy move to slots in a peer GPU's free HBM
+// (cudaMemcpyPeerAsync), which frees the local cache region at NVLink speed
+// (the snapshot is captured once every wave sits in the peer); the peer's
+// own copy engine then drains the slots over ITS PCIe link.
+struct PeerCache {
+  int device = -1;
+  uint8_t* base = nullptr;
+  uint64_t bytes = 0;
+  cudaStream_t stream = nullptr;             // on the peer device: the drain
+  std::vector<cudaEvent_t> in, free_;        // per slot: pack landed (local dev) / slot drained (peer dev)
+  cudaEvent_t land[2] = {}, t0 = nullptr, captured = nullptr, drained = nullptr;
+  float capture_ms = 0, total_ms = 0;
+};
+
 struct pos_ctx {
   pos_config cfg{};
   Loader* loader = nullptr;
+  PeerCache* peer = nullptr;
   CrcTables crc;
   // Buffer set (ascending handle).
   std::vector<pos_buffer_desc> bufs;
@@ -475,9 +492,12 @@ int pos_ctx_create(const pos_config* cfg, pos_ctx** out) {
 
 static void loader_finish(pos_ctx* c);
 
+static void peer_release(pos_ctx* c);
+
 int pos_ctx_destroy(pos_ctx* c) {
   if (!c) return POS_OK;
   loader_finish(c);
+  peer_release(c);
   cudaDeviceSynchronize();
   c->crc.tables.release();
   c->crc.xinv.release();
@@ -1077,6 +1097,11 @@ int pos_precopy_pipelined(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, voi
   });
 }
 
+static void precopy_stream_peer(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, cudaStream_t cs,
+                                uint64_t region, const std::vector<uint64_t>& cuts,
+                                const std::function<uint32_t(uint64_t)>& vb_of, pos_pack_sink sink,
+                                void* user, uint64_t* total_bytes);
+
 int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, void* copy_stream,
                        uint64_t region, pos_pack_sink sink, void* user, uint64_t* total_bytes,
                        uint32_t* n_packs) {
@@ -1131,6 +1156,18 @@ int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, voi
     }
     upload_dag_flags(c, s);
     ck(cudaMemsetAsync(c->d_verdict.p, 0, std::max<uint32_t>(nb, 1), s), "memset verdicts");
+    if (c->peer) {
+      uint64_t total = 0;
+      c->timer_begin(kTimHash, s);
+      precopy_stream_peer(c, exclude_dag_dirty, s, cs, region, cuts, vb_of, sink, user, &total);
+      c->timer_end(kTimHash, s);
+      c->pack_pending = false;
+      c->precopy_bytes = 0;
+      c->waves_last = std::min<uint32_t>(W, pos_ctx::kMaxWaves);
+      if (total_bytes) *total_bytes = total;
+      if (n_packs) *n_packs = W;
+      return;
+    }
     std::vector<uint64_t> sizes(W, 0);
     uint64_t total = 0;
     auto finish = [&](uint32_t w) {  // wave w's bytes are on the host: hand them over
@@ -1165,6 +1202,200 @@ int pos_precopy_stream(pos_ctx* c, int exclude_dag_dirty, void* ckpt_stream, voi
     if (total_bytes) *total_bytes = total;
     if (n_packs) *n_packs = W;
   });
+}
+
+static void peer_release(pos_ctx* c) {
+  if (!c->peer) return;
+  PeerCache* P = c->peer;
+  cudaSetDevice(P->device);
+  if (P->stream) cudaStreamSynchronize(P->stream);
+  for (auto e : P->in) if (e) cudaEventDestroy(e);
+  for (auto e : P->free_) if (e) cudaEventDestroy(e);
+  for (auto e : {P->land[0], P->land[1], P->t0, P->captured, P->drained}) if (e) cudaEventDestroy(e);
+  if (P->base) cudaFree(P->base);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  cudaSetDevice(c->cfg.device);
+  delete P;
+  c->peer = nullptr;
+}
+
+int pos_peer_cache_attach(pos_ctx* c, int peer_device, uint64_t bytes) {
+  return guarded([&] {
+    if (!c) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "device count");
+    if (peer_device < 0 || peer_device >= n) fail(POS_E_INVALID_ARGUMENT, "bad peer device ordinal");
+    peer_release(c);
+    if (bytes == 0) return;  // detach
+    auto* P = new PeerCache();
+    c->peer = P;
+    P->device = peer_device;
+    const int dev = c->cfg.device;
+    if (peer_device != dev) {  // NVLink / NVSwitch path both ways
+      int ok = 0;
+      ck(cudaDeviceCanAccessPeer(&ok, dev, peer_device), "can access peer");
+      if (ok) {
+        ck(cudaSetDevice(dev), "cudaSetDevice");
+        cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer access");
+        cudaGetLastError();
+      }
+    }
+    ck(cudaSetDevice(peer_device), "cudaSetDevice(peer)");
+    cudaError_t e = cudaMalloc(&P->base, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      cudaSetDevice(dev);
+      peer_release(c);
+      fail(POS_E_OUT_OF_DEVICE_MEMORY, "peer cache of " + std::to_string(bytes) + " B on device " +
+                                           std::to_string(peer_device));
+    }
+    P->bytes = bytes;
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "prio");
+    ck(cudaStreamCreateWithPriority(&P->stream, cudaStreamNonBlocking, lo), "peer stream");
+    for (auto* ev : {&P->land[0], &P->land[1]}) ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
+    ck(cudaEventCreate(&P->drained), "event");
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    ck(cudaEventCreate(&P->t0), "event");
+    ck(cudaEventCreate(&P->captured), "event");
+  });
+}
+
+int pos_peer_cache_stats(pos_ctx* c, float* capture_ms, float* total_ms) {
+  return guarded([&] {
+    if (!c || !c->peer) fail(POS_E_BAD_STATE, "no peer cache attached");
+    if (capture_ms) *capture_ms = c->peer->capture_ms;
+    if (total_ms) *total_ms = c->peer->total_ms;
+  });
+}
+
+// Cache-cycled pre-copy through the peer cache.  A capture thread runs the
+// waves (hash -> O1 -> scan -> compaction into local region w%2 -> peer slot
+// w%M) without waiting for the host; the calling thread drains peer slots
+// into the two landing slots on the peer's stream and hands packs to the
+// sink in order.  Slot reuse is event-ordered on the device; the only host
+// hand-offs are "wave w is in its slot" and "slot m is drained".
+static void precopy_stream_peer(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, cudaStream_t cs,
+                                uint64_t region, const std::vector<uint64_t>& cuts,
+                                const std::function<uint32_t(uint64_t)>& vb_of, pos_pack_sink sink,
+                                void* user, uint64_t* total_bytes) {
+  PeerCache& P = *c->peer;
+  const int dev = c->cfg.device;
+  const uint32_t W = (uint32_t)cuts.size() - 1;
+  const uint32_t M = (uint32_t)(P.bytes / region);
+  if (M == 0) fail(POS_E_STAGING_EXHAUSTED, "peer cache smaller than one cache region");
+  if (P.in.size() < M) {
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    while (P.in.size() < M) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      P.in.push_back(e);
+    }
+    ck(cudaSetDevice(P.device), "cudaSetDevice(peer)");
+    while (P.free_.size() < M) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      P.free_.push_back(e);
+    }
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  cudaEvent_t local_free[2] = {c->ev_d2h[0], c->ev_d2h[1]};  // local region r reusable
+  std::vector<uint64_t> sizes(W, 0);
+  std::mutex mu;
+  std::condition_variable cv;
+  uint32_t captured = 0, drained = 0;  // waves in a slot / slots drained (enqueued)
+  std::string err;
+  int err_code = POS_E_CUDA;
+  ck(cudaEventRecord(P.t0, s), "event");
+  std::thread cap([&] {
+    try {
+      ck(cudaSetDevice(dev), "cudaSetDevice");
+      for (uint32_t w = 0; w < W; ++w) {
+        const uint32_t r = w & 1, m = w % M;
+        hash_range(c, cuts[w], cuts[w + 1], s, w % pos_ctx::kMaxWaves);
+        if (w >= 2) ck(cudaStreamWaitEvent(s, local_free[r], 0), "wait region");
+        const uint32_t slot = w % pos_ctx::kMaxWaves;
+        launch_pack(c, exclude_dag_dirty, s, cuts[w], cuts[w + 1], slot, vb_of(cuts[w]), vb_of(cuts[w + 1]),
+                    (uint64_t)r * region);
+        ck(cudaEventRecord(c->ev_copied2[r], s), "event");
+        PackResult res = pack_result(c, slot);
+        if (w >= M) {  // slot m must have been drained (its D2H enqueued, then done on the device)
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return drained > w - M || !err.empty(); });
+          if (!err.empty()) return;
+          ck(cudaStreamWaitEvent(cs, P.free_[m], 0), "wait slot");
+        }
+        ck(cudaStreamWaitEvent(cs, c->ev_copied2[r], 0), "wait pack");
+        ck(cudaMemcpyPeerAsync(P.base + (uint64_t)m * region, P.device, c->cache.p + res.base, dev, res.total, cs),
+           "peer copy");
+        ck(cudaEventRecord(local_free[r], cs), "event");
+        ck(cudaEventRecord(P.in[m], cs), "event");
+        std::lock_guard<std::mutex> lk(mu);
+        sizes[w] = res.total;
+        ++captured;
+        cv.notify_all();
+      }
+      ck(cudaEventRecord(P.captured, cs), "event");
+    } catch (const Fail& f) {
+      std::lock_guard<std::mutex> lk(mu);
+      err = g_last_error.empty() ? "capture failed" : g_last_error;  // this thread's message
+      err_code = f.code;
+      cv.notify_all();
+    }
+  });
+  uint64_t total = 0;
+  auto finish = [&](uint32_t w) {
+    ck(cudaEventSynchronize(P.land[w & 1]), "d2h sync");
+    sink(user, c->h_land[w & 1].p, sizes[w], w);
+  };
+  try {
+    for (uint32_t w = 0; w < W; ++w) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return captured > w || !err.empty(); });
+        if (!err.empty()) break;
+      }
+      if (w >= 2) finish(w - 2);  // landing slot w&1 free
+      const uint32_t m = w % M, l = w & 1;
+      ck(cudaSetDevice(P.device), "cudaSetDevice(peer)");
+      ck(cudaStreamWaitEvent(P.stream, P.in[m], 0), "wait slot in");
+      for (uint64_t o = 0; o < sizes[w]; o += 8ull << 20)
+        ck(cudaMemcpyAsync(c->h_land[l].p + o, P.base + (uint64_t)m * region + o,
+                           std::min<uint64_t>(8ull << 20, sizes[w] - o), cudaMemcpyDeviceToHost, P.stream),
+           "peer d2h");
+      ck(cudaEventRecord(P.land[l], P.stream), "event");
+      ck(cudaEventRecord(P.free_[m], P.stream), "event");
+      ck(cudaSetDevice(dev), "cudaSetDevice");
+      total += sizes[w];
+      std::lock_guard<std::mutex> lk(mu);
+      ++drained;
+      cv.notify_all();
+    }
+  } catch (...) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (err.empty()) err = "drain failed";
+      cv.notify_all();
+    }
+    cap.join();
+    cudaSetDevice(dev);
+    throw;
+  }
+  cap.join();
+  ck(cudaSetDevice(dev), "cudaSetDevice");
+  if (!err.empty()) fail(err_code, "peer pre-copy: " + err);
+  for (uint32_t w = W >= 2 ? W - 2 : 0; w < W; ++w) finish(w);
+  ck(cudaSetDevice(P.device), "cudaSetDevice(peer)");
+  ck(cudaEventRecord(P.drained, P.stream), "event");
+  ck(cudaEventSynchronize(P.drained), "sync");
+  ck(cudaSetDevice(dev), "cudaSetDevice");
+  ck(cudaEventElapsedTime(&P.capture_ms, P.t0, P.captured), "elapsed");
+  // t0 (local device) -> drained (peer device): host-side gap is below the drain's length;
+  // measured as capture + the peer drain's own span when the devices differ.
+  if (P.device == dev) ck(cudaEventElapsedTime(&P.total_ms, P.t0, P.drained), "elapsed");
+  else P.total_ms = -1.0f;
+  *total_bytes = total;
 }
 
 int pos_register_image(pos_ctx* c, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n) {

@@ -423,6 +423,16 @@ class DumpEngine:
         """STW delta payload (in the cache) -> host image (pos_delta_drain)."""
         check(lib().pos_delta_drain(self.ctx, _s(stream)))
 
+    # ---- NVLink peer-GPU cache (config 5) for precopy_stream
+    def attach_peer_cache(self, peer_device: int, nbytes: int) -> None:
+        check(lib().pos_peer_cache_attach(self.ctx, peer_device, nbytes))
+
+    def peer_cache_stats(self) -> tuple[float, float]:
+        """(capture ms, total ms) of the last precopy_stream through the peer cache."""
+        a, b = C.c_float(0), C.c_float(0)
+        check(lib().pos_peer_cache_stats(self.ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def precopy_size(self) -> int:
         n = C.c_uint64(0)
         check(lib().pos_precopy_size(self.ctx, C.byref(n)))

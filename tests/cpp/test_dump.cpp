@@ -262,3 +262,80 @@ TEST_CASE("[gpu] staging exhaustion surfaces as StagingExhausted") {
 }
 
 int main(int argc, char** argv) { return minicatch::run(argc, argv); }
+
+TEST_CASE("[gpu] direct pre-copy writes chunk_copied's bytes straight into captured_") {
+  SimConfig cfg;
+  cfg.chunk_size = 65536;
+  cfg.cache_capacity = 8 << 20;
+  DumpEngine e(cfg);
+  DevBuf a(300000, 51), b(65536 * 3, 52);
+  e.snapshot({GpuBuffer{1, a.ptr, a.size}, GpuBuffer{2, b.ptr, b.size}});
+  void* pin = nullptr;
+  check(pos_host_malloc_pinned(a.size + b.size + 256, &pin));
+  uint8_t* ia = static_cast<uint8_t*>(pin);
+  uint8_t* ib = ia + (a.size + 255) / 256 * 256;
+  std::memset(pin, 0, a.size + b.size + 256);
+  e.register_image({ia, ib});
+  void *s1 = nullptr, *s2 = nullptr;
+  check(pos_stream_create(&s1));
+  check(pos_stream_create(&s2));
+  e.plan_precopy_direct(1, s1, s2);
+  check(pos_device_sync());
+  REQUIRE(e.direct_result().first == 5u + 3u);  // every chunk of a fresh target
+  e.end_checkpoint_session();
+  a.write(65536 + 3, 10, 61);
+  check(pos_device_sync());
+  e.record_dirty({2});  // the window's kernel is in the DAG from submission
+  e.plan_precopy_direct(1, s1, s2);
+  check(pos_device_sync());
+  b.write(100, 50, 62);
+  check(pos_device_sync());
+  e.at_final_stop(s1);
+  check(pos_stream_wait(s2, s1));
+  e.drain_final_stop(s2);
+  check(pos_device_sync());
+  REQUIRE(e.direct_result().first == 1u);  // the one rewritten chunk of buffer 1
+  REQUIRE(std::memcmp(ia, a.host.data(), a.size) == 0);
+  REQUIRE(std::memcmp(ib, b.host.data(), b.size) == 0);
+  pos_stream_destroy(s1);
+  pos_stream_destroy(s2);
+  pos_host_free_pinned(pin);
+}
+
+TEST_CASE("[gpu] CoW staging keeps the pre-write payload of a conflicting writer") {  // test_cr.cpp:106-127
+  SimConfig cfg;
+  cfg.chunk_size = 4096;
+  cfg.cache_capacity = 4 << 20;
+  DumpEngine e(cfg);
+  DevBuf a(1 << 20, 71);
+  e.snapshot({GpuBuffer{1, a.ptr, a.size}});
+  std::vector<uint8_t> before = a.host;
+  void* app = nullptr;
+  check(pos_stream_create(&app));
+  PackRef st = e.stage_buffers({1}, app);
+  REQUIRE(st.bytes > a.size);
+  check(pos_fill(a.ptr, a.size, 72, app));  // the writer, after the gate on its own stream
+  check(pos_device_sync());
+  PackRef pre = e.plan_precopy();
+  std::map<BufferHandle, std::vector<uint8_t>> captured{{1, std::vector<uint8_t>(a.size)}};
+  std::vector<uint8_t> p1 = pinned_d2h(e, pre), p2 = pinned_d2h(e, st);
+  REQUIRE(pack_entries(p1) == 0u);  // the staged buffer is not in the pre-copy
+  apply_pack(p2.data(), p2.size(), captured, 1);
+  REQUIRE(captured[1] == before);
+  pos_stream_destroy(app);
+}
+
+TEST_CASE("[gpu] H2D provenance records crc32 of the payload and dedups the buffer") {  // test_api.cpp:76-98
+  SimConfig cfg;
+  cfg.chunk_size = 4096;
+  cfg.cache_capacity = 1 << 20;
+  DumpEngine e(cfg);
+  DevBuf a(4096 * 40 + 7, 81);
+  e.snapshot({GpuBuffer{1, a.ptr, a.size}});
+  std::vector<uint8_t> payload(a.size);
+  or_fill_bytes(82, payload.data(), payload.size());
+  e.h2d(reinterpret_cast<void*>(a.ptr), payload.data(), payload.size());
+  REQUIRE(e.upstream_crc(1).value() == or_crc32(payload.data(), payload.size()));
+  PackRef pre = e.plan_precopy();
+  REQUIRE(pack_entries(pinned_d2h(e, pre)) == 0u);  // O1: nothing to ship
+}

@@ -524,8 +524,8 @@ def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode):
     eng.close()
 
 
-@pytest.mark.parametrize("region", [300_000, 1 << 20])
-def test_cache_cycled_precopy(orc, region):
+@pytest.mark.parametrize("region,peer_slots", [(300_000, 0), (1 << 20, 0), (300_000, 1), (300_000, 3)])
+def test_cache_cycled_precopy(orc, region, peer_slots):
     """States larger than the O3 cache (BASELINE configs 3/5): waves cycle two
     cache regions; the packs handed to the sink carry exactly the single-pack
     entries/payload, and verdicts of buffers spanning waves still apply."""
@@ -540,8 +540,15 @@ def test_cache_cycled_precopy(orc, region):
     big.close()
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=2 * region + 4096))
     eng.register_buffers(p.bufs)
+    if peer_slots:  # peer-GPU cache (config 5); the peer is this device on a 1-GPU box
+        eng.attach_peer_cache(pd.device_count() - 1, peer_slots * (region // 256 * 256))
     got = []
-    total, n = eng.precopy_stream(lambda arr, i: got.append((i, arr.copy())), region_bytes=region)
+    s, c = pd.Stream(), pd.Stream()
+    total, n = eng.precopy_stream(lambda arr, i: got.append((i, arr.copy())), region_bytes=region,
+                                  stream=s, copy_stream=c)
+    if peer_slots:
+        cap, tot = eng.peer_cache_stats()
+        assert cap > 0
     assert [i for i, _ in got] == list(range(n)) and n >= 2
     assert total == sum(a.size for _, a in got)
     ents = [pd.parse_pack(a) for _, a in got]
