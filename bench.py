@@ -96,6 +96,15 @@ class Workload:
             self.phases = []
             self.desc = (f"Llama-3 8B bf16 training state (params bf16 + fp32 master + Adam m,v; "
                          f"{len(self.sizes)} buffers, {sum(self.sizes)} B), Adam step rewrites all")
+        elif name == "c5":
+            # config 5: a 120 GB per-GPU training state (960 tensors of 125 MB),
+            # every tensor rewritten per step, checkpointed concurrently on
+            # every rank through the NVLink peer-GPU cache (next GPU's HBM)
+            self.sizes = [125_000_000] * 960
+            self.params = set()
+            self.phases = []
+            self.desc = ("120 GB per-GPU state (960 x 125 MB), all rewritten per step, cache-cycled pre-copy "
+                         "through the NVLink peer-GPU cache")
         elif name == "c4":
             # LLM inference KV cache: 32 layers x {K, V} paged tensors, 40 GB;
             # 16-token blocks of 8 KV heads x 128 dims bf16 = 32 KiB per block
@@ -126,7 +135,7 @@ class Workload:
                 for h in range(1, len(self.sizes) + 1):
                     out.append((h, blk * self.block, self.block, mix64(mix64(e, s), h)))
             return out
-        if self.name == "c3":  # the optimizer step rewrites every tensor
+        if self.name in ("c3", "c5"):  # the optimizer step rewrites every tensor
             return [(h, 0, n, mix64(e, h)) for h, n in enumerate(self.sizes, start=1)]
         if self.name == "c1":
             nch = self.total // CHUNK
@@ -147,7 +156,7 @@ class Workload:
     def window(self, e: int):
         """Kernels of the next iteration's compute phase (stream 1 and 2
         kernels are serialised on one app stream)."""
-        if self.name in ("c1", "c3", "c4"):
+        if self.name in ("c1", "c3", "c4", "c5"):
             return []
         it = (e + 1) % self.n_iter
         ph = self.phases[2 * it]
@@ -428,7 +437,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         pd.fill_batch([(by_handle[h].dev_ptr + o, n, seed) for h, o, n, seed in wl.epoch_writes(e)])
         pd.check(pd.lib().pos_memset(flush.ptr, e & 0xFF, flush.nbytes, None))  # flush L2
         pd.device_synchronize()
-        window = wl.window(e)
+        window = [] if args.no_window else wl.window(e)
         launches0 = eng.launches
 
         # The window's kernels, argument blocks prepared ahead (as an application
@@ -468,6 +477,11 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         copy.synchronize()
         ckpt.synchronize()
         if direct:
+            if args.trace:
+                import ctypes as C
+                qs = (C.c_uint64 * 14)()
+                pd.lib().pos_debug_ship_queue(eng.ctx, qs)
+                print(json.dumps({"ship_queue": list(qs)}), file=sys.stderr, flush=True)
             _, pre_payload = eng.precopy_direct_result()
             dpay = sum(by_handle[h].size for h in dag_writes)
         # host image = the checkpoint target (captured_); inside the e2e wall
@@ -691,6 +705,10 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
     pd.device_synchronize()
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0))
     eng.register_buffers(bufs)
+    peer = None
+    if args.peer_cache_gb > 0:  # NVLink peer-GPU cache (config 5): the next GPU, or this one on a 1-GPU box
+        peer = (local + 1) % pd.device_count()
+        eng.attach_peer_cache(peer, int(args.peer_cache_gb * 1e9))
     ckpt, copy = pd.Stream(priority=1), pd.Stream()
     flush = pd.DeviceMemory(256 << 20)
     by_handle = {b.handle: b for b in bufs}
@@ -718,7 +736,8 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
         t1 = time.perf_counter()
         r = {"ms": eng.event_elapsed(0, 5), "stw_ms": eng.event_elapsed(3, 4), "wall_ms": (t1 - t0) * 1e3,
              "precopy_bytes": nbytes, "delta_bytes": dbytes, "packs": npk, "entries": seen["entries"],
-             "hash_ms": eng.kernel_ms("hash_waves")}
+             "hash_ms": eng.kernel_ms("hash_waves"),
+             "capture_ms": eng.peer_cache_stats()[0] if peer is not None else None}
         eng.commit_epoch()
         return r
 
@@ -751,6 +770,13 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
                        "parallelism": f"replicas{world}", "host_cpus": numa,
                        "mode": "cache-cycled pre-copy (pos_precopy_stream), app idle at the checkpoint"},
             "stages_ms": {"hash_waves_ms": round(statistics.mean(r["hash_ms"] for r in res), 3)},
+            **({"peer_cache": {"device": peer, "bytes": int(args.peer_cache_gb * 1e9),
+                               "capture_ms": round(statistics.mean(r["capture_ms"] for r in res), 3),
+                               "note": ("capture = every pack in the peer's HBM (the application may resume); "
+                                        "peer == this GPU on a 1-GPU box (D2D slots, not NVLink)"
+                                        if peer == local else
+                                        "capture = every pack in the peer's HBM over NVLink")}}
+               if peer is not None else {}),
             "host_link": {"achieved": round(d2h / (step_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                           "achieved_over": "whole step (D2H-bound)"},
             "e2e": {"value": round(aggregate_value(world, total, wall_ms), 3), "unit": "GB/s",
@@ -785,7 +811,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4"], default="c2")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
@@ -795,13 +821,18 @@ def main():
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
+    ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")
+    ap.add_argument("--peer-cache-gb", type=float, default=0.0,
+                    help="c3: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local, dist = dist_setup()
     wl = Workload(args.workload)
     if args.impl == "reference":
         out = run_reference(args, wl, world, rank)
-    elif wl.name == "c3":
+    elif wl.name in ("c3", "c5"):
+        if wl.name == "c5" and args.peer_cache_gb == 0:
+            args.peer_cache_gb = 16.0
         out = run_gpu_stream(args, wl, world, rank, local, dist)
     else:
         out = run_gpu(args, wl, world, rank, local, dist)

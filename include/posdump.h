@@ -216,6 +216,9 @@ int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void
  * of its index packs in the cache (waits for the scans only). */
 int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_bytes,
                               uint64_t* index_bytes);
+/* Diagnostics of the direct pre-copy's ship queue: {tail, head, done,
+ * exited, watchdog error, current sequence, 8 debug words}. */
+int pos_debug_ship_queue(pos_ctx* ctx, uint64_t* out14);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) stored into the image on
  * `stream` by k_copy_host. */

@@ -92,7 +92,49 @@ struct HashParams {
   // launch (every warp holds one chunk) has the whole list in flight at once.
   uint32_t pf_bytes;
   uint32_t pad2;
+  // Ship queue (direct pre-copy): a dirty, eligible chunk of a buffer without
+  // provenance is pushed the moment its digest is known; k_drain_queue warps
+  // running beside the hash store it into the host image.
+  struct ShipQueue* q;
+  unsigned long long q_seq;
+  int dedup;
+  int pad3;
 };
+
+// Device ship queue: slots are tagged with the pre-copy's sequence number,
+// so no memset is needed between pre-copies; only {tail, head} are reset.
+struct ShipQueue {
+  unsigned long long tail;   // slots claimed by producers
+  unsigned long long head;   // slots claimed by drain warps
+  unsigned long long done;   // sequence number of the last finished producer pass
+  unsigned long long exited; // drain CTAs gone; the last one resets tail/head for the next pre-copy
+  unsigned long long* slots; // (seq << 32) | global chunk
+  unsigned long long error;  // watchdog: seq of a drain that gave up waiting (never 0 for a real seq)
+  unsigned long long dbg[8]; // diagnostics: watchdog slot/tail/done, globaltimer stamps
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Every push of this launch (and of earlier launches) precedes `done`.
+__device__ __forceinline__ void publish_done(ShipQueue* q, unsigned long long seq) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    q->dbg[6] = globaltimer_ns();
+    __threadfence();
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&q->done), "l"(seq) : "memory");
+  }
+}
+
+__device__ __forceinline__ void ship_push(ShipQueue* q, unsigned long long seq, uint64_t g) {
+  const unsigned long long i = atomicAdd(&q->tail, 1ull);
+  if (i == 0) q->dbg[5] = globaltimer_ns();
+  const unsigned long long v = (seq << 32) | g;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(q->slots + i), "l"(v) : "memory");
+}
 
 // Hash kernel geometry.
 constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
@@ -363,7 +405,9 @@ enum : int { kModeHash = 0, kModeCopy = 1, kModeCached = 2 };
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
 template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault, bool kRoll = false>
-__global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
+// <= 120 registers: 16 warps x 3840 leave 4096 registers of the SM for the
+// drain CTAs (k_drain_queue / k_copy_host) to run beside the hash.
+__global__ void __maxnreg__(kThreads >= 512 ? 120 : (kThreads >= 384 ? 168 : 255)) k_hash_chunks(HashParams p) {
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -461,6 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_hash_chunks(HashParams p) {
         const bool dirty = !p.prev_valid || p.digest_prev[g] != crc;
         p.flags[g] = dirty;
         if (dirty && p.bitmap) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
+        // ship now unless O1 may still drop the buffer (provenance: the scan
+        // pushes the O1 losers); DAG-dirty buffers are skipped by the drain
+        if (dirty && p.q && !(p.dedup && (b.flags & kBufHasUpstream))) ship_push(p.q, p.q_seq, g);
       }
     }
   }
@@ -568,8 +615,12 @@ __global__ void k_note_upstream(DevBuf* bufs, uint32_t i, const uint32_t* digest
 // contiguous range of rounds; two block barriers join the warp totals.
 // Bitmap word k is written by the launch holding its last existing chunk
 // (earlier launches' flags are final by then), so waves need no memset.
-constexpr int kScanThreads = 1024;
+// 512 threads x 64 registers: half an SM, so the scan can start on an SM
+// that also hosts ship-queue drain CTAs (a full-register-file CTA could not,
+// and waited for the drain -- measured).
+constexpr int kScanThreads = 512;
 constexpr int kScanWarps = kScanThreads / 32;
+constexpr uint32_t kCandSlots = 1024;  // O1 candidate list (the rest is walked)
 constexpr int kScanKeep = 4;  // rounds per warp kept in registers between the passes
 
 __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
@@ -584,15 +635,18 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     uint32_t vb0, uint32_t vb1, const uint32_t* tcs, const uint32_t* xfold, int dedup, uint32_t* crc_out,
     uint8_t* verdict_out, uint64_t fixed_base /* ~0 = at *cursor; cursor (if set) is advanced */,
     int direct /* items target DevBuf::image; the pack keeps header + entries only */,
-    uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total) {
+    uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total,
+    ShipQueue* q /* direct + queue: push eligible chunks of provenance buffers; publish done */,
+    unsigned long long q_seq, int last_wave) {
   __shared__ uint32_t tz[1024];  // Z^chunk_size
   __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_tot[3];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (q && t == 0) q->dbg[7] = globaltimer_ns();
   const uint32_t lt = (1u << lane) - 1u;
   if (vb1 > vb0) {
     // Candidates (upstream provenance) into a smem list in one parallel pass,
     // then one warp per candidate: no warp walks buffers it has nothing to do for.
-    __shared__ uint32_t s_cand[kScanThreads];
+    __shared__ uint32_t s_cand[kCandSlots];
     __shared__ uint32_t s_ncand;
     if (t == 0) s_ncand = 0;
     for (int q = t; q < 1024; q += kScanThreads) tz[q] = __ldg(tcs + q);
@@ -601,14 +655,14 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       const bool cand = dedup && (bufs[i].flags & kBufHasUpstream);
       if (cand) {
         const uint32_t slot = atomicAdd(&s_ncand, 1u);
-        if (slot < kScanThreads) s_cand[slot] = i;
+        if (slot < kCandSlots) s_cand[slot] = i;
         else verdict_out[i] = 2;  // list full: folded by the walk below
       } else {
         verdict_out[i] = 0;  // no provenance -> no verdict (cr.hpp:390)
       }
     }
     __syncthreads();
-    const uint32_t nc = s_ncand < kScanThreads ? s_ncand : kScanThreads;
+    const uint32_t nc = s_ncand < kCandSlots ? s_ncand : kCandSlots;
     for (uint32_t q = warp; q < nc; q += kScanWarps) {
       const uint32_t i = s_cand[q];
       const DevBuf b = bufs[i];
@@ -618,7 +672,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
         verdict_out[i] = crc == b.upstream_crc && (b.flags & kBufHostUntouched) && !dag_dirty[i];
       }
     }
-    if (s_ncand > kScanThreads) {  // more candidates than list slots: walk the rest
+    if (s_ncand > kCandSlots) {  // more candidates than list slots: walk the rest
       __syncthreads();
       for (uint32_t i = vb0 + warp; i < vb1; i += kScanWarps) {
         if (verdict_out[i] != 2) continue;
@@ -701,7 +755,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   }
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the warp totals
-    uint64_t n = s_wn[lane], b = s_wb[lane];
+    uint64_t n = lane < kScanWarps ? s_wn[lane] : 0, b = lane < kScanWarps ? s_wb[lane] : 0;
     uint64_t in_n = n, in_b = b;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -711,8 +765,10 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
         in_b += ab;
       }
     }
-    s_wn[lane] = in_n - n;
-    s_wb[lane] = in_b - b;
+    if (lane < kScanWarps) {
+      s_wn[lane] = in_n - n;
+      s_wb[lane] = in_b - b;
+    }
     const uint64_t N = __shfl_sync(0xffffffffu, in_n, 31), B = __shfl_sync(0xffffffffu, in_b, 31);
     if (lane == 0) {
       const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
@@ -737,6 +793,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
         __threadfence_system();
         result_host[5] = seq;
         __threadfence_system();
+        if (q) q->dbg[3] = globaltimer_ns();  // diagnostics: after the system fences
       }
       s_tot[0] = N;
       s_tot[1] = B;
@@ -745,7 +802,10 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   }
   __syncthreads();
   const uint64_t N = s_tot[0], B = s_tot[1];
-  if (s_tot[2]) return;
+  if (s_tot[2]) {  // overflow: nothing more to ship from here; let the drain finish
+    if (q && last_wave) publish_done(q, q_seq);
+    return;
+  }
   const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
   if (t == 0) {
     uint32_t* h = reinterpret_cast<uint32_t*>(pack);
@@ -781,12 +841,16 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)my_off,
                           (uint32_t)(my_off >> 32));
       ent[1] = make_uint4(L.cm.y, (uint32_t)L.len, digests[g], 0u);
-      CopyItem ci;
-      ci.src = b.ptr + (uint64_t)L.cm.y * chunk_size;
-      ci.dst = direct ? b.image + (uint64_t)L.cm.y * chunk_size : (uint64_t)pack + payload_off + my_off;
-      ci.len = L.len;
-      ci.padded = padded(L.len);
-      items[my_e] = ci;
+      if (q) {  // the hash shipped every other eligible chunk already
+        if (dedup && (b.flags & kBufHasUpstream)) ship_push(q, q_seq, g);
+      } else {
+        CopyItem ci;
+        ci.src = b.ptr + (uint64_t)L.cm.y * chunk_size;
+        ci.dst = direct ? b.image + (uint64_t)L.cm.y * chunk_size : (uint64_t)pack + payload_off + my_off;
+        ci.len = L.len;
+        ci.padded = padded(L.len);
+        items[my_e] = ci;
+      }
     }
     e += __popc(L.mask);
     off += __shfl_sync(0xffffffffu, incl, 31);
@@ -795,6 +859,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   for (int j = 0; j < kScanKeep; ++j)
     if (r0 + j < r1) emit(r0 + j, keep[j]);
   for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k, false));
+  if (q && last_wave) publish_done(q, q_seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -975,6 +1040,94 @@ __global__ void __launch_bounds__(kHostCopyThreads, 16) k_copy_host(const CopyIt
     for (uint64_t q = body / kStep * kStep + lane * 16; q + 16 <= body; q += 32 * 16)
       *reinterpret_cast<uint4*>(d + q) = ldg_stream(s + q);
     for (uint64_t q = body + lane; q < c.padded; q += 32) d[q] = q < c.len ? s[q] : 0;
+  }
+}
+
+// Persistent drain of the ship queue into the host image: launched before
+// the hash on the drain stream, co-resident with it (same footprint as
+// k_copy_host); a warp claims a slot, waits for its producer, stores the
+// chunk at image + chunk * chunk_size, and leaves once the last producer pass
+// (the final wave's scan) has published `done` and every claimed slot is past
+// the final tail.
+constexpr int kDrainThreads = 64;  // 2 warps x 32 registers: two CTAs still fit beside a hash CTA
+constexpr int kDrainCtas = 32;
+
+__global__ void __launch_bounds__(kDrainThreads, 32) k_drain_queue(ShipQueue* q, unsigned long long seq,
+                                                                   const DevBuf* bufs, const uint2* chunk_map,
+                                                                   uint64_t chunk_size, const uint8_t* dag_dirty,
+                                                                   unsigned long long watchdog_ns) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) q->dbg[4] = globaltimer_ns();
+  for (;;) {
+    unsigned long long i = 0;
+    if (lane == 0) i = atomicAdd(&q->head, 1ull);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    unsigned long long v = 0;
+    int state = 0;  // 1 got the slot, 2 finished
+    if (lane == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      for (uint32_t ns = 32;;) {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(q->slots + i) : "memory");
+        if ((v >> 32) == seq) {
+          state = 1;
+          break;
+        }
+        unsigned long long d, t;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(d) : "l"(&q->done) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(t) : "l"(&q->tail) : "memory");
+        if (d == seq && i >= t) {
+          state = 2;
+          break;
+        }
+        if (globaltimer_ns() - t0 > watchdog_ns) {  // a producer that never came: do not hang the GPU
+          q->dbg[0] = i;
+          q->dbg[1] = t;
+          q->dbg[2] = d;
+          q->dbg[3] = globaltimer_ns();
+          atomicExch(&q->error, seq);
+          state = 2;
+          break;
+        }
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : ns;
+      }
+    }
+    state = __shfl_sync(0xffffffffu, state, 0);
+    if (state == 2) break;
+    const uint64_t g = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)v, 0);
+    const uint2 cm = chunk_map[g];
+    if (dag_dirty && dag_dirty[cm.x]) continue;  // left to the STW delta (cr.hpp:487)
+    const DevBuf& b = bufs[cm.x];
+    const uint64_t start = (uint64_t)cm.y * chunk_size;
+    const uint64_t len = cm.y + 1 == b.nchunks ? b.size - start : chunk_size;
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(b.ptr + start);
+    uint8_t* d = reinterpret_cast<uint8_t*>(b.image + start);
+    const uint64_t body = (((uint64_t)s | (uint64_t)d) & 15) == 0 ? len & ~15ull : 0;
+    constexpr uint32_t kStep = 32 * 16 * kHostUnroll;
+    const uint4* sp = reinterpret_cast<const uint4*>(s) + lane;
+    uint4* dp = reinterpret_cast<uint4*>(d) + lane;
+    const uint4* const se = reinterpret_cast<const uint4*>(s + body / kStep * kStep);
+    for (; sp < se; sp += 32 * kHostUnroll, dp += 32 * kHostUnroll) {
+      uint4 w[kHostUnroll];
+#pragma unroll
+      for (int u = 0; u < kHostUnroll; ++u) w[u] = ldg_stream(sp + u * 32);
+#pragma unroll
+      for (int u = 0; u < kHostUnroll; ++u) dp[u * 32] = w[u];
+    }
+    for (uint64_t o = body / kStep * kStep + lane * 16; o + 16 <= body; o += 32 * 16)
+      *reinterpret_cast<uint4*>(d + o) = ldg_stream(s + o);
+    for (uint64_t o = body + lane; o < len; o += 32) d[o] = s[o];
+  }
+  // the last warp out resets the counters for the next pre-copy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&q->exited, 1ull) == (unsigned long long)gridDim.x - 1) {
+      q->tail = 0;
+      q->head = 0;
+      q->exited = 0;
+      __threadfence();
+    }
   }
 }
 

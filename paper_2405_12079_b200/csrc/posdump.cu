@@ -172,6 +172,28 @@ struct CrcTables {
     set_hash_smem<kModeCached>();
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
+    // Load every kernel now: under lazy module loading (the CUDA 12 default)
+    // a kernel's first launch loads it, and that load waits for the device --
+    // behind a persistent k_drain_queue that waits for this very kernel
+    // (measured: the first direct pre-copy of a process stalled until the
+    // drain's watchdog fired).
+    // The drain CTAs run beside the hash kernel's 193 KiB CTAs: an SM's
+    // L1/shared split can only change while it is idle, so the drains (and
+    // the scan) ask for the hash kernel's maximal-shared carveout -- otherwise
+    // every SM holding a drain CTA is closed to the hash (measured: the hash
+    // ran in two rounds, 2-4x slower, while the ship-queue drain was live).
+    for (const void* f : {(const void*)k_drain_queue, (const void*)k_copy_host, (const void*)k_pack_scan})
+      ck(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+         "carveout");
+    cudaFuncAttributes fa;
+    ck(cudaFuncGetAttributes(&fa, k_pack_scan), "load k_pack_scan");
+    ck(cudaFuncGetAttributes(&fa, k_drain_queue), "load k_drain_queue");
+    ck(cudaFuncGetAttributes(&fa, k_copy_host), "load k_copy_host");
+    ck(cudaFuncGetAttributes(&fa, k_copy_simt), "load k_copy_simt");
+    ck(cudaFuncGetAttributes(&fa, k_pack_items), "load k_pack_items");
+    ck(cudaFuncGetAttributes(&fa, k_buffer_crc), "load k_buffer_crc");
+    ck(cudaFuncGetAttributes(&fa, k_note_upstream), "load k_note_upstream");
+    ck(cudaFuncGetAttributes(&fa, k_fill), "load k_fill");
   }
 };
 
@@ -291,6 +313,11 @@ struct pos_ctx {
   uint64_t drain_n = 0;              // items of the last delta copy (pos_delta_drain)
   bool drain_pending = false;
   bool direct_pending = false;       // a pos_precopy_direct awaits pos_precopy_direct_result
+  // ship queue (hash -> k_drain_queue) of the direct pre-copy
+  DevArray<ShipQueue> d_q;
+  DevArray<unsigned long long> d_qslots;
+  unsigned long long q_seq = 0;
+  cudaEvent_t ev_drained = nullptr;  // the last k_drain_queue exited (queue reset)
   uint32_t direct_waves = 0;
   // O3 cache
   DevArray<uint8_t> cache;
@@ -522,6 +549,9 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_items.release();
   c->d_delta_items.release();
   c->d_drain_items.release();
+  c->d_q.release();
+  c->d_qslots.release();
+  if (c->ev_drained) cudaEventDestroy(c->ev_drained);
   for (void* h : c->image_pinned) cudaHostUnregister(h);
   c->d_scan.release();
   c->d_work.release();
@@ -925,7 +955,8 @@ int pos_clear_dirty(pos_ctx* c) {
 // event scanned[slot] for pack_result().
 static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
                         uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0, uint64_t fixed_base = ~0ull,
-                        cudaStream_t direct_stream = nullptr, bool direct = false, bool chain_start = false) {
+                        cudaStream_t direct_stream = nullptr, bool direct = false, bool chain_start = false,
+                        ShipQueue* q = nullptr, unsigned long long q_seq = 0, bool last_wave = false) {
   upload_dag_flags(c, s);
   // Packs chain at the device-side cursor; the first of a chain starts at 0
   // (no memset), a fixed-region pack (cache cycling) leaves the cursor alone.
@@ -939,12 +970,16 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
       c->cache_cap - c->staging_used, cursor, c->d_items.p + lo, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
       c->d_tcs.p, c->d_xfold.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base, direct ? 1 : 0,
-      c->d_bitmap.p, c->n_chunks);
+      c->d_bitmap.p, c->n_chunks, q, q_seq, last_wave ? 1 : 0);
   c->slot_seq[slot] = c->scan_seq;
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
   ++c->launches;
   ck(cudaEventRecord(c->scanned[slot], s), "event");
+  if (direct && q) {  // the hash and this scan pushed every chunk to the running drain
+    c->pack_pending = true;
+    return;
+  }
   if (direct) {  // chunks go straight to the host image from the drain stream
     ck(cudaStreamWaitEvent(direct_stream, c->scanned[slot], 0), "wait scan");
     if (slot == 0) c->timer_begin(kTimD2H, direct_stream);
@@ -994,9 +1029,13 @@ static uint64_t pack_size(pos_ctx* c) {
   return r.total;
 }
 
-static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uint32_t wave) {
-  if (hi <= lo) return;  // the caller zeroes the bitmap (boundary words are shared)
+static void hash_range(pos_ctx* c, uint64_t lo, uint64_t hi, cudaStream_t s, uint32_t wave,
+                       ShipQueue* q = nullptr, unsigned long long q_seq = 0) {
+  if (hi <= lo) return;
   HashParams p{};
+  p.q = q;
+  p.q_seq = q_seq;
+  p.dedup = c->cfg.dedup;
   p.bufs = c->d_bufs.p;
   p.chunk_map = c->d_chunk_map.p;
   p.n_items = hi - lo;
@@ -1425,6 +1464,29 @@ int pos_register_image(pos_ctx* c, uint8_t* const* hosts, const uint64_t* sizes,
   });
 }
 
+// Longest a drain warp waits for one producer before giving up (and
+// reporting POS_E_CUDA from pos_precopy_direct_result instead of hanging).
+static unsigned long long watchdog_ns() {
+  static const unsigned long long v = [] {
+    const char* e = std::getenv("POSDUMP_WATCHDOG_MS");
+    unsigned long long ms = e ? std::strtoull(e, nullptr, 10) : 10000;
+    return (ms ? ms : 10000) * 1000000ull;
+  }();
+  return v;
+}
+
+int pos_debug_ship_queue(pos_ctx* c, uint64_t* out14) {
+  return guarded([&] {
+    if (!c || !out14) fail(POS_E_INVALID_ARGUMENT, "null argument");
+    if (!c->d_q.p) fail(POS_E_BAD_STATE, "no ship queue");
+    ShipQueue h{};
+    ck(cudaMemcpy(&h, c->d_q.p, sizeof h, cudaMemcpyDeviceToHost), "queue");
+    const uint64_t v[6] = {h.tail, h.head, h.done, h.exited, h.error, c->q_seq};
+    std::memcpy(out14, v, sizeof v);
+    std::memcpy(out14 + 6, h.dbg, sizeof h.dbg);
+  });
+}
+
 int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                        void* drain_stream) {
   return guarded([&] {
@@ -1453,14 +1515,52 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
       reserve += round_up(kPackHeader + kPackEntry * (chunk_of(bb[w + 1]) - chunk_of(bb[w])), kPackAlign);
     if (reserve > c->cache_cap - c->staging_used) fail(POS_E_STAGING_EXHAUSTED, "index packs exceed the cache");
     upload_dag_flags(c, s, ds);  // on the drain stream, under the first hash
+    static const bool use_queue = [] {
+      const char* e = std::getenv("POSDUMP_DIRECT_QUEUE");  // 0: per-wave drains after each scan
+      return !(e && e[0] == '0');
+    }();
+    ShipQueue* q = nullptr;
+    if (use_queue) {
+      // Ship queue: chunks leave while the rest is still being hashed.
+      const uint64_t cap = c->n_chunks + 2 * kDrainCtas * (kDrainThreads / 32) + 64;
+      if (!c->d_q.p || c->d_qslots.n < cap) {
+        ck(cudaStreamSynchronize(ds), "sync");
+        c->d_qslots.ensure(cap);
+        ck(cudaMemset(c->d_qslots.p, 0, cap * sizeof(unsigned long long)), "memset slots");
+        c->d_q.ensure(1);
+        ShipQueue hq{};
+        hq.slots = c->d_qslots.p;
+        ck(cudaMemcpy(c->d_q.p, &hq, sizeof hq, cudaMemcpyHostToDevice), "queue");
+        c->q_seq = 0;
+        if (!c->ev_drained) ck(cudaEventCreateWithFlags(&c->ev_drained, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(c->ev_drained, ds), "event");
+      }
+      q = c->d_q.p;
+      ++c->q_seq;
+      ck(cudaStreamWaitEvent(s, c->ev_drained, 0), "wait queue reset");  // previous drain gone
+      static const bool after_hash = std::getenv("POSDUMP_DRAIN_AFTER_HASH") != nullptr;  // diagnostics
+      if (after_hash) {
+        hash_range(c, 0, 0, s, 0);
+        ck(cudaEventRecord(c->ev_drained, s), "event");
+        ck(cudaStreamWaitEvent(ds, c->ev_drained, 0), "wait");
+      }
+      c->timer_begin(kTimD2H, ds);
+      k_drain_queue<<<kDrainCtas, kDrainThreads, 0, ds>>>(q, c->q_seq, c->d_bufs.p, c->d_chunk_map.p,
+                                                         c->cfg.chunk_size,
+                                                         exclude_dag_dirty ? c->d_dag_dirty.p : nullptr,
+                                                         watchdog_ns());
+      check_launch("k_drain_queue");
+      ++c->launches;
+    }
     c->timer_begin(kTimHash, s);
     for (uint32_t w = 0; w < W; ++w) {
-      hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
+      hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w, q, c->q_seq);
       launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1], ~0ull,
-                  ds, true, w == 0);
+                  ds, true, w == 0, q, c->q_seq, w + 1 == W);
     }
     c->timer_end(kTimHash, s);
     c->timer_end(kTimD2H, ds);
+    if (q) ck(cudaEventRecord(c->ev_drained, ds), "event");
     c->waves_last = W;
     c->direct_waves = W;
     c->direct_pending = true;
@@ -1481,6 +1581,14 @@ int pos_precopy_direct_result(pos_ctx* c, uint64_t* chunks, uint64_t* payload_by
       end = r.base + round_up(r.total, kPackAlign);
     }
     c->direct_pending = false;  // the index packs stay in [0, end) of the cache
+    if (c->d_q.p) {  // watchdog of the ship-queue drain
+      unsigned long long err = 0;
+      ck(cudaMemcpy(&err, &c->d_q.p->error, sizeof err, cudaMemcpyDeviceToHost), "queue error");
+      if (err) {
+        ck(cudaMemset(&c->d_q.p->error, 0, sizeof err), "queue error reset");
+        fail(POS_E_CUDA, "ship-queue drain watchdog fired (pre-copy " + std::to_string(err) + ")");
+      }
+    }
     if (chunks) *chunks = n;
     if (payload_bytes) *payload_bytes = pay;
     if (index_bytes) *index_bytes = end;

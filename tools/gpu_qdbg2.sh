@@ -1,0 +1,7 @@
+export POSDUMP_WATCHDOG_MS=2000
+for spec in ":: --no-window" ":: --workload c1" "POSDUMP_DIRECT_QUEUE=0 ::" "POSDUMP_DRAIN_AFTER_HASH=1 ::" ":: --mode pack"; do
+  env_s="${spec%%::*}"; args="${spec#*::}"
+  echo "== $spec"
+  env $env_s timeout 60 python bench.py --steps 3 --warmup 3 --trace --no-cpu-baseline $args > gpurun_out/q.out 2> gpurun_out/q.err; echo rc=$?
+  grep -o '"value": [0-9.]*' gpurun_out/q.out; grep "ship_queue\|Error" gpurun_out/q.err | head -4
+done
