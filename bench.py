@@ -815,7 +815,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
-    ap.add_argument("--waves", type=int, default=1, help="pre-copy pipeline waves (1 = no overlap)")
+    ap.add_argument("--waves", type=int, default=0,
+                    help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c4 8)")
     ap.add_argument("--mode", choices=["pack", "direct"], default="direct",
                     help="pack: POSD pack D2H by the copy engine + host apply; direct: SM stores into the pinned image")
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
@@ -826,6 +827,8 @@ def main():
                     help="c3: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.waves <= 0:
+        args.waves = {"c1": 4, "c4": 8}.get(args.workload, 1)
     world, rank, local, dist = dist_setup()
     wl = Workload(args.workload)
     if args.impl == "reference":

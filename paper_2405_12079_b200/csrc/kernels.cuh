@@ -637,9 +637,13 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     int direct /* items target DevBuf::image; the pack keeps header + entries only */,
     uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total,
     ShipQueue* q /* direct + queue: push eligible chunks of provenance buffers; publish done */,
-    unsigned long long q_seq, int last_wave) {
+    unsigned long long q_seq, int last_wave,
+    // direct + copy engine: maximal runs of eligible chunks (within a buffer
+    // and a 32-chunk bitmap word) as SoA {src, dst, bytes} in mapped pinned
+    // memory -- the argument arrays of cudaMemcpyBatchAsync
+    uint64_t* run_src, uint64_t* run_dst, uint64_t* run_len) {
   __shared__ uint32_t tz[1024];  // Z^chunk_size
-  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_tot[3];
+  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_wr[kScanWarps], s_tot[4];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (q && t == 0) q->dbg[7] = globaltimer_ns();
   const uint32_t lt = (1u << lane) - 1u;
@@ -696,13 +700,14 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
 
   struct Lane {
     uint2 cm;
-    uint32_t mask;  // ballot of eligible lanes
-    uint64_t len;   // this lane's chunk length (0 if not eligible)
+    uint32_t mask;   // ballot of eligible lanes
+    uint32_t start;  // eligible lanes that begin a run (predecessor not eligible or another buffer)
+    uint64_t len;    // this lane's chunk length (0 if not eligible)
   };
   auto look = [&](uint64_t k, bool with_bitmap) -> Lane {
     const uint64_t g = 32 * k + lane;
     const bool in = g >= chunk_lo && g < chunk_hi;
-    Lane L{make_uint2(0, 0), 0u, 0};
+    Lane L{make_uint2(0, 0), 0u, 0u, 0};
     uint8_t f = 0;
     if (in) {
       L.cm = chunk_map[g];
@@ -717,6 +722,9 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       }
     }
     L.mask = __ballot_sync(0xffffffffu, el);
+    const uint32_t prev_buf = __shfl_up_sync(0xffffffffu, L.cm.x, 1);
+    const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && prev_buf == L.cm.x);
+    L.start = L.mask & ~(L.mask & (L.mask << 1) & same);
     if (with_bitmap && bitmap) {
       const uint64_t last = (32 * k + 31 < n_total ? 32 * k + 31 : n_total - 1);
       if (last >= chunk_lo && last < chunk_hi) {  // this launch owns word k
@@ -735,9 +743,10 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   };
   // Pass 1: per-warp totals (entries, padded payload bytes).
   Lane keep[kScanKeep];
-  uint64_t wn = 0, wb = 0;
+  uint64_t wn = 0, wb = 0, wr = 0;
   auto count = [&](const Lane& L) {
     wn += __popc(L.mask);
+    wr += __popc(L.start);
     wb += warp_sum(L.len ? (L.len + 15) & ~15ull : 0);
   };
 #pragma unroll
@@ -752,24 +761,30 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   if (lane == 0) {
     s_wn[warp] = wn;
     s_wb[warp] = wb;
+    s_wr[warp] = wr;
   }
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the warp totals
     uint64_t n = lane < kScanWarps ? s_wn[lane] : 0, b = lane < kScanWarps ? s_wb[lane] : 0;
-    uint64_t in_n = n, in_b = b;
+    uint64_t r = lane < kScanWarps ? s_wr[lane] : 0;
+    uint64_t in_n = n, in_b = b, in_r = r;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint64_t an = __shfl_up_sync(0xffffffffu, in_n, o), ab = __shfl_up_sync(0xffffffffu, in_b, o);
+      const uint64_t ar = __shfl_up_sync(0xffffffffu, in_r, o);
       if (lane >= o) {
         in_n += an;
         in_b += ab;
+        in_r += ar;
       }
     }
     if (lane < kScanWarps) {
       s_wn[lane] = in_n - n;
       s_wb[lane] = in_b - b;
+      s_wr[lane] = in_r - r;
     }
     const uint64_t N = __shfl_sync(0xffffffffu, in_n, 31), B = __shfl_sync(0xffffffffu, in_b, 31);
+    const uint64_t R = __shfl_sync(0xffffffffu, in_r, 31);
     if (lane == 0) {
       const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
       // Direct: entries keep the offsets a payload would have, but nothing is
@@ -782,14 +797,16 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       result[3] = overflow ? 0 : N;  // items for the copy kernel
       result[4] = base;
       result[6] = B;
+      result[7] = R;
       if (!overflow && cursor) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
-      if (result_host) {
+      if (result_host && (!run_src || overflow)) {  // copy-engine runs: published after pass 2
         result_host[0] = N;
         result_host[1] = total;
         result_host[2] = overflow;
         result_host[3] = overflow ? 0 : N;
         result_host[4] = base;
         result_host[6] = B;
+        result_host[7] = R;
         __threadfence_system();
         result_host[5] = seq;
         __threadfence_system();
@@ -798,6 +815,7 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       s_tot[0] = N;
       s_tot[1] = B;
       s_tot[2] = overflow;
+      s_tot[3] = R;
     }
   }
   __syncthreads();
@@ -823,8 +841,23 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   if (!direct)
     for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
   // Pass 2: entries + copy items at the warp's base.
-  uint64_t e = s_wn[warp], off = s_wb[warp];
+  uint64_t e = s_wn[warp], off = s_wb[warp], rb = s_wr[warp];
   auto emit = [&](uint64_t k, const Lane& L) {
+    if (run_src) {  // runs: a start lane covers its run's chunks up to the first gap in the word
+      const uint32_t cont = L.mask & ~L.start;
+      const uint32_t rest = lane < 31 ? cont >> (lane + 1) : 0u;
+      const int nrun = __ffs(~rest);  // chunks in the run (>= 1)
+      const int last = lane + nrun - 1 < 31 ? lane + nrun - 1 : 31;
+      const uint64_t last_len = __shfl_sync(0xffffffffu, L.len, last);
+      if (L.start >> lane & 1) {
+        const DevBuf& b = bufs[L.cm.x];
+        const uint64_t ri = rb + __popc(L.start & lt);
+        run_src[ri] = b.ptr + (uint64_t)L.cm.y * chunk_size;
+        run_dst[ri] = b.image + (uint64_t)L.cm.y * chunk_size;
+        run_len[ri] = (uint64_t)(nrun - 1) * chunk_size + last_len;
+      }
+      rb += __popc(L.start);
+    }
     const uint64_t pl = L.len ? (L.len + 15) & ~15ull : 0;
     uint64_t incl = pl;  // inclusive prefix of the round's padded lengths
 #pragma unroll
@@ -860,6 +893,22 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     if (r0 + j < r1) emit(r0 + j, keep[j]);
   for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k, false));
   if (q && last_wave) publish_done(q, q_seq);
+  if (run_src && result_host) {  // the host reads the run lists once it sees seq
+    __threadfence_system();
+    __syncthreads();
+    if (t == 0) {
+      result_host[0] = N;
+      result_host[1] = direct ? kPackHeader + kPackEntry * N : payload_off + B;
+      result_host[2] = 0;
+      result_host[3] = N;
+      result_host[4] = base;
+      result_host[6] = B;
+      result_host[7] = s_tot[3];
+      __threadfence_system();
+      result_host[5] = seq;
+      __threadfence_system();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

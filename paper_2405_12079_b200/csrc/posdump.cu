@@ -318,6 +318,12 @@ struct pos_ctx {
   DevArray<unsigned long long> d_qslots;
   unsigned long long q_seq = 0;
   cudaEvent_t ev_drained = nullptr;  // the last k_drain_queue exited (queue reset)
+  // copy-engine drain (default direct mode): run lists written by the scan
+  // into mapped pinned memory = the arguments of cudaMemcpyBatchAsync
+  PinnedArray<uint64_t> h_run;   // [3][n_chunks]: src, dst, bytes
+  PinnedArray<uint64_t> h_drun;  // STW delta drain runs, same layout
+  uint64_t drun_n = 0, drun_cap = 0;
+  uint32_t direct_lo[16] = {};  // first chunk of each direct wave (kMaxWaves)
   uint32_t direct_waves = 0;
   // O3 cache
   DevArray<uint8_t> cache;
@@ -376,6 +382,18 @@ void check_launch(const char* what) {
 }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// Host leg of the direct pre-copy: 0 copy-engine runs, 1 SM ship queue, 2 SM after each scan.
+int direct_drain_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("POSDUMP_DIRECT_DRAIN");
+    if (e && !std::strcmp(e, "queue")) return 1;
+    if (e && !std::strcmp(e, "sm")) return 2;
+    return 0;
+  }();
+  return m;
+}
+
 
 // Per-buffer DAG-dirty flags (dirty_set_) to the device.  With a side
 // stream the copy runs there (concurrently with the first hash) and `s`
@@ -550,6 +568,8 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_delta_items.release();
   c->d_drain_items.release();
   c->d_q.release();
+  c->h_run.release();
+  c->h_drun.release();
   c->d_qslots.release();
   if (c->ev_drained) cudaEventDestroy(c->ev_drained);
   for (void* h : c->image_pinned) cudaHostUnregister(h);
@@ -956,7 +976,8 @@ int pos_clear_dirty(pos_ctx* c) {
 static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
                         uint32_t slot, uint32_t vb0 = 0, uint32_t vb1 = 0, uint64_t fixed_base = ~0ull,
                         cudaStream_t direct_stream = nullptr, bool direct = false, bool chain_start = false,
-                        ShipQueue* q = nullptr, unsigned long long q_seq = 0, bool last_wave = false) {
+                        ShipQueue* q = nullptr, unsigned long long q_seq = 0, bool last_wave = false,
+                        bool ce_runs = false) {
   upload_dag_flags(c, s);
   // Packs chain at the device-side cursor; the first of a chain starts at 0
   // (no memset), a fixed-region pack (cache cycling) leaves the cursor alone.
@@ -970,13 +991,15 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
       c->d_dag_dirty.p, exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, 0u, c->cache.p,
       c->cache_cap - c->staging_used, cursor, c->d_items.p + lo, res, c->h_scan.p + 8 * slot, ++c->scan_seq, vb0, vb1,
       c->d_tcs.p, c->d_xfold.p, c->cfg.dedup, c->d_buf_crc.p, c->d_verdict.p, fixed_base, direct ? 1 : 0,
-      c->d_bitmap.p, c->n_chunks, q, q_seq, last_wave ? 1 : 0);
+      c->d_bitmap.p, c->n_chunks, q, q_seq, last_wave ? 1 : 0,
+      ce_runs ? c->h_run.p + lo : nullptr, ce_runs ? c->h_run.p + c->n_chunks + lo : nullptr,
+      ce_runs ? c->h_run.p + 2 * c->n_chunks + lo : nullptr);
   c->slot_seq[slot] = c->scan_seq;
   check_launch("k_pack_scan");
   c->timer_end(kTimScan, s);
   ++c->launches;
   ck(cudaEventRecord(c->scanned[slot], s), "event");
-  if (direct && q) {  // the hash and this scan pushed every chunk to the running drain
+  if (direct && (q || ce_runs)) {  // shipped by the running drain / by the copy engine (host submits the runs)
     c->pack_pending = true;
     return;
   }
@@ -1515,12 +1538,53 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
       reserve += round_up(kPackHeader + kPackEntry * (chunk_of(bb[w + 1]) - chunk_of(bb[w])), kPackAlign);
     if (reserve > c->cache_cap - c->staging_used) fail(POS_E_STAGING_EXHAUSTED, "index packs exceed the cache");
     upload_dag_flags(c, s, ds);  // on the drain stream, under the first hash
-    static const bool use_queue = [] {
-      const char* e = std::getenv("POSDUMP_DIRECT_QUEUE");  // 0: per-wave drains after each scan
-      return !(e && e[0] == '0');
-    }();
+    // Host leg of the direct mode (POSDUMP_DIRECT_DRAIN):
+    //   ce    (default) the copy engine moves runs of shipped chunks straight
+    //         into the image (cudaMemcpyBatchAsync over the scan's run lists);
+    //   queue SM warps drain a ship queue fed by the hash (starts earliest, but
+    //         SM stores over PCIe slow concurrent HBM kernels ~4x: measured);
+    //   sm    k_copy_host after each wave's scan.
+    const int drain_mode = direct_drain_mode();
+    if (drain_mode == 0) {
+      c->h_run.ensure(3 * std::max<uint64_t>(c->n_chunks, 1));
+      c->timer_begin(kTimHash, s);
+      for (uint32_t w = 0; w < W; ++w) {
+        hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
+        launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1], ~0ull,
+                    ds, true, w == 0, nullptr, 0, false, true);
+        c->direct_lo[w] = (uint32_t)chunk_of(bb[w]);
+      }
+      c->timer_end(kTimHash, s);
+      // each wave's runs go to the copy engine the moment its scan lands
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.srcLocHint.type = cudaMemLocationTypeDevice;
+      attr.srcLocHint.id = c->cfg.device;
+      attr.dstLocHint.type = cudaMemLocationTypeHost;
+      for (uint32_t w = 0; w < W; ++w) {
+        pack_result(c, w);
+        const uint64_t nr = c->h_scan.p[8 * w + 7];
+        const uint64_t lo = c->direct_lo[w];
+        if (w == 0) c->timer_begin(kTimD2H, ds);
+        if (nr) {
+          size_t zero = 0, fail_idx = 0;
+          ck(cudaMemcpyBatchAsync(reinterpret_cast<void**>(c->h_run.p + c->n_chunks + lo),
+                                  reinterpret_cast<void**>(c->h_run.p + lo),
+                                  reinterpret_cast<size_t*>(c->h_run.p + 2 * c->n_chunks + lo), nr, &attr, &zero,
+                                  1, &fail_idx, ds),
+             "cudaMemcpyBatchAsync(direct runs)");
+        }
+      }
+      c->timer_end(kTimD2H, ds);
+      c->waves_last = W;
+      c->direct_waves = W;
+      c->direct_pending = true;
+      c->pack_pending = false;
+      c->precopy_bytes = reserve;
+      return;
+    }
     ShipQueue* q = nullptr;
-    if (use_queue) {
+    if (drain_mode == 1) {
       // Ship queue: chunks leave while the rest is still being hashed.
       const uint64_t cap = c->n_chunks + 2 * kDrainCtas * (kDrainThreads / 32) + 64;
       if (!c->d_q.p || c->d_qslots.n < cap) {
@@ -1601,7 +1665,22 @@ int pos_delta_drain(pos_ctx* c, void* stream) {
     if (!c->drain_pending) fail(POS_E_BAD_STATE, "no STW delta to drain (pos_delta_copy with an image)");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     c->drain_pending = false;
-    if (c->drain_n) launch_copy_host(c, c->d_drain_items.p, nullptr, c->drain_n, S(stream));
+    if (!c->drain_n) return;
+    if (direct_drain_mode() == 0 && c->drun_n) {
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.srcLocHint.type = cudaMemLocationTypeDevice;
+      attr.srcLocHint.id = c->cfg.device;
+      attr.dstLocHint.type = cudaMemLocationTypeHost;
+      size_t zero = 0, fail_idx = 0;
+      const uint64_t r = c->drun_n;
+      ck(cudaMemcpyBatchAsync(reinterpret_cast<void**>(c->h_drun.p + r), reinterpret_cast<void**>(c->h_drun.p),
+                              reinterpret_cast<size_t*>(c->h_drun.p + 2 * r), r, &attr, &zero, 1, &fail_idx,
+                              S(stream)),
+         "cudaMemcpyBatchAsync(delta runs)");
+      return;
+    }
+    launch_copy_host(c, c->d_drain_items.p, nullptr, c->drain_n, S(stream));
   });
 }
 
@@ -1767,6 +1846,29 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
         const uint2 cm = where[e];
         d[e] = CopyItem{items[e].dst, c->hbufs[cm.x].image + (uint64_t)cm.y * cs, items[e].len, items[e].len};
       }
+      // copy-engine drain: the same copies merged into runs where both sides
+      // are contiguous (full chunks of one buffer: no padding between them)
+      c->h_drun.ensure(3 * std::max<uint64_t>(n, 1));
+      uint64_t* rs = c->h_drun.p;
+      uint64_t* rd = rs + n;
+      uint64_t* rl = rs + 2 * n;
+      uint64_t r = 0;
+      for (uint64_t e = 0; e < n; ++e) {
+        if (r && rs[r - 1] + rl[r - 1] == d[e].src && rd[r - 1] + rl[r - 1] == d[e].dst && rl[r - 1] % 16 == 0) {
+          rl[r - 1] += d[e].len;
+        } else {
+          rs[r] = d[e].src;
+          rd[r] = d[e].dst;
+          rl[r] = d[e].len;
+          ++r;
+        }
+      }
+      // compact the dst / len columns behind the first r entries
+      if (r < n) {
+        std::memmove(rs + r, rd, r * sizeof(uint64_t));
+        std::memmove(rs + 2 * r, rl, r * sizeof(uint64_t));
+      }
+      c->drun_n = r;
     }
   }
   // The kernels write the entries and the payload; the header and the gap go up now.
