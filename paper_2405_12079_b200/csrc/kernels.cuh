@@ -894,9 +894,9 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k, false));
   if (q && last_wave) publish_done(q, q_seq);
   if (run_src && result_host) {  // the host reads the run lists once it sees seq
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();  // every run write happens-before thread 0's fence (cumulativity)
     if (t == 0) {
+      __threadfence_system();
       result_host[0] = N;
       result_host[1] = direct ? kPackHeader + kPackEntry * N : payload_off + B;
       result_host[2] = 0;

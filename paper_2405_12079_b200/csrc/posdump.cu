@@ -1550,7 +1550,18 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
       c->timer_begin(kTimHash, s);
       for (uint32_t w = 0; w < W; ++w) {
         hash_range(c, chunk_of(bb[w]), chunk_of(bb[w + 1]), s, w);
-        launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, bb[w], bb[w + 1], ~0ull,
+        // O1 as its own wide launch (one warp per buffer, all SMs) rather
+        // than inside the one-CTA scan, where candidates queue behind 16 warps
+        upload_dag_flags(c, s);
+        const uint32_t nbw = bb[w + 1] - bb[w];
+        if (nbw) {
+          k_buffer_crc<<<(nbw + 7) / 8, 256, 0, s>>>(c->d_bufs.p + bb[w], nbw, c->d_digest[c->cur].p, c->d_tcs.p,
+                                                     c->d_xfold.p + bb[w], c->d_dag_dirty.p + bb[w], c->cfg.dedup, 0,
+                                                     c->d_buf_crc.p + bb[w], c->d_verdict.p + bb[w]);
+          check_launch("k_buffer_crc");
+          ++c->launches;
+        }
+        launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, 0, 0, ~0ull,
                     ds, true, w == 0, nullptr, 0, false, true);
         c->direct_lo[w] = (uint32_t)chunk_of(bb[w]);
       }

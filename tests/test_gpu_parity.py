@@ -853,3 +853,62 @@ def test_cow_staging_keeps_prewrite_bytes(orc, cs):
         small.stage_buffers([1], stream=app)  # 1 MiB + header does not
     assert ei.value.errc == "StagingExhausted"
     small.close()
+
+
+_DRAIN_SCRIPT = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import paper_2405_12079_b200 as pd
+from oracle_ctypes import oracle
+orc = oracle()
+cs = 4096
+sizes = [300000, 1 << 20, 12345, 70001]
+mems, bufs, host = [], [], []
+for i, n in enumerate(sizes):
+    m = pd.DeviceMemory(n); pd.fill_bytes(m.ptr, n, 80 + i)
+    h = np.empty(n, np.uint8); orc.or_fill_bytes(80 + i, h.ctypes.data, n)
+    mems.append(m); host.append(h); bufs.append(pd.GpuBuffer(handle=i + 1, dev_ptr=m.ptr, size=n))
+pd.device_synchronize()
+eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=8 << 20))
+eng.register_buffers(bufs)
+pin = pd.PinnedHost(sum(sizes) + 1024); pin.array[:] = 0
+img, o = [], 0
+for n in sizes:
+    img.append(pin.array[o:o + n]); o += (n + 255) // 256 * 256
+eng.register_image(img)
+s, d = pd.Stream(), pd.Stream()
+for epoch in range(3):
+    if epoch:
+        for i, n in enumerate(sizes):
+            off = (epoch * 7919 * (i + 1)) % n
+            m = min(5000, n - off)
+            pd.fill_bytes(bufs[i].dev_ptr + off, m, 900 + 10 * epoch + i)
+            host[i][off:off + m] = 0
+            t = np.empty(m, np.uint8); orc.or_fill_bytes(900 + 10 * epoch + i, t.ctypes.data, m); host[i][off:off + m] = t
+        pd.device_synchronize()
+        eng.record_dirty([3])
+    eng.precopy_direct(waves=2, stream=s, drain_stream=d)
+    eng.at_final_stop(stream=s); d.wait(s); eng.delta_drain(stream=d)
+    d.synchronize(); s.synchronize()
+    eng.precopy_direct_result()
+    for i in range(len(sizes)):
+        assert np.array_equal(img[i], host[i]), (os.environ.get("POSDUMP_DIRECT_DRAIN"), epoch, i)
+    eng.commit_epoch()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("mode", ["ce", "queue", "sm"])
+def test_direct_drain_modes_agree(mode, tmp_path):
+    """The three host legs of the direct pre-copy (copy-engine runs, SM ship
+    queue, SM drain after each scan) each rebuild the image byte for byte over
+    three incremental epochs with a DAG-dirty buffer (each mode is fixed per
+    process, so each runs in its own interpreter)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ROOT=root, POSDUMP_DIRECT_DRAIN=mode, POSDUMP_WATCHDOG_MS="5000")
+    r = subprocess.run([sys.executable, "-c", _DRAIN_SCRIPT], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
