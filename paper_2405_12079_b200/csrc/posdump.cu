@@ -190,6 +190,7 @@ struct CrcTables {
     ck(cudaFuncGetAttributes(&fa, k_drain_queue), "load k_drain_queue");
     ck(cudaFuncGetAttributes(&fa, k_copy_host), "load k_copy_host");
     ck(cudaFuncGetAttributes(&fa, k_copy_simt), "load k_copy_simt");
+    ck(cudaFuncGetAttributes(&fa, k_copy_vec), "load k_copy_vec");
     ck(cudaFuncGetAttributes(&fa, k_pack_items), "load k_pack_items");
     ck(cudaFuncGetAttributes(&fa, k_buffer_crc), "load k_buffer_crc");
     ck(cudaFuncGetAttributes(&fa, k_note_upstream), "load k_note_upstream");
@@ -416,14 +417,21 @@ void upload_dag_flags(pos_ctx* c, cudaStream_t s, cudaStream_t side = nullptr) {
 }
 
 void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
-                 bool aligned, cudaStream_t s) {
+                 bool aligned, cudaStream_t s, bool prefer_vec = false) {
   int sms = c->crc.sm_count;
   static const bool force_simt = [] {
     const char* e = std::getenv("POSDUMP_COPY");
     return e && !std::strcmp(e, "simt");
   }();
   if (force_simt) aligned = false;
-  if (aligned) {
+  static const bool force_vec = [] {
+    const char* e = std::getenv("POSDUMP_COPY");
+    return e && !std::strcmp(e, "vec");
+  }();
+  if (aligned && (force_vec || prefer_vec)) {
+    const uint32_t ppi = (uint32_t)std::max<uint64_t>(1, (c->cfg.chunk_size + 15 + kVecPiece - 1) / kVecPiece);
+    k_copy_vec<<<sms * 8, 256, 0, s>>>(items, n_dev, n_host, ppi);
+  } else if (aligned) {
     // 3 CTAs/SM fit in smem (64 KiB ring each); one elected thread per CTA.
     int grid = sms * 3;
     if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host));
@@ -1944,6 +1952,7 @@ int pos_delta_copy_ex(pos_ctx* c, void* stream, int stw_end_slot, uint64_t* pack
     const uint64_t n = c->delta_n, cs = c->cfg.chunk_size;
     // Stop-the-world part: a pure TMA bulk gather of the flagged buffers.
     c->timer_begin(kTimDelta, s);
+    // (TMA and SIMT gathers both run ~3x slower while the copy engine drains: measured)
     if (n) launch_copy(c, c->d_delta_items.p, nullptr, n, c->delta_aligned, s);
     c->timer_end(kTimDelta, s);
     if (stw_end_slot >= 0) ck(cudaEventRecord(c->events[stw_end_slot], s), "event");
