@@ -239,7 +239,8 @@ template <bool COPY, int kUnroll, bool kRoll>
 __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
                                                const uint32_t* xinv, uint32_t lsel, int lane,
                                                uint64_t src, uint64_t len, uint32_t k_len,
-                                               uint8_t* dst) {
+                                               uint8_t* dst, bool pf = kL2Prefetch,
+                                               uint32_t pf_steps = kPrefetchSteps) {
   const uint64_t a0 = src & ~15ull;
   const uint64_t lead = src - a0;
   const uint64_t end = lead + len;
@@ -264,7 +265,7 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
   // lookups run), plus a TMA bulk prefetch into L2 kPrefetchSteps ahead so the
   // LDGs mostly hit L2.
   auto prefetch = [&](uint64_t from_blk) {
-    if (kL2Prefetch && lane == 0 && from_blk * kStepBytes < end) {
+    if (pf && lane == 0 && from_blk * kStepBytes < end) {
       uint64_t lo = from_blk * kStepBytes;
       uint64_t hi = (from_blk + kUnroll) * kStepBytes;
       hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
@@ -285,8 +286,8 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
       c3 = adv512(lsel, c3 ^ buf[u].w);
     }
   };
-  if (kL2Prefetch && lane == 0) {  // head of the chunk
-    uint64_t hi = (uint64_t)kPrefetchSteps * kStepBytes;
+  if (pf && lane == 0) {  // head of the chunk
+    uint64_t hi = (uint64_t)pf_steps * kStepBytes;
     hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
     if (hi) l2_prefetch(reinterpret_cast<const void*>(a0), (uint32_t)hi);
   }
@@ -334,13 +335,13 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
     for (;;) {
       const bool moreB = blk + 2 * kUnroll <= full_end;
       if (moreB) load_batch(bufB, blk + kUnroll);
-      prefetch(blk + kPrefetchSteps);
+      prefetch(blk + pf_steps);
       run_batch(bufA, blk);
       blk += kUnroll;
       if (!moreB) break;
       const bool moreA = blk + 2 * kUnroll <= full_end;
       if (moreA) load_batch(bufA, blk + kUnroll);
-      prefetch(blk + kPrefetchSteps);
+      prefetch(blk + pf_steps);
       run_batch(bufB, blk);
       blk += kUnroll;
       if (!moreA) break;
@@ -462,14 +463,15 @@ __global__ void __maxnreg__(kThreads >= 512 ? 120 : (kThreads >= 384 ? 168 : 255
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
-    if (p.pf_bytes && n) {
+    if (p.pf_bytes > 1 && n) {
       const uint64_t pa = (src + lo + 15) & ~15ull;
       const uint64_t pe = (src + lo + (n < p.pf_bytes ? n : p.pf_bytes)) & ~15ull;
       for (uint64_t q = pa + (uint64_t)lane * 16384; q < pe; q += 32 * 16384)
         l2_prefetch(reinterpret_cast<const void*>(q), (uint32_t)(pe - q < 16384 ? pe - q : 16384));
     }
     const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll>(small, p.xinv, lsel, lane, src + lo, n,
-                                            p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr)
+                                            p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr,
+                                            p.pf_bytes == 1, (uint32_t)p.pad3)
                          : 0u;
     if (nseg == 1) {
       crc = r;

@@ -844,9 +844,15 @@ static void set_segments(const pos_ctx* c, uint64_t items, HashParams& p) {
   p.xseg = c->d_xseg.p + 32 * L;
   p.lastseg = c->d_lastseg.p + (size_t)nb * L;
   p.pf_bytes = 0;
-  if (const char* e = std::getenv("POSDUMP_PF")) {  // tuning: L2 prefetch of single-round units
-    uint64_t v = std::strtoull(e, nullptr, 10);
-    if (v && (items << L) <= warps) p.pf_bytes = (uint32_t)std::min<uint64_t>(v, p.seg_bytes);
+  if (const char* e = std::getenv("POSDUMP_PF")) {  // tuning: L2 bulk prefetch
+    if (!std::strcmp(e, "slide")) {
+      p.pf_bytes = 1;  // a sliding window POSDUMP_PF_STEPS (default 32) 512-B steps ahead of every warp
+      const char* d = std::getenv("POSDUMP_PF_STEPS");
+      p.pad3 = d ? std::atoi(d) : 32;
+    } else {  // the first N bytes of single-round units at unit start
+      uint64_t v = std::strtoull(e, nullptr, 10);
+      if (v > 1 && (items << L) <= warps) p.pf_bytes = (uint32_t)std::min<uint64_t>(v, p.seg_bytes);
+    }
   }
 }
 

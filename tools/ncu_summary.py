@@ -51,10 +51,14 @@ def launches(path):
     return out
 
 
-def report(path, alg_bytes=None):
+def report(path, alg_bytes=None, match=None):
+    """Summary of the first launch in the report (or the first whose kernel
+    name contains `match`)."""
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u = rows[0], rows[1]
+    ki = h.index("Kernel Name")
+    v = next(r for r in rows[2:] if match is None or match in r[ki])
     out = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else None}
     for i, n in enumerate(h):
         if n in KEYS:
@@ -82,4 +86,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     else:
-        print(json.dumps(report(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None), indent=1))
+        print(json.dumps(report(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] else None,
+                                sys.argv[4] if len(sys.argv) > 4 else None), indent=1))
