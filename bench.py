@@ -602,20 +602,20 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": round(hash_ms, 5),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                         "note": ("dominant HBM kernel; the step's largest kernel by time is the drain "
-                                  "(k_copy_host in direct mode, ~87% of kernel time in the ncu launch list), "
-                                  "which is host-link bound: see host_link")},
+                         "note": ("dominant HBM kernel of the dump; the step itself is bound by the host leg "
+                                  "(copy-engine runs into the pinned image in direct mode): see host_link")},
             "host_link": {"bound": "pcie", "achieved": round(d2h_achieved, 2), "peak": round(link_peak, 2),
                           "unit": "GB/s", "frac": round(d2h_achieved / link_peak, 4),
                           "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run",
-                          "achieved_over": "pre-copy pack D2H window (first wave copy -> last wave byte)"},
+                          "achieved_over": "pre-copy host leg (first byte -> last byte of the pre-copy)"},
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
                           for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "delta_hash_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": int(statistics.mean(r["h2d_bytes"] for r in e2e_res)),
                     "d2h_bytes_per_step": int(statistics.mean(r["precopy_bytes"] + r["delta_bytes"] + 24
                                                               for r in e2e_res)),
-                    "how": "host wall clock around DumpEngine calls incl. pinned D2H and host-side pack apply into the image"},
+                    "how": ("host wall clock around the DumpEngine calls until every byte is in the host image "
+                            "(direct: the copy engine writes the pinned image; pack: D2H + host-side pack apply)")},
             "image_parity": bool(ok),
             **({"restore": restore} if restore else {}),
             "clocks": clk.summary(),
