@@ -1535,9 +1535,18 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
     const uint32_t nb = (uint32_t)c->bufs.size();
     uint32_t W = std::max<uint32_t>(1, std::min<uint32_t>(waves, pos_ctx::kMaxWaves));
     W = std::min<uint32_t>(W, std::max<uint32_t>(nb, 1));
-    std::vector<uint32_t> bb(1, 0);  // waves of whole buffers (O1), ~equal chunk counts
+    // Waves of whole buffers (O1), ~equal chunk counts -- except an optional
+    // small first wave (POSDUMP_FIRST_WAVE = fraction of the chunks) so the
+    // host leg starts after a short hash + scan while the rest is hashed.
+    static const double first = [] {
+      const char* e = std::getenv("POSDUMP_FIRST_WAVE");
+      return e ? std::atof(e) : 0.0;
+    }();
+    std::vector<uint32_t> bb(1, 0);
     for (uint32_t w = 1; w < W; ++w) {
       uint64_t target = c->n_chunks * w / W;
+      if (first > 0 && first < 1)
+        target = (uint64_t)(c->n_chunks * (first + (1 - first) * (double)(w - 1) / (W - 1)));
       uint32_t b = bb.back();
       while (b < nb && c->chunk_base[b] < target) ++b;
       if (b > bb.back() && b < nb) bb.push_back(b);
@@ -1627,12 +1636,6 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
       q = c->d_q.p;
       ++c->q_seq;
       ck(cudaStreamWaitEvent(s, c->ev_drained, 0), "wait queue reset");  // previous drain gone
-      static const bool after_hash = std::getenv("POSDUMP_DRAIN_AFTER_HASH") != nullptr;  // diagnostics
-      if (after_hash) {
-        hash_range(c, 0, 0, s, 0);
-        ck(cudaEventRecord(c->ev_drained, s), "event");
-        ck(cudaStreamWaitEvent(ds, c->ev_drained, 0), "wait");
-      }
       c->timer_begin(kTimD2H, ds);
       k_drain_queue<<<kDrainCtas, kDrainThreads, 0, ds>>>(q, c->q_seq, c->d_bufs.p, c->d_chunk_map.p,
                                                          c->cfg.chunk_size,
