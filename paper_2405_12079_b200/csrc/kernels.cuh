@@ -976,6 +976,260 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
 }
 
 // ---------------------------------------------------------------------------
+// Tiled scan for the copy-engine direct pre-copy (no O1 phase: k_buffer_crc
+// ran before it).  Tiles of `wpt` 32-chunk words are taken in order through an
+// atomic ticket; each publishes its aggregate {entries, padded bytes, runs},
+// looks back over its predecessors (decoupled look-back: an inclusive prefix
+// stops the walk, aggregates are summed past) and publishes its inclusive
+// prefix.  Status flags carry the launch's sequence number, so nothing is
+// cleared between launches; the last ticket resets the ticket counter, and
+// the last tile to finish emitting writes the header and the host mirror.
+struct TileStatus {
+  unsigned long long agg_flag, inc_flag;  // = seq when the values below are valid
+  unsigned long long agg[3], inc[3];      // entries, padded payload bytes, runs
+};
+struct TileCtl {
+  unsigned int ticket;     // next tile id
+  unsigned int finished;   // tiles done emitting
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
+    const DevBuf* bufs, const uint2* chunk_map, uint64_t chunk_lo, uint64_t chunk_hi, uint64_t chunk_size,
+    const uint8_t* flags, const uint8_t* verdict, const uint8_t* dag_dirty, int exclude_dag,
+    const uint32_t* digests, uint64_t epoch, uint8_t* cache, uint64_t cache_capacity, uint64_t* cursor,
+    uint64_t fixed_base, uint64_t* result, volatile uint64_t* result_host, uint64_t seq, uint32_t* bitmap,
+    uint64_t n_total, uint64_t* run_src, uint64_t* run_dst, uint64_t* run_len, TileStatus* status,
+    TileCtl* ctl, uint32_t wpt) {
+  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_wr[kScanWarps];
+  __shared__ uint64_t s_pre[3], s_agg[3];
+  __shared__ uint32_t s_tile, s_last;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t w0 = chunk_lo >> 5, w1 = (chunk_hi + 31) >> 5;
+  const uint32_t ntiles = (uint32_t)((w1 - w0 + wpt - 1) / wpt);
+  if (t == 0) s_tile = atomicAdd(&ctl->ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  if (t == 0 && tile == ntiles - 1) ctl->ticket = 0;  // every other ticket is taken
+  const uint64_t base = fixed_base != ~0ull ? fixed_base : *cursor;
+  uint8_t* pack = cache + base;
+  const uint64_t tw0 = w0 + (uint64_t)tile * wpt, tw1 = tw0 + wpt < w1 ? tw0 + wpt : w1;
+  const uint64_t per_w = (tw1 - tw0 + kScanWarps - 1) / kScanWarps;
+  const uint64_t r0 = tw0 + (uint64_t)warp * per_w < tw1 ? tw0 + (uint64_t)warp * per_w : tw1;
+  const uint64_t r1 = r0 + per_w < tw1 ? r0 + per_w : tw1;
+  struct Lane {
+    uint2 cm;
+    uint32_t mask, start;
+    uint64_t len;
+  };
+  auto look = [&](uint64_t k) -> Lane {
+    const uint64_t g = 32 * k + lane;
+    const bool in = g >= chunk_lo && g < chunk_hi;
+    Lane L{make_uint2(0, 0), 0u, 0u, 0};
+    uint8_t f = 0;
+    if (in) {
+      L.cm = chunk_map[g];
+      f = flags[g];
+    }
+    bool el = false;
+    if (in && f) {
+      el = !verdict[L.cm.x] && !(exclude_dag && dag_dirty[L.cm.x]);
+      if (el) {
+        const DevBuf& b = bufs[L.cm.x];
+        L.len = L.cm.y + 1 == b.nchunks ? b.size - (uint64_t)L.cm.y * chunk_size : chunk_size;
+      }
+    }
+    L.mask = __ballot_sync(0xffffffffu, el);
+    const uint32_t prev_buf = __shfl_up_sync(0xffffffffu, L.cm.x, 1);
+    const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && prev_buf == L.cm.x);
+    L.start = L.mask & ~(L.mask & (L.mask << 1) & same);
+    if (bitmap) {
+      const uint64_t last = (32 * k + 31 < n_total ? 32 * k + 31 : n_total - 1);
+      if (last >= chunk_lo && last < chunk_hi) {
+        const uint32_t fb = in ? f : (g < n_total ? flags[g] : 0);
+        const uint32_t word = __ballot_sync(0xffffffffu, fb != 0);
+        if (lane == 0) bitmap[k] = word;
+      }
+    }
+    return L;
+  };
+  auto warp_sum = [&](uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  Lane keep[kScanKeep];
+  uint64_t wn = 0, wb = 0, wr = 0;
+  auto count = [&](const Lane& L) {
+    wn += __popc(L.mask);
+    wr += __popc(L.start);
+    wb += warp_sum(L.len ? (L.len + 15) & ~15ull : 0);
+  };
+#pragma unroll
+  for (int j = 0; j < kScanKeep; ++j) {
+    keep[j] = Lane{make_uint2(0, 0), 0u, 0u, 0};
+    if (r0 + j < r1) {
+      keep[j] = look(r0 + j);
+      count(keep[j]);
+    }
+  }
+  for (uint64_t k = r0 + kScanKeep; k < r1; ++k) count(look(k));
+  if (lane == 0) {
+    s_wn[warp] = wn;
+    s_wb[warp] = wb;
+    s_wr[warp] = wr;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t v[3] = {lane < kScanWarps ? s_wn[lane] : 0, lane < kScanWarps ? s_wb[lane] : 0,
+                     lane < kScanWarps ? s_wr[lane] : 0};
+    uint64_t in[3] = {v[0], v[1], v[2]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint64_t a = __shfl_up_sync(0xffffffffu, in[q], o);
+        if (lane >= o) in[q] += a;
+      }
+    }
+    if (lane < kScanWarps) {
+      s_wn[lane] = in[0] - v[0];
+      s_wb[lane] = in[1] - v[1];
+      s_wr[lane] = in[2] - v[2];
+    }
+    uint64_t agg[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) agg[q] = __shfl_sync(0xffffffffu, in[q], 31);
+    if (lane == 0) {
+      TileStatus* my = status + tile;
+      if (tile == 0) {  // no predecessor: the inclusive prefix is the aggregate
+        for (int q = 0; q < 3; ++q) my->inc[q] = agg[q];
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&my->inc_flag), "l"((unsigned long long)seq)
+                     : "memory");
+        for (int q = 0; q < 3; ++q) s_pre[q] = 0;
+      } else {
+        for (int q = 0; q < 3; ++q) my->agg[q] = agg[q];
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&my->agg_flag), "l"((unsigned long long)seq)
+                     : "memory");
+        uint64_t pre[3] = {0, 0, 0};
+        for (int p = (int)tile - 1; p >= 0;) {
+          TileStatus* st = status + p;
+          unsigned long long fi, fa;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(fi) : "l"(&st->inc_flag) : "memory");
+          if (fi == seq) {
+            for (int q = 0; q < 3; ++q) pre[q] += st->inc[q];
+            break;
+          }
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(fa) : "l"(&st->agg_flag) : "memory");
+          if (fa == seq) {
+            for (int q = 0; q < 3; ++q) pre[q] += st->agg[q];
+            --p;
+          }
+          // else: the predecessor has not published yet -- poll again
+        }
+        for (int q = 0; q < 3; ++q) my->inc[q] = pre[q] + agg[q];
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&my->inc_flag), "l"((unsigned long long)seq)
+                     : "memory");
+        for (int q = 0; q < 3; ++q) s_pre[q] = pre[q];
+      }
+      for (int q = 0; q < 3; ++q) s_agg[q] = agg[q];
+    }
+  }
+  __syncthreads();
+  // Emit: entries at their global index, runs at their global run index.
+  uint64_t e = s_pre[0] + s_wn[warp], off = s_pre[1] + s_wb[warp], rb = s_pre[2] + s_wr[warp];
+  auto emit = [&](uint64_t k, const Lane& L) {
+    const uint32_t cont = L.mask & ~L.start;
+    const uint32_t rest = lane < 31 ? cont >> (lane + 1) : 0u;
+    const int nrun = __ffs(~rest);
+    const int last = lane + nrun - 1 < 31 ? lane + nrun - 1 : 31;
+    const uint64_t last_len = __shfl_sync(0xffffffffu, L.len, last);
+    const uint64_t pl = L.len ? (L.len + 15) & ~15ull : 0;
+    uint64_t incl = pl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t a = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += a;
+    }
+    if (L.mask >> lane & 1) {
+      const DevBuf& b = bufs[L.cm.x];
+      const uint64_t g = 32 * k + lane;
+      const uint64_t my_e = e + __popc(L.mask & lt), my_off = off + incl - pl;
+      if (base + kPackHeader + (my_e + 1) * kPackEntry <= cache_capacity) {  // (host reserves the worst case)
+        uint4* ent = reinterpret_cast<uint4*>(pack + kPackHeader + my_e * kPackEntry);
+        ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)my_off,
+                            (uint32_t)(my_off >> 32));
+        ent[1] = make_uint4(L.cm.y, (uint32_t)L.len, digests[g], 0u);
+      }
+      if (L.start >> lane & 1) {
+        const uint64_t ri = rb + __popc(L.start & lt);
+        run_src[ri] = b.ptr + (uint64_t)L.cm.y * chunk_size;
+        run_dst[ri] = b.image + (uint64_t)L.cm.y * chunk_size;
+        run_len[ri] = (uint64_t)(nrun - 1) * chunk_size + last_len;
+      }
+    }
+    e += __popc(L.mask);
+    off += __shfl_sync(0xffffffffu, incl, 31);
+    rb += __popc(L.start);
+  };
+#pragma unroll
+  for (int j = 0; j < kScanKeep; ++j)
+    if (r0 + j < r1) emit(r0 + j, keep[j]);
+  for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k));
+  // The last tile to finish writes the header and tells the host.
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctl->finished, 1u) == ntiles - 1;
+  }
+  __syncthreads();
+  if (!s_last || t != 0) return;
+  ctl->finished = 0;
+  const TileStatus* lastst = status + (ntiles - 1);
+  unsigned long long fl;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(fl) : "l"(&lastst->inc_flag) : "memory");
+  } while (fl != seq);
+  const uint64_t N = lastst->inc[0], B = lastst->inc[1], R = lastst->inc[2];
+  const uint64_t total = kPackHeader + kPackEntry * N;  // index pack: header + entries
+  const bool overflow = base + total > cache_capacity;
+  uint32_t* h = reinterpret_cast<uint32_t*>(pack);
+  if (!overflow) {
+    h[0] = kPackMagic;
+    h[1] = 1;
+    *reinterpret_cast<uint64_t*>(pack + 8) = chunk_size;
+    h[4] = (uint32_t)N;
+    h[5] = kPackFlagDirect;
+    *reinterpret_cast<uint64_t*>(pack + 24) = total;
+    *reinterpret_cast<uint64_t*>(pack + 32) = 0;
+    *reinterpret_cast<uint64_t*>(pack + 40) = epoch;
+    *reinterpret_cast<uint64_t*>(pack + 48) = total;
+    *reinterpret_cast<uint64_t*>(pack + 56) = 0;
+    if (cursor) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
+  }
+  result[0] = N;
+  result[1] = total;
+  result[2] = overflow;
+  result[3] = overflow ? 0 : N;
+  result[4] = base;
+  result[6] = B;
+  result[7] = R;
+  result_host[0] = N;
+  result_host[1] = total;
+  result_host[2] = overflow;
+  result_host[3] = overflow ? 0 : N;
+  result_host[4] = base;
+  result_host[6] = B;
+  result_host[7] = R;
+  __threadfence_system();
+  result_host[5] = seq;
+  __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------
 // Bulk copy engine: each CTA streams its items (grid-stride) through a ring of
 // kCopyStages smem slots with cp.async.bulk (TMA bulk) G->S loads completing
 // on an mbarrier and S->G bulk stores tracked by bulk groups; one elected

@@ -187,6 +187,7 @@ struct CrcTables {
          "carveout");
     cudaFuncAttributes fa;
     ck(cudaFuncGetAttributes(&fa, k_pack_scan), "load k_pack_scan");
+    ck(cudaFuncGetAttributes(&fa, k_scan_tiles), "load k_scan_tiles");
     ck(cudaFuncGetAttributes(&fa, k_drain_queue), "load k_drain_queue");
     ck(cudaFuncGetAttributes(&fa, k_copy_host), "load k_copy_host");
     ck(cudaFuncGetAttributes(&fa, k_copy_simt), "load k_copy_simt");
@@ -323,6 +324,8 @@ struct pos_ctx {
   // into mapped pinned memory = the arguments of cudaMemcpyBatchAsync
   PinnedArray<uint64_t> h_run;   // [3][n_chunks]: src, dst, bytes
   PinnedArray<uint64_t> h_drun;  // STW delta drain runs, same layout
+  DevArray<TileStatus> d_tiles;  // tiled scan: decoupled look-back status
+  DevArray<TileCtl> d_tile_ctl;  // [kMaxWaves]: ticket + finished counters
   uint64_t drun_n = 0, drun_cap = 0;
   uint32_t direct_lo[16] = {};  // first chunk of each direct wave (kMaxWaves)
   uint32_t direct_waves = 0;
@@ -577,6 +580,8 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_drain_items.release();
   c->d_q.release();
   c->h_run.release();
+  c->d_tiles.release();
+  c->d_tile_ctl.release();
   c->h_drun.release();
   c->d_qslots.release();
   if (c->ev_drained) cudaEventDestroy(c->ev_drained);
@@ -1031,6 +1036,39 @@ static void launch_pack(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint6
   launch_copy(c, c->d_items.p + lo, res + 3, 0, aligned, s);
   c->timer_end(kTimCopy, s);
   ck(cudaEventRecord(c->copied[slot], s), "event");
+  c->pack_pending = true;
+}
+
+// Tiled scan (copy-engine direct mode): index entries + runs of [lo, hi)
+// over many CTAs with decoupled look-back.
+static void launch_scan_tiles(pos_ctx* c, int exclude_dag_dirty, cudaStream_t s, uint64_t lo, uint64_t hi,
+                              uint32_t slot, bool chain_start) {
+  upload_dag_flags(c, s);
+  const uint64_t words = (hi + 31) / 32 - lo / 32;
+  const uint32_t wpt = words <= 16ull * 2 * (uint64_t)c->crc.sm_count ? 16u : 64u;  // 1 or 4 rounds per warp
+  const uint32_t ntiles = (uint32_t)std::max<uint64_t>(1, (words + wpt - 1) / wpt);
+  if (c->d_tiles.n < ntiles) {
+    ck(cudaStreamSynchronize(s), "sync");
+    c->d_tiles.ensure(ntiles);
+    ck(cudaMemset(c->d_tiles.p, 0, ntiles * sizeof(TileStatus)), "tiles");
+  }
+  if (!c->d_tile_ctl.p) {
+    c->d_tile_ctl.ensure(pos_ctx::kMaxWaves);
+    ck(cudaMemset(c->d_tile_ctl.p, 0, pos_ctx::kMaxWaves * sizeof(TileCtl)), "tile ctl");
+  }
+  uint64_t* res = c->d_scan.p + 8 * slot;
+  c->timer_begin(kTimScan, s);
+  k_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(
+      c->d_bufs.p, c->d_chunk_map.p, lo, hi, c->cfg.chunk_size, c->d_flags.p, c->d_verdict.p, c->d_dag_dirty.p,
+      exclude_dag_dirty, c->d_digest[c->cur].p, c->epoch, c->cache.p, c->cache_cap - c->staging_used,
+      c->d_cursor.p, chain_start ? 0ull : ~0ull, res, c->h_scan.p + 8 * slot, ++c->scan_seq, c->d_bitmap.p,
+      c->n_chunks, c->h_run.p + lo, c->h_run.p + c->n_chunks + lo, c->h_run.p + 2 * c->n_chunks + lo, c->d_tiles.p,
+      c->d_tile_ctl.p + slot, wpt);
+  c->slot_seq[slot] = c->scan_seq;
+  check_launch("k_scan_tiles");
+  c->timer_end(kTimScan, s);
+  ++c->launches;
+  ck(cudaEventRecord(c->scanned[slot], s), "event");
   c->pack_pending = true;
 }
 
@@ -1584,8 +1622,15 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
           check_launch("k_buffer_crc");
           ++c->launches;
         }
-        launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, 0, 0, ~0ull,
-                    ds, true, w == 0, nullptr, 0, false, true);
+        static const bool tiled = [] {
+          const char* e = std::getenv("POSDUMP_SCAN");  // "single": the one-CTA k_pack_scan
+          return !(e && !std::strcmp(e, "single"));
+        }();
+        if (tiled)
+          launch_scan_tiles(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, w == 0);
+        else
+          launch_pack(c, exclude_dag_dirty, s, chunk_of(bb[w]), chunk_of(bb[w + 1]), w, 0, 0, ~0ull,
+                      ds, true, w == 0, nullptr, 0, false, true);
         c->direct_lo[w] = (uint32_t)chunk_of(bb[w]);
       }
       c->timer_end(kTimHash, s);

@@ -912,3 +912,68 @@ def test_direct_drain_modes_agree(mode, tmp_path):
     env = dict(os.environ, ROOT=root, POSDUMP_DIRECT_DRAIN=mode, POSDUMP_WATCHDOG_MS="5000")
     r = subprocess.run([sys.executable, "-c", _DRAIN_SCRIPT], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_direct_tiled_scan_many_tiles(orc):
+    """The tiled scan (decoupled look-back over ~200 CTAs) with 64-byte chunks
+    over ~20 MB: index entries == the oracle pack's entries, the dirty bitmap
+    == the digest comparison, the image == the device, across a fresh and an
+    incremental epoch with provenance buffers and a DAG-dirty buffer."""
+    rng = np.random.default_rng(11)
+    cs = 64
+    sizes = [int(x) for x in rng.integers(1, 900_000, 40)] + [1, 63, 64, 65]
+    p = Proc(orc, sizes, seed0=8100)
+    for i in (3, 17):  # dedup-ok provenance buffers
+        p.bufs[i].upstream = pd.Upstream(ocrc(orc, p.host[i]), True)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=64 << 20))
+    eng.register_buffers(p.bufs)
+    pin = pd.PinnedHost(sum((n + 255) // 256 * 256 for n in sizes))
+    pin.array[:] = 0
+    img, o = [], 0
+    for n in sizes:
+        img.append(pin.array[o:o + n])
+        o += (n + 255) // 256 * 256
+    eng.register_image(img)
+    s, d = pd.Stream(), pd.Stream()
+    prev = None
+    for epoch in range(2):
+        if epoch:
+            for i in rng.choice(len(sizes), 12, replace=False):
+                n = sizes[i]
+                off = int(rng.integers(0, n))
+                m = int(min(n - off, rng.integers(1, 5000)))
+                p.write(int(i), off, m, 7000 + int(i))
+            pd.device_synchronize()
+            eng.record_dirty([9])
+        eng.precopy_direct(waves=1, stream=s, drain_stream=d)
+        eng.at_final_stop(stream=s)
+        d.wait(s)
+        eng.delta_drain(stream=d)
+        d.synchronize()
+        s.synchronize()
+        nch, _ = eng.precopy_direct_result()
+        dig = np.concatenate([odigests(orc, h, cs) for h in p.host])
+        assert np.array_equal(eng.digests(), dig)
+        flags = np.ones(dig.size, bool) if prev is None else dig != prev
+        bounds = np.cumsum([0] + [(n + cs - 1) // cs for n in sizes])
+        bm = eng.bitmap()
+        want_bm = np.zeros(bm.size, np.uint32)
+        for g in np.nonzero(flags)[0]:
+            want_bm[g >> 5] |= np.uint32(1 << (int(g) & 31))
+        assert np.array_equal(bm, want_bm)
+        elig = flags.copy()
+        for i in (3, 17):
+            elig[bounds[i]:bounds[i + 1]] = False  # O1: dedup
+        if epoch:
+            elig[bounds[8]:bounds[9]] = False  # DAG-dirty handle 9: the STW delta ships it
+        assert nch == int(elig.sum())
+        idx = download_cache(eng, 0, 64 + 32 * nch)
+        ref = opack(orc, list(zip(p.handles, p.host)), cs, elig.astype(np.uint8), epoch)
+        assert np.array_equal(idx[64:], ref[64:64 + 32 * nch])
+        for i in range(len(sizes)):
+            if i in (3, 17):
+                continue  # dedup'd: the image keeps whatever the target had (DedupRef)
+            assert np.array_equal(img[i], p.host[i]), f"epoch {epoch} buffer {i}"
+        prev = dig
+        eng.commit_epoch()
+    eng.close()
