@@ -403,12 +403,17 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
 
     class AppThread:
         """Long-lived application host thread: submits a window of kernels
-        (pos_fill_batch) on the app stream, then records event 2."""
+        (pos_fill_batch) on the app stream, records event 2, and -- like an
+        interception layer on the application's own thread -- enqueues the
+        final stop right behind its last kernel (once the dump's host side
+        has staged the delta), so the stop-the-world gather starts the moment
+        the window drains."""
 
         def __init__(self):
             self.q, self.done = [], threading.Event()
-            self.go = threading.Event()
+            self.go, self.staged = threading.Event(), threading.Event()
             self.fill, self.h = pd.lib().pos_fill_batch, int(app)
+            self.stw = None
             threading.Thread(target=self.run, daemon=True).start()
 
         def run(self):
@@ -418,10 +423,16 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                 for a in self.q:
                     self.fill(a.ctypes.data, a.shape[0], self.h)
                 eng.event_record(2, app)
+                self.staged.wait()  # the engine is not re-entrant: after prepare_final_stop
+                self.staged.clear()
+                try:
+                    self.stw_result, self.error = self.stw(), None
+                except Exception as ex:  # surfaced on the main thread
+                    self.stw_result, self.error = None, ex
                 self.done.set()
 
-        def submit(self, args_list):
-            self.q = args_list
+        def submit(self, args_list, stw):
+            self.q, self.stw = args_list, stw
             self.done.clear()
             self.go.set()
 
@@ -451,7 +462,13 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # sets, process.hpp:313-344): their buffers are left to the STW pass,
         # as record_dirty's copy cancellation does (cr.hpp:909-918).
         eng.record_dirty(dag_writes)
-        app_thread.submit(app_args)  # the application's own host thread
+        def final_stop():  # at_final_stop (cr.hpp:599-621): drain the app, STW gather
+            eng.stream_wait_event(2, ckpt)
+            eng.event_record(3, ckpt)
+            eng.stamp(3, ckpt)
+            return eng.at_final_stop(stream=ckpt, stw_end_slot=4)  # STW ends after the gather
+
+        app_thread.submit(app_args, final_stop)  # the application's own host thread
         eng.event_record(0, ckpt)  # device clock starts with the dump's first operation
         if direct:  # hash -> O1 -> scan per wave; chunks stored into the image on `copy`
             eng.precopy_direct(waves=args.waves, stream=ckpt, drain_stream=copy)
@@ -464,10 +481,11 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # stop window holds only the gather; then the final stop: hold the app
         # (its window is fully submitted) and drain it.
         eng.prepare_final_stop(stream=ckpt)
+        app_thread.staged.set()
         app_thread.wait()
-        eng.stream_wait_event(2, ckpt)
-        eng.event_record(3, ckpt)
-        doff, dbytes = eng.at_final_stop(stream=ckpt, stw_end_slot=4)  # STW ends after the gather
+        if app_thread.error is not None:
+            raise app_thread.error
+        doff, dbytes = app_thread.stw_result
         copy.wait(ckpt)
         if direct:
             eng.delta_drain(stream=copy)
@@ -493,6 +511,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         t1 = time.perf_counter()
         ms = eng.event_elapsed(0, 5)
         stw = eng.event_elapsed(3, 4)
+        stw_dev = eng.stamp_elapsed(3, 4)  # same window on the device clock
 
         def kms(name):
             try:
@@ -506,7 +525,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             tl.update(eng.timeline(0))
             tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]
             print(json.dumps(tl), file=sys.stderr)
-        r = {"ms": ms, "stw_ms": stw, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
+        r = {"ms": ms, "stw_ms": stw, "stw_dev_ms": stw_dev, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
              "precopy_bytes": pre_payload if direct else sum(z for _, z in packs),
              "delta_bytes": dpay if direct else dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
@@ -587,6 +606,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             "warmup": args.warmup,
             "ms_per_step": round(step_ms, 4),
             "stw_ms": round(stw_ms, 4),
+            "stw_device_clock_ms": round(statistics.median(r["stw_dev_ms"] for r in res), 4),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,

@@ -328,6 +328,11 @@ int pos_stream_wait_event(pos_ctx* ctx, uint32_t slot, void* stream);
 /* Device timeline: for each internal timer (hash, combine, scan, copy, delta,
  * scatter, d2h) the ms from event `slot` to its begin and end (-1 if unused). */
 int pos_timeline(pos_ctx* ctx, uint32_t slot, float* out14);
+/* Device clock (globaltimer) stamp in stream order, by a one-thread kernel;
+ * pos_delta_copy_ex also stamps its stw_end_slot.  Elapsed ms between two
+ * stamps (synchronises the device). */
+int pos_stamp(pos_ctx* ctx, uint32_t slot, void* stream);
+int pos_stamp_elapsed(pos_ctx* ctx, uint32_t a, uint32_t b, float* ms);
 /* Kernels this context has launched (monotone counter). */
 int pos_launch_count(pos_ctx* ctx, uint64_t* out);
 /* Device time of the most recent hash kernel launch (ms). */

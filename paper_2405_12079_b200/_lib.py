@@ -141,6 +141,8 @@ SIGNATURES = {
     "pos_event_record": [P, U32, P],
     "pos_event_elapsed": [P, U32, U32, C.POINTER(C.c_float)],
     "pos_stream_wait_event": [P, U32, P],
+    "pos_stamp": [P, U32, P],
+    "pos_stamp_elapsed": [P, U32, U32, C.POINTER(C.c_float)],
     "pos_timeline": [P, U32, P],
     "pos_launch_count": [P, PU64],
     "pos_last_kernel_ms": [P, C.c_char_p, C.POINTER(C.c_float)],

@@ -1496,6 +1496,42 @@ __global__ void __launch_bounds__(kDrainThreads, 32) k_drain_queue(ShipQueue* q,
   }
 }
 
+// Staging without the copy engine: the STW delta's header, work list and copy
+// items travel from mapped pinned memory into device memory by SM loads (the
+// copy engines are busy with the pre-copy's host leg; an H2D memcpy queued
+// behind it held the ckpt stream -- and so the final stop -- for ~50 us).
+struct StageSeg {
+  const uint8_t* src;  // mapped pinned host memory (16-B aligned)
+  uint8_t* dst;        // device memory (16-B aligned); src == null: zero-fill
+  uint64_t len;        // multiple of 16
+};
+struct StageList {
+  StageSeg seg[5];
+  uint32_t n;
+};
+
+__global__ void k_stage_in(const __grid_constant__ StageList L) {
+  for (uint32_t s = 0; s < L.n; ++s) {
+    const StageSeg g = L.seg[s];
+    const uint64_t n16 = g.len / 16;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (g.src)  // uncached: the host rewrites the staging buffer between launches
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(g.src + 16 * i));
+      reinterpret_cast<uint4*>(g.dst)[i] = v;
+    }
+  }
+}
+
+// A globaltimer stamp in stream order, written by a one-thread kernel: a
+// clock that does not ride the channel's event machinery (timing events on a
+// stream queued next to a long copy-engine batch were seen landing ~40 us
+// late).
+__global__ void k_stamp(unsigned long long* at) { *at = globaltimer_ns(); }
+
 // ---------------------------------------------------------------------------
 // Restore: POSD entries -> copy items (pack payload -> buffer chunk).
 // Validation mirrors write_content's range check (buffer.hpp:80) and the

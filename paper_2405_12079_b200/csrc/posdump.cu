@@ -196,6 +196,8 @@ struct CrcTables {
     ck(cudaFuncGetAttributes(&fa, k_buffer_crc), "load k_buffer_crc");
     ck(cudaFuncGetAttributes(&fa, k_note_upstream), "load k_note_upstream");
     ck(cudaFuncGetAttributes(&fa, k_fill), "load k_fill");
+    ck(cudaFuncGetAttributes(&fa, k_stage_in), "load k_stage_in");
+    ck(cudaFuncGetAttributes(&fa, k_stamp), "load k_stamp");
   }
 };
 
@@ -361,6 +363,7 @@ struct pos_ctx {
   bool pack_pending = false;
   // timing
   std::vector<cudaEvent_t> events;
+  DevArray<unsigned long long> d_stamps;  // [64] globaltimer stamps (pos_stamp)
   Timer timers[kTimCount];
   uint64_t launches = 0;
 
@@ -579,6 +582,7 @@ int pos_ctx_destroy(pos_ctx* c) {
   c->d_delta_items.release();
   c->d_drain_items.release();
   c->d_q.release();
+  c->d_stamps.release();
   c->h_run.release();
   c->d_tiles.release();
   c->d_tile_ctl.release();
@@ -1944,24 +1948,26 @@ static void delta_prepare(pos_ctx* c, cudaStream_t s) {
       c->drun_n = r;
     }
   }
-  // The kernels write the entries and the payload; the header and the gap go up now.
-  ck(cudaMemcpyAsync(pack, st, kPackHeader, cudaMemcpyHostToDevice, s), "delta header");
-  if (payload_off > kPackHeader + kPackEntry * n)
-    ck(cudaMemsetAsync(pack + kPackHeader + kPackEntry * n, 0, payload_off - kPackHeader - kPackEntry * n, s),
-       "gap");
+  // The kernels write the entries and the payload; the header, the gap and
+  // the work / item lists go up now -- by SM loads from the mapped staging
+  // buffer, not by the copy engine (which the host leg keeps busy).
+  StageList sl{};
+  sl.seg[sl.n++] = StageSeg{st, pack, kPackHeader};
+  const uint64_t gap0 = kPackHeader + kPackEntry * n;
+  if (payload_off > gap0) sl.seg[sl.n++] = StageSeg{nullptr, pack + gap0, payload_off - gap0};
   if (n) {
     c->d_delta_items.ensure(n);
-    ck(cudaMemcpyAsync(c->d_work.p, st + kPackHeader, work_bytes, cudaMemcpyHostToDevice, s), "work");
-    ck(cudaMemcpyAsync(c->d_delta_items.p, st + kPackHeader + work_bytes, item_bytes,
-                       cudaMemcpyHostToDevice, s),
-       "items");
+    sl.seg[sl.n++] = StageSeg{st + kPackHeader, reinterpret_cast<uint8_t*>(c->d_work.p), work_bytes};
+    sl.seg[sl.n++] = StageSeg{st + kPackHeader + work_bytes, reinterpret_cast<uint8_t*>(c->d_delta_items.p), item_bytes};
     if (drain_bytes) {
       c->d_drain_items.ensure(n);
-      ck(cudaMemcpyAsync(c->d_drain_items.p, st + kPackHeader + work_bytes + item_bytes, drain_bytes,
-                         cudaMemcpyHostToDevice, s),
-         "drain items");
+      sl.seg[sl.n++] = StageSeg{st + kPackHeader + work_bytes + item_bytes,
+                                reinterpret_cast<uint8_t*>(c->d_drain_items.p), drain_bytes};
     }
   }
+  k_stage_in<<<8, 256, 0, s>>>(sl);
+  check_launch("k_stage_in");
+  ++c->launches;
   ck(cudaEventRecord(c->stage_free, s), "event");
   c->delta_ready = true;
   c->delta_version = c->dirty_version;
@@ -2009,7 +2015,12 @@ int pos_delta_copy_ex(pos_ctx* c, void* stream, int stw_end_slot, uint64_t* pack
     // (TMA and SIMT gathers both run ~3x slower while the copy engine drains: measured)
     if (n) launch_copy(c, c->d_delta_items.p, nullptr, n, c->delta_aligned, s);
     c->timer_end(kTimDelta, s);
-    if (stw_end_slot >= 0) ck(cudaEventRecord(c->events[stw_end_slot], s), "event");
+    if (stw_end_slot >= 0) {
+      ck(cudaEventRecord(c->events[stw_end_slot], s), "event");
+      c->d_stamps.ensure(64);
+      k_stamp<<<1, 1, 0, s>>>(c->d_stamps.p + stw_end_slot);  // device clock of the same point
+      check_launch("k_stamp");
+    }
     // After the stop: hash the gathered copy -> entry crcs + refreshed digests.
     if (n) {
       HashParams p{};
@@ -2520,6 +2531,26 @@ int pos_event_record(pos_ctx* c, uint32_t slot, void* stream) {
   return guarded([&] {
     if (!c || slot >= c->events.size()) fail(POS_E_INVALID_ARGUMENT, "bad event slot");
     ck(cudaEventRecord(c->events[slot], S(stream)), "event record");
+  });
+}
+
+int pos_stamp(pos_ctx* c, uint32_t slot, void* stream) {
+  return guarded([&] {
+    if (!c || slot >= 64) fail(POS_E_INVALID_ARGUMENT, "bad stamp slot");
+    c->d_stamps.ensure(64);
+    k_stamp<<<1, 1, 0, S(stream)>>>(c->d_stamps.p + slot);
+    check_launch("k_stamp");
+  });
+}
+
+int pos_stamp_elapsed(pos_ctx* c, uint32_t a, uint32_t b, float* ms) {
+  return guarded([&] {
+    if (!c || !ms || a >= 64 || b >= 64) fail(POS_E_INVALID_ARGUMENT, "bad stamp slot");
+    if (!c->d_stamps.p) fail(POS_E_BAD_STATE, "no stamps");
+    ck(cudaDeviceSynchronize(), "sync");
+    unsigned long long t[64];
+    ck(cudaMemcpy(t, c->d_stamps.p, sizeof t, cudaMemcpyDeviceToHost), "stamps");
+    *ms = (float)((double)((long long)(t[b] - t[a])) * 1e-6);
   });
 }
 

@@ -524,6 +524,15 @@ class DumpEngine:
         check(lib().pos_event_elapsed(self.ctx, a, b, C.byref(ms)))
         return ms.value
 
+    def stamp(self, slot: int, stream=None) -> None:
+        """globaltimer stamp in stream order (pos_stamp)."""
+        check(lib().pos_stamp(self.ctx, slot, _s(stream)))
+
+    def stamp_elapsed(self, a: int, b: int) -> float:
+        ms = C.c_float(0)
+        check(lib().pos_stamp_elapsed(self.ctx, a, b, C.byref(ms)))
+        return ms.value
+
     def stream_wait_event(self, slot: int, stream=None) -> None:
         check(lib().pos_stream_wait_event(self.ctx, slot, _s(stream)))
 

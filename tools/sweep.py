@@ -21,7 +21,7 @@ for spec in sys.argv[1:]:
         print(f"{spec!r}: FAILED rc={p.returncode} {p.stderr[-800:]}", flush=True)
         continue
     r = json.loads(line)
-    out = {"value": r["value"], "ms": r["ms_per_step"], "stw": r.get("stw_ms"),
+    out = {"value": r["value"], "ms": r["ms_per_step"], "stw": r.get("stw_ms"), "stw_dev": r.get("stw_device_clock_ms"),
            "e2e": r.get("e2e", {}).get("value"), "frac": r.get("roofline", {}).get("frac"),
            "stages": r.get("stages_ms"), "link": r.get("host_link", {}).get("frac")}
     print(f"{spec!r}: {json.dumps(out)}", flush=True)
