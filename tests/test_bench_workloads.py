@@ -1,0 +1,46 @@
+"""CPU: the bench's synthetic workloads have the shapes BASELINE.json names
+and are deterministic per epoch."""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_c1_shape_and_dirty_fraction():
+    wl = bench.Workload("c1")
+    assert wl.sizes == [16 << 20] * 64 and wl.total == 1 << 30
+    w = wl.epoch_writes(3)
+    assert len(w) == (1 << 30) // bench.CHUNK // 10  # 10 % of the chunks
+    assert len({(h, o) for h, o, _, _ in w}) == len(w)  # distinct chunks
+    assert all(n == bench.CHUNK and o % bench.CHUNK == 0 for _, o, n, _ in w)
+    assert w == wl.epoch_writes(3) and w != wl.epoch_writes(4)
+
+
+def test_c2_trace_is_the_reference_resnet_desk():
+    wl = bench.Workload("c2")
+    assert len(wl.sizes) == 224 and wl.total == 100_000_000
+    assert len(wl.params) > 0 and wl.window(1)
+    hs = {h for k in wl.window(1) for h, _ in k}
+    assert hs and all(1 <= h <= 224 for h in hs)
+
+
+@pytest.mark.parametrize("name,total", [("c3", 112_423_657_472), ("c4", 40_000_000_000),
+                                        ("c5", 120_000_000_000)])
+def test_large_states(name, total):
+    wl = bench.Workload(name)
+    assert wl.total == total and wl.window(1) == []
+    w = wl.epoch_writes(1)
+    if name == "c4":  # 256 sequences append one 32 KiB block per layer tensor
+        assert len(w) == 256 * 64 and all(n == 32768 for _, _, n, _ in w)
+        assert sum(n for _, _, n, _ in w) / total < 0.02
+    else:  # an optimizer step rewrites every tensor
+        assert sum(n for _, _, n, _ in w) == total
+
+
+def test_aggregate_value_is_whole_job():
+    assert bench.aggregate_value(8, 100_000_000, 1.0) == pytest.approx(800.0)
