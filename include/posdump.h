@@ -205,11 +205,16 @@ int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, v
  * (and unpinned at pos_ctx_destroy).  Re-register after pos_register_buffers. */
 int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n);
 /* Pre-copy straight into the registered image: per wave (<= 16 groups of
- * whole buffers) hash -> O1 -> scan on ckpt_stream, then every eligible chunk
- * is stored by SMs over PCIe into its place in the image on drain_stream
- * (k_copy_host, zero copy) -- no compaction pass, no host round trip, no
- * host-side apply.  The cache keeps an index-only POSD pack per wave (header
- * + entries, flag 2).  Asynchronous: returns after enqueueing. */
+ * whole buffers) hash -> O1 -> scan on ckpt_stream; the host leg then moves
+ * every eligible chunk to its place in the image on drain_stream.  Host leg
+ * (POSDUMP_DIRECT_DRAIN): "ce" (default) -- the scan writes maximal runs of
+ * shipped chunks into mapped pinned memory and the copy engine moves them
+ * (cudaMemcpyBatchAsync); the call returns once every wave's runs are
+ * submitted (it waits for each wave's scan, not for the copies).  "queue" --
+ * the hash pushes chunks to a ship queue drained by SM stores while hashing
+ * continues; "sm" -- SM stores after each scan; both return after
+ * enqueueing.  No compaction pass, no host-side apply; the cache keeps an
+ * index-only POSD pack per wave (header + entries, flag 2). */
 int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                        void* drain_stream);
 /* Chunks and payload bytes the last pos_precopy_direct shipped, and the end
@@ -220,8 +225,9 @@ int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_
  * exited, watchdog error, current sequence, 8 debug words}. */
 int pos_debug_ship_queue(pos_ctx* ctx, uint64_t* out14);
 /* After pos_delta_copy with an image registered: the delta pack's payload
- * (already in the cache -- the stop is over) stored into the image on
- * `stream` by k_copy_host. */
+ * (already in the cache -- the stop is over) moved into the image on
+ * `stream`: copy-engine runs merged where both sides are contiguous (default),
+ * or k_copy_host in the SM drain modes. */
 int pos_delta_drain(pos_ctx* ctx, void* stream);
 
 /* ---- CoW staging (gate_cow / stage_buffers, cr.hpp:806-888) ------------- */

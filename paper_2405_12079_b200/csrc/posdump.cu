@@ -390,6 +390,16 @@ void check_launch(const char* what) {
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
+// cudaMemcpyBatchAsync flags of the host leg (POSDUMP_CE_OVERLAP=1: prefer
+// overlap with compute).
+unsigned int ce_flags() {
+  static const unsigned int f = [] {
+    const char* e = std::getenv("POSDUMP_CE_OVERLAP");
+    return (e && e[0] == '1') ? (unsigned int)cudaMemcpyFlagPreferOverlapWithCompute : 0u;
+  }();
+  return f;
+}
+
 // Host leg of the direct pre-copy: 0 copy-engine runs, 1 SM ship queue, 2 SM after each scan.
 int direct_drain_mode() {
   static const int m = [] {
@@ -1644,6 +1654,7 @@ int pos_precopy_direct(pos_ctx* c, int exclude_dag_dirty, uint32_t waves, void* 
       attr.srcLocHint.type = cudaMemLocationTypeDevice;
       attr.srcLocHint.id = c->cfg.device;
       attr.dstLocHint.type = cudaMemLocationTypeHost;
+      attr.flags = ce_flags();
       for (uint32_t w = 0; w < W; ++w) {
         pack_result(c, w);
         const uint64_t nr = c->h_scan.p[8 * w + 7];
@@ -1749,6 +1760,7 @@ int pos_delta_drain(pos_ctx* c, void* stream) {
       attr.srcLocHint.type = cudaMemLocationTypeDevice;
       attr.srcLocHint.id = c->cfg.device;
       attr.dstLocHint.type = cudaMemLocationTypeHost;
+      attr.flags = ce_flags();
       size_t zero = 0, fail_idx = 0;
       const uint64_t r = c->drun_n;
       ck(cudaMemcpyBatchAsync(reinterpret_cast<void**>(c->h_drun.p + r), reinterpret_cast<void**>(c->h_drun.p),
