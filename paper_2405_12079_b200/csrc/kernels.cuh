@@ -152,6 +152,12 @@ constexpr uint32_t kSmallTablesBytes = 6 * 4096;
 // window (which begins at the ~1 KiB reserved offset).
 constexpr uint32_t kRepAbs = 0x10000;
 constexpr uint32_t kHashSmem = 0x30000;
+// kTma variant: 16 x 4 KiB TMA slots -- 8 in the gap below the replicated
+// table (after the small tables, the Z^512 source and the mbarriers), 8 after
+// it -- and one mbarrier per warp.
+constexpr uint32_t kTmaBarOff = kSmallTablesBytes + 4096 + 64;  // 16 x 8 B
+constexpr uint32_t kTmaSlotLoOff = 0x7400;                       // 29 KiB
+constexpr uint32_t kHashSmemTma = 0x38000;
 
 // ---------------------------------------------------------------------------
 // Load helpers.
@@ -198,6 +204,48 @@ __device__ __forceinline__ uint4 load_masked(uint64_t a0, uint64_t blk, int lane
   return make_uint4(w0, w1, w2, w3);
 }
 
+// TMA / mbarrier helpers (also used by the bulk copy engine below).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // CRC advance operators.
 //
@@ -235,12 +283,21 @@ __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
 // with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
 // which leaves a register that starts at 0 unchanged.  COPY: every loaded
 // vector is also stored at dst (only when src is 16-B aligned).
-template <bool COPY, int kUnroll, bool kRoll>
+// TMA stage of the three-stage pipeline (kTma): a 4 KiB shared-memory slot
+// per warp filled by cp.async.bulk, beside the two register batches.
+struct TmaStage {
+  uint8_t* slot;      // kUnroll * 512 bytes, 128-B aligned
+  uint64_t* bar;      // this warp's mbarrier
+  uint32_t* phase;    // its parity (persists across chunks)
+};
+
+template <bool COPY, int kUnroll, bool kRoll, bool kTma = false>
 __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
                                                const uint32_t* xinv, uint32_t lsel, int lane,
                                                uint64_t src, uint64_t len, uint32_t k_len,
                                                uint8_t* dst, bool pf = kL2Prefetch,
-                                               uint32_t pf_steps = kPrefetchSteps) {
+                                               uint32_t pf_steps = kPrefetchSteps,
+                                               TmaStage tma = TmaStage{nullptr, nullptr, nullptr}) {
   const uint64_t a0 = src & ~15ull;
   const uint64_t lead = src - a0;
   const uint64_t end = lead + len;
@@ -329,6 +386,56 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
     }
     blk = full_end;
   }
+  if (kTma && !COPY && blk + 3 * kUnroll <= full_end) {
+    // Three-stage pipeline: batches rotate through register buffers A, B and
+    // the warp's shared-memory slot S (filled by one TMA bulk copy), so two
+    // batches (8 KiB) are in flight while the third is hashed -- twice the
+    // register-only ping-pong, without more registers.
+    uint4 bufA[kUnroll], bufB[kUnroll];
+    const uint64_t nb = (full_end - blk) / kUnroll;
+    constexpr uint32_t kBatchBytes = kUnroll * kStepBytes;
+    auto tma_issue = [&](uint64_t batch) {
+      if (lane == 0) {
+        // the slot's earlier generic-proxy reads before this async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(tma.bar, kBatchBytes);
+        bulk_g2s(tma.slot, reinterpret_cast<const void*>(a0 + (blk + batch * kUnroll) * kStepBytes),
+                 kBatchBytes, tma.bar);
+      }
+    };
+    auto run_slot = [&]() {
+      mbar_wait(tma.bar, *tma.phase & 1u);
+      *tma.phase ^= 1u;
+      const uint32_t sa = smem_addr(tma.slot) + lane * 16;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(sa + u * kStepBytes));
+        c0 = adv512(lsel, c0 ^ v.x);
+        c1 = adv512(lsel, c1 ^ v.y);
+        c2 = adv512(lsel, c2 ^ v.z);
+        c3 = adv512(lsel, c3 ^ v.w);
+      }
+      __syncwarp();  // every lane has read the slot before lane 0 refills it
+    };
+    load_batch(bufA, blk);
+    load_batch(bufB, blk + kUnroll);
+    tma_issue(2);
+    uint64_t i = 0;
+    for (; i + 3 <= nb; i += 3) {
+      run_batch(bufA, blk + i * kUnroll);
+      if (i + 3 < nb) load_batch(bufA, blk + (i + 3) * kUnroll);
+      run_batch(bufB, blk + (i + 1) * kUnroll);
+      if (i + 4 < nb) load_batch(bufB, blk + (i + 4) * kUnroll);
+      run_slot();
+      if (i + 5 < nb) tma_issue(i + 5);
+    }
+    if (i < nb) run_batch(bufA, blk + i * kUnroll);
+    if (i + 1 < nb) run_batch(bufB, blk + (i + 1) * kUnroll);
+    blk += nb * kUnroll;
+  }
   if (!kRoll && blk + kUnroll <= full_end) {
     uint4 bufA[kUnroll], bufB[kUnroll];
     load_batch(bufA, blk);
@@ -387,48 +494,6 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
   return crc;
 }
 
-// TMA / mbarrier helpers (also used by the bulk copy engine below).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(sdst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_addr(ssrc)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // Table prologue: one TMA bulk copy brings the 24 KiB of small tables and the
 // 4 KiB Z^512 source into shared memory (the per-thread __ldg loop it
 // replaces was 27 % of a 100 MB launch's stall samples: 76 dependent L2
@@ -467,16 +532,32 @@ enum : int { kModeHash = 0, kModeCopy = 1, kModeCached = 2 };
 // kModeHash: every chunk -> digest, dirty flag, bitmap bit.
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
-template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault, bool kRoll = false>
+template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault, bool kRoll = false,
+          bool kTma = false>
 // <= 120 registers: 16 warps x 3840 leave 4096 registers of the SM for the
 // drain CTAs (k_drain_queue / k_copy_host) to run beside the hash.
-__global__ void __maxnreg__(kThreads >= 512 ? 120 : (kThreads >= 384 ? 168 : 255)) k_hash_chunks(HashParams p) {
+__global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 384 ? 168 : 255)) k_hash_chunks(HashParams p) {
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
   load_hash_tables(smem, p.tables);
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
+  uint32_t tma_phase = 0;
+  TmaStage tma{nullptr, nullptr, &tma_phase};
+  if (kTma) {
+    const int wi = threadIdx.x >> 5;
+    const uint32_t sbase = smem_addr(smem);
+    const uint32_t hi_off = (kRepAbs - sbase) + 0x20000;  // just past the replicated table
+    tma.slot = smem + (wi < 8 ? kTmaSlotLoOff + wi * 4096u : hi_off + (wi - 8) * 4096u);
+    tma.bar = reinterpret_cast<uint64_t*>(smem + kTmaBarOff) + wi;
+    if (lane == 0) {
+      if (kTmaSlotLoOff + 8 * 4096u > kRepAbs - sbase || hi_off + 8 * 4096u > kHashSmemTma) __trap();
+      mbar_init(tma.bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   const uint32_t lsel = (uint32_t)lane * 4 | kRepAbs;
   // nseg == 1: item i goes to CTA i % grid, warp (i / grid) % W, so a short
   // list still spreads over every SM.  nseg > 1: the nseg segments of a chunk
@@ -531,9 +612,9 @@ __global__ void __maxnreg__(kThreads >= 512 ? 120 : (kThreads >= 384 ? 168 : 255
       for (uint64_t q = pa + (uint64_t)lane * 16384; q < pe; q += 32 * 16384)
         l2_prefetch(reinterpret_cast<const void*>(q), (uint32_t)(pe - q < 16384 ? pe - q : 16384));
     }
-    const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll>(small, p.xinv, lsel, lane, src + lo, n,
-                                            p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr,
-                                            p.pf_bytes == 1, (uint32_t)p.pad3)
+    const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll, kTma>(small, p.xinv, lsel, lane, src + lo, n,
+                                                  p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr,
+                                                  p.pf_bytes == 1, (uint32_t)p.pad3, tma)
                          : 0u;
     if (nseg == 1) {
       crc = r;

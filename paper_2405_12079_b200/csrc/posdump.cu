@@ -102,7 +102,7 @@ struct PinnedArray {
 
 // Hash kernel variants (threads per CTA x warp steps per batch); one CTA per
 // SM either way.  POSDUMP_HASH_CFG selects one for tuning runs.
-enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12, kCfg512r12, kCfg512r16, kCfg256r24 };
+enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12, kCfg512r12, kCfg512r16, kCfg256r24, kCfg512t6 };
 
 HashCfg hash_cfg() {
   static const HashCfg c = [] {
@@ -113,6 +113,7 @@ HashCfg hash_cfg() {
     if (!std::strcmp(e, "512r12")) return kCfg512r12;
     if (!std::strcmp(e, "512r16")) return kCfg512r16;
     if (!std::strcmp(e, "256r24")) return kCfg256r24;
+    if (!std::strcmp(e, "512t6")) return kCfg512t6;
     return kCfg512x8;
   }();
   return c;
@@ -135,6 +136,7 @@ void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
     case kCfg512r12: k_hash_chunks<COPY, 512, 12, true><<<grid, 512, kHashSmem, s>>>(p); break;
     case kCfg512r16: k_hash_chunks<COPY, 512, 16, true><<<grid, 512, kHashSmem, s>>>(p); break;
     case kCfg256r24: k_hash_chunks<COPY, 256, 24, true><<<grid, 256, kHashSmem, s>>>(p); break;
+    case kCfg512t6: k_hash_chunks<COPY, 512, 6, false, true><<<grid, 512, kHashSmemTma, s>>>(p); break;
     default: k_hash_chunks<COPY, 512, 8><<<grid, 512, kHashSmem, s>>>(p); break;
   }
 }
@@ -147,6 +149,8 @@ void set_hash_smem() {
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
   ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
+  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 6, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kHashSmemTma), "smem attr");
 }
 
 // Tables shared by every launch on a device: Z^512 (replicated in smem by the
