@@ -398,7 +398,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # direct mode: the drain kernel (k_copy_host) must win SM slots over queued
     # application blocks too, so its stream shares the dump's priority
     ckpt, app = pd.Stream(priority=args.ckpt_priority), pd.Stream()
-    copy = pd.Stream(priority=args.ckpt_priority if args.mode == "direct" else 0)
+    copy = pd.Stream(priority=args.drain_priority if args.drain_priority >= 0 else
+                     (args.ckpt_priority if args.mode == "direct" else 0))
     by_handle = {b.handle: b for b in bufs}
 
     class AppThread:
@@ -843,6 +844,7 @@ def main():
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
     ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")
+    ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
     ap.add_argument("--peer-cache-gb", type=float, default=0.0,
                     help="c3: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
     args = ap.parse_args()

@@ -197,7 +197,7 @@ int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, v
                           void* copy_stream, void* host_dst, uint64_t slice_bytes,
                           uint64_t* offsets, uint64_t* sizes, uint32_t* n_packs);
 
-/* ---- direct pre-copy into the host image (zero-copy chunk_copied) ------ */
+/* ---- direct pre-copy into the host image (chunk_copied, no host copy) -- */
 /* The checkpoint target's image of captured_ (cr.hpp:499-501, the byte
  * vectors chunk_copied writes at ci * chunk_size): hosts[i] / sizes[i] is the
  * host copy of registered buffer i (ascending handle; sizes must match).
