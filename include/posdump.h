@@ -375,6 +375,22 @@ typedef struct pos_image_desc {
  * size; bytes are written when cap >= size. */
 int pos_image_write(const pos_image_desc* img, uint8_t* out, uint64_t cap, uint64_t* size);
 
+/* read_image (image.hpp:209-361): validate a POSI image on the host -- the
+ * reference's checks in its order; POS_E_CORRUPT_IMAGE with the reader
+ * offset of its CorruptImageError in *corrupt_offset.  The DAG section is
+ * opaque here (its structure belongs to the kernel DAG): a corrupt DAG body,
+ * and recompute nodes missing from a non-empty DAG, are not detected. */
+int pos_image_check(const uint8_t* img, uint64_t size, uint64_t* corrupt_offset);
+/* Restore from a POSI image (read_image + install/materialize, cr.hpp:
+ * 1026-1030, dedup_content image.hpp:364-376): validate it (nothing is
+ * written from a corrupt image), then every Inline / DedupRef record of a
+ * registered buffer is copied H2D on `stream` (DedupRef assembled from the
+ * image's host pages and its checksum verified on the device); Recompute
+ * records are left to delta-restore replay (cr.hpp:1099-1119).  Registered
+ * buffers must have the image's allocation sizes (POS_E_INVALID_LOCATOR). */
+int pos_image_restore(pos_ctx* ctx, const uint8_t* img, uint64_t size, void* stream, uint64_t* corrupt_offset,
+                      uint32_t* n_loaded, uint32_t* n_recompute);
+
 /* ---- plumbing (device memory / streams for hosts without their own) ---- */
 int pos_device_count(int* n);
 int pos_set_device(int device);

@@ -113,6 +113,8 @@ SIGNATURES = {
     "pos_precopy_pipelined": [P, I32, U32, P, P, P, U64, P, P, P],
     "pos_precopy_stream": [P, I32, P, P, U64, P, P, PU64, PU32],
     "pos_register_image": [P, P, P, U32],
+    "pos_image_check": [P, U64, PU64],
+    "pos_image_restore": [P, P, U64, P, PU64, PU32, PU32],
     "pos_peer_cache_attach": [P, I32, U64],
     "pos_peer_cache_stats": [P, C.POINTER(C.c_float), C.POINTER(C.c_float)],
     "pos_h2d_provenance": [P, U64, P, U64, I32, P],
@@ -199,12 +201,17 @@ def load() -> C.CDLL:
     return lib
 
 
+def error_from(rc: int) -> SimError:
+    """The exception for return code rc (with pos_last_error's message)."""
+    msg = load().pos_last_error().decode(errors="replace")
+    if rc == CODES["CorruptImage"]:
+        return CorruptImageError(rc, msg)
+    if rc == POS_E_NO_DEVICE:
+        return NoDeviceError(rc, msg)
+    return SimError(rc, msg)
+
+
 def check(rc: int) -> None:
     if rc == POS_OK:
         return
-    msg = load().pos_last_error().decode(errors="replace")
-    if rc == CODES["CorruptImage"]:
-        raise CorruptImageError(rc, msg)
-    if rc == POS_E_NO_DEVICE:
-        raise NoDeviceError(rc, msg)
-    raise SimError(rc, msg)
+    raise error_from(rc)

@@ -25,6 +25,7 @@
 #include "crc_math.h"
 #include "kernels.cuh"
 #include "image_writer.h"
+#include "image_reader.h"
 
 using namespace posdump;
 

@@ -487,6 +487,19 @@ class DumpEngine:
         check(lib().pos_restore_packs(self.ctx, ptrs, sizes.ctypes.data, n, _s(h2d_stream), _s(stream),
                                       region_bytes))
 
+    # ---- restore from a POSI image (read_image + materialize)
+    def restore_image(self, data: bytes, stream=None) -> tuple[int, int]:
+        """Returns (records loaded, recompute records left to replay)."""
+        buf = np.frombuffer(bytes(data), np.uint8)
+        off, nl, nr = C.c_uint64(0), C.c_uint32(0), C.c_uint32(0)
+        rc = lib().pos_image_restore(self.ctx, buf.ctypes.data if buf.size else None, buf.size, _s(stream),
+                                     C.byref(off), C.byref(nl), C.byref(nr))
+        if rc != 0:
+            err = _lib.error_from(rc)
+            err.offset = off.value
+            raise err
+        return nl.value, nr.value
+
     # ---- on-demand restore of a flat host image (restore / gate_restore, cr.hpp:167-204, 1043-1143)
     def restore_image_begin(self, hosts: Sequence[np.ndarray], order: Sequence[int] = (), slice_bytes: int = 0,
                             h2d_stream=None) -> None:
@@ -581,6 +594,19 @@ class CheckpointImage:
     cursor: int = 0
     next_handle: int = 1
     next_base: int = kDeviceAddrBase
+
+
+def read_image_check(data: bytes) -> int:
+    """read_image's validation (image.hpp:209-361) on the host: 0 if valid,
+    else raises CorruptImageError whose .offset is the reference's offset."""
+    buf = np.frombuffer(bytes(data), np.uint8)
+    off = C.c_uint64(0)
+    rc = lib().pos_image_check(buf.ctypes.data if buf.size else None, buf.size, C.byref(off))
+    if rc != 0:
+        err = _lib.error_from(rc)
+        err.offset = off.value
+        raise err
+    return 0
 
 
 def write_image(img: CheckpointImage) -> bytes:

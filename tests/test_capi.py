@@ -157,3 +157,53 @@ def test_pack_apply_host_matches_oracle(orc):
     bad[:4] = 0
     with pytest.raises(pd.CorruptImageError):
         pd.apply_pack_host(bad, [h for h, _ in bufs], [np.zeros_like(a) for _, a in bufs])
+
+
+def _ours_check(data: bytes) -> int:
+    """0 if valid, else 1 + the CorruptImageError offset (ref_read_image_check's encoding)."""
+    try:
+        pd.read_image_check(data)
+        return 0
+    except pd.CorruptImageError as e:
+        return 1 + e.offset
+
+
+def test_read_image_check_matches_reference(orc, ref):
+    """read_image (image.hpp:209-361): on 300 writer-generated images (no DAG:
+    its body is opaque to us) and ~4000 corruptions of them -- byte flips,
+    truncations, appended bytes -- our validator accepts exactly what the
+    reference accepts and reports the same CorruptImageError offset."""
+    from oracle_ctypes import ref_image
+    rng = np.random.default_rng(77)
+    n_valid = n_checked = 0
+    for _ in range(300):
+        d = _random_desc(rng)
+        d["dag"] = ""
+        if rng.random() < 0.5:  # make the dedup checksums right so some images are valid
+            for r in d["recs"]:
+                if r["kind"] == 1:
+                    r["page_count"] = 1
+                    r["first_page"] = 0
+                    r["offset"] = 0
+            d["pages"] = [(0, 99)] + [p for p in d["pages"] if p[0] != 0]
+            d["pages"].sort()
+        data = ref_image(ref, d)
+        cases = [data]
+        for _ in range(12):
+            b = bytearray(data)
+            k = int(rng.integers(0, 3))
+            if k == 0 and b:
+                i = int(rng.integers(0, len(b)))
+                b[i] ^= 1 << int(rng.integers(0, 8))
+            elif k == 1 and b:
+                del b[int(rng.integers(0, len(b))):]
+            else:
+                b += bytes(rng.integers(0, 256, int(rng.integers(1, 9)), dtype=np.uint8))
+            cases.append(bytes(b))
+        for c in cases:
+            buf = np.frombuffer(c, np.uint8)
+            want = ref.ref_read_image_check(buf.ctypes.data if buf.size else None, buf.size)
+            assert _ours_check(c) == want, (d, len(c))
+            n_valid += want == 0
+            n_checked += 1
+    assert n_valid > 50 and n_checked > 3500

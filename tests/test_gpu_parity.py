@@ -977,3 +977,52 @@ def test_direct_tiled_scan_many_tiles(orc):
         prev = dig
         eng.commit_epoch()
     eng.close()
+
+
+@pytest.mark.parametrize("profile,seed,mode", [("gpt2-infer-desk", 1, 3), ("resnet-train-desk", 1, 3)])
+def test_restore_from_reference_image(orc, ref, profile, seed, mode):
+    """Restore from a POSI image the reference's CrEngine wrote (read_image +
+    materialize, cr.hpp:1026-1030; dedup_content image.hpp:364-376): every
+    Inline / DedupRef buffer lands byte for byte on the device, Recompute
+    records are left to replay, and a corrupted copy of the image is rejected
+    with the reference's offset before anything is written."""
+    import ctypes as C
+    from posi import dedup_bytes, read_posi
+    n = ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, None, 0)
+    buf = C.create_string_buffer(n)
+    ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, buf, n)
+    data = buf.raw[:n]
+    img = read_posi(data)
+    allocs = {h: size for h, base, size in img["meta"]["allocs"]}
+    mems, bufs, want = [], [], {}
+    for h in sorted(allocs):
+        m = pd.DeviceMemory(allocs[h])
+        pd.check(pd.lib().pos_memset(m.ptr, 0, allocs[h], None))
+        mems.append(m)
+        bufs.append(pd.GpuBuffer(handle=h, dev_ptr=m.ptr, size=allocs[h]))
+    for r in img["recs"]:
+        if r["kind"] == 0:
+            want[r["handle"]] = r["inline"]
+        elif r["kind"] == 1:
+            want[r["handle"]] = dedup_bytes(img, r, allocs[r["handle"]])
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=8 << 20))
+    eng.register_buffers(bufs)
+    # corrupt copy first: rejected with the reference's offset, nothing written
+    bad = bytearray(data)
+    bad[len(bad) // 2] ^= 0x40
+    wbad = np.frombuffer(bytes(bad), np.uint8)
+    code = ref.ref_read_image_check(wbad.ctypes.data, wbad.size)
+    if code:
+        with pytest.raises(pd.CorruptImageError) as ei:
+            eng.restore_image(bytes(bad))
+        assert ei.value.offset == code - 1
+        for m in mems:
+            assert not m.download().any()
+    loaded, recompute = eng.restore_image(data)
+    assert loaded == len(want)
+    assert recompute == sum(1 for r in img["recs"] if r["kind"] == 2)
+    by_h = {b.handle: m for b, m in zip(bufs, mems)}
+    for h, content in want.items():
+        assert by_h[h].download().tobytes() == bytes(content), h
+    eng.close()
