@@ -382,10 +382,10 @@ int pos_image_write(const pos_image_desc* img, uint8_t* out, uint64_t cap, uint6
  * and recompute nodes missing from a non-empty DAG, are not detected. */
 int pos_image_check(const uint8_t* img, uint64_t size, uint64_t* corrupt_offset);
 /* Restore from a POSI image (read_image + install/materialize, cr.hpp:
- * 1026-1030, dedup_content image.hpp:364-376): validate it (nothing is
- * written from a corrupt image), then every Inline / DedupRef record of a
- * registered buffer is copied H2D on `stream` (DedupRef assembled from the
- * image's host pages and its checksum verified on the device); Recompute
+ * 1026-1030, dedup_content image.hpp:364-376): validate it in full (dedup
+ * checksums included -- nothing is written from a corrupt image), then every
+ * Inline / DedupRef record of a registered buffer is copied H2D on `stream`
+ * (DedupRef assembled from the image's host pages); Recompute
  * records are left to delta-restore replay (cr.hpp:1099-1119).  Registered
  * buffers must have the image's allocation sizes (POS_E_INVALID_LOCATOR). */
 int pos_image_restore(pos_ctx* ctx, const uint8_t* img, uint64_t size, void* stream, uint64_t* corrupt_offset,
