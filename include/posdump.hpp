@@ -64,6 +64,12 @@ class SimError : public std::runtime_error {  // errors.hpp:48-56
 class CorruptImageError : public SimError {  // errors.hpp:59-68
  public:
   explicit CorruptImageError(const std::string& what) : SimError(Errc::CorruptImage, what) {}
+  CorruptImageError(uint64_t offset, const std::string& what)
+      : SimError(Errc::CorruptImage, what), offset_(offset) {}
+  uint64_t offset() const { return offset_; }
+
+ private:
+  uint64_t offset_ = 0;
 };
 
 inline void check(int rc) {
@@ -271,6 +277,22 @@ class DumpEngine {
   void gate_restore(BufferHandle h, void* stream) { check(pos_restore_gate(ctx_, h, stream)); }
   void restore_wait() { check(pos_restore_image_wait(ctx_)); }
 
+  // read_image + materialize (image.hpp:209-361, cr.hpp:1026-1030): restore a
+  // POSI image onto the snapshot's buffers; returns (loaded, recompute).
+  std::pair<uint32_t, uint32_t> restore_image(const std::vector<uint8_t>& posi, void* stream = nullptr) {
+    uint64_t off = 0;
+    uint32_t loaded = 0, recompute = 0;
+    int rc = pos_image_restore(ctx_, posi.data(), posi.size(), stream, &off, &loaded, &recompute);
+    if (rc == POS_E_CORRUPT_IMAGE) throw CorruptImageError(off, pos_last_error());
+    check(rc);
+    return {loaded, recompute};
+  }
+
+  // NVLink peer-GPU cache for the cache-cycled pre-copy (config 5).
+  void attach_peer_cache(int peer_device, uint64_t bytes) {
+    check(pos_peer_cache_attach(ctx_, peer_device, bytes));
+  }
+
   // finalize_image's written_since_ckpt = false (cr.hpp:745): next epoch compares here.
   void end_checkpoint_session() {
     check(pos_commit_epoch(ctx_));
@@ -354,6 +376,15 @@ struct CheckpointImage {
 };
 
 // Byte-identical to gpucrsim::write_image (streaming, no deep copy).
+// read_image's validation (image.hpp:209-361): throws CorruptImageError with
+// the reference's offset.  (The DAG body is opaque to this reader.)
+inline void read_image_check(const std::vector<uint8_t>& posi) {
+  uint64_t off = 0;
+  int rc = pos_image_check(posi.data(), posi.size(), &off);
+  if (rc == POS_E_CORRUPT_IMAGE) throw CorruptImageError(off, pos_last_error());
+  check(rc);
+}
+
 inline std::vector<uint8_t> write_image(const CheckpointImage& img) {
   std::vector<pos_image_page> pages;
   for (const auto& p : img.host_pages) {

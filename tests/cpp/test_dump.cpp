@@ -339,3 +339,18 @@ TEST_CASE("[gpu] H2D provenance records crc32 of the payload and dedups the buff
   PackRef pre = e.plan_precopy();
   REQUIRE(pack_entries(pinned_d2h(e, pre)) == 0u);  // O1: nothing to ship
 }
+
+TEST_CASE("[cpu] read_image rejects a truncated image at the reference's offset") {  // image.hpp:209-230
+  CheckpointImage img;
+  std::vector<uint8_t> bytes = write_image(img);
+  read_image_check(bytes);  // the 64-byte empty image is valid
+  bytes.resize(10);
+  bool threw = false;
+  try {
+    read_image_check(bytes);
+  } catch (const CorruptImageError& e) {
+    threw = true;
+    REQUIRE(e.offset() == 8u);  // flags u16 read at 6..8 succeeds; n_pages u32 at 8 is truncated
+  }
+  REQUIRE(threw);
+}
