@@ -19,8 +19,10 @@ def _run(tag):
 
 
 def test_cpp_suite_cpu_cases():
+    import re
     out = _run("[cpu]")
-    assert "5/5 passed" in out
+    m = re.search(r"(\d+)/(\d+) passed", out)
+    assert m and m.group(1) == m.group(2) and int(m.group(2)) >= 6, out
 
 
 @pytest.mark.gpu
