@@ -148,6 +148,48 @@ def test_chunk_digests_and_epoch_bitmap(orc, cs):
     eng.close()
 
 
+def _digest_layout(kind):
+    rng = np.random.default_rng(hash(kind) & 0xFFFF)
+    if kind == "tiny512":      # 1-6 warp steps per chunk
+        return 512, [int(x) for x in rng.integers(1, 3000, 200)]
+    if kind == "mixed64k":     # ResNet-like mix: scalars, tails, multi-chunk buffers
+        return 65536, [int(x) for x in rng.integers(1, 4 << 20, 40)] + [1, 4, 65536, 65537, 3 * 65536]
+    if kind == "big1m":        # 1 MiB chunks: few chunks, segmented over warps
+        return 1 << 20, [4 << 20, (1 << 20) + 3, 7, (3 << 20) - 100, 2 << 20]
+    if kind == "many4k":       # one 64 MiB buffer of 4 KiB chunks: many rounds per warp
+        return 4096, [64 << 20]
+    if kind == "sparse2k":     # 2 KiB chunks over 300 small buffers
+        return 2048, [int(x) for x in rng.integers(1, 5000, 300)]
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["tiny512", "mixed64k", "big1m", "many4k", "sparse2k"])
+def test_chunk_digest_layouts(orc, kind):
+    """The O2 hash gives the reference's chunk digests (chunk_digests,
+    buffer.hpp:117-128) for chunk/buffer layouts from 1-step chunks over
+    hundreds of buffers to 1 MiB chunks (segmented across warps), epoch after
+    epoch."""
+    cs, sizes = _digest_layout(kind)
+    p = Proc(orc, sizes)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    rng = np.random.default_rng(5)
+    for epoch in range(3):
+        if epoch:
+            for _ in range(8):
+                i = int(rng.integers(0, len(sizes)))
+                off = int(rng.integers(0, sizes[i]))
+                p.write(i, off, int(min(sizes[i] - off, rng.integers(1, 3 * cs))), 700 + epoch * 10 + i)
+            pd.device_synchronize()
+        eng.hash_chunks()
+        want = np.concatenate([odigests(orc, h, cs) for h in p.host])
+        got = eng.digests()
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (kind, epoch, bad[:10], got.size)
+        eng.commit_epoch()
+    eng.close()
+
+
 @pytest.mark.parametrize("cs", [4096, 65536])
 def test_unaligned_buffers(orc, cs):
     p = Proc(orc, [5000, 12345, 3, 3 * cs + 77], offsets=[1, 7, 13, 5])

@@ -74,7 +74,7 @@ float run(const uint8_t* d, uint64_t bytes, uint64_t cb, int blocks, int threads
   return bytes / (best * 1e-3) / 1e9;
 }
 
-int main() {
+int main(int argc, char** argv) {
   const uint64_t bytes = 1ull << 30;
   uint8_t *d, *flush;
   uint32_t* out;
@@ -84,6 +84,21 @@ int main() {
   cudaMemset(d, 1, bytes);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // balanced split: ~100 MB as one piece per warp (16 warps/SM) vs 64 KiB chunks
+    const uint64_t steps = 83, cb = steps * 512, n = (uint64_t)sms * 16;
+    printf("100MB 64K chunks (10.3 warps/SM)  U4 %7.1f U8 %7.1f U12 %7.1f\n",
+           run<4, 0>(d, 1526ull * 65536, 65536, sms, 512, out, flush), run<8, 0>(d, 1526ull * 65536, 65536, sms, 512, out, flush),
+           run<12, 0>(d, 1526ull * 65536, 65536, sms, 512, out, flush));
+    printf("100MB %llu x 42.5K pieces (16 warps/SM) U4 %7.1f U8 %7.1f U12 %7.1f\n", (unsigned long long)n,
+           run<4, 0>(d, n * cb, cb, sms, 512, out, flush), run<8, 0>(d, n * cb, cb, sms, 512, out, flush),
+           run<12, 0>(d, n * cb, cb, sms, 512, out, flush));
+    printf("100MB %llu x 42.5K pieces (8 warps/SM, 2 CTA) U8 %7.1f\n", (unsigned long long)n,
+           run<8, 0>(d, n * cb, cb, 2 * sms, 256, out, flush));
+    printf("1GiB 64K chunks U8 %7.1f   1GiB balanced (16 w/SM) U8 %7.1f\n",
+           run<8, 0>(d, bytes, 65536, sms, 512, out, flush),
+           run<8, 0>(d, bytes / (n * 512) * n * 512, bytes / (n * 512) * 512, sms, 512, out, flush));
+    return 0;
+  }
   for (int thr : {256, 512}) {
     printf("100MB 64K chunks %d thr U8: pf0 %7.1f pf1 %7.1f pf2 %7.1f pf3 %7.1f\n", thr,
            run<8, 0>(d, 1526ull * 65536, 65536, sms, thr, out, flush), run<8, 1>(d, 1526ull * 65536, 65536, sms, thr, out, flush),
