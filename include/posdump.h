@@ -255,6 +255,14 @@ int pos_delta_copy(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* 
  * of the stop-the-world window. */
 int pos_delta_copy_ex(pos_ctx* ctx, void* stream, int stw_end_slot, uint64_t* pack_offset,
                       uint64_t* pack_bytes);
+/* at_final_stop with the stop-the-world window delimited by the engine: on
+ * `stream`, event `stw_begin_slot`, the gather, event `stw_end_slot` -- and
+ * nothing else (each extra stream operation costs ~10 us while the copy
+ * engine writes to the host); the post-stop hash follows.  The delta timer
+ * (pos_last_kernel_ms "delta") reads the two events.  Replaces
+ * at_final_stop's copy loop, cr.hpp:599-621. */
+int pos_final_stop(pos_ctx* ctx, void* stream, int stw_begin_slot, int stw_end_slot, uint64_t* pack_offset,
+                   uint64_t* pack_bytes);
 /* Stage the delta pack's header and work list ahead of the stop (the DAG
  * write sets are known at submission, process.hpp:313-344), so the STW window
  * holds only the kernel.  pos_delta_copy re-stages if dirty_set_ or the

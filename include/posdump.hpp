@@ -217,6 +217,13 @@ class DumpEngine {
     check(pos_delta_copy(ctx_, stream, &r.offset, &r.bytes));
     return r;
   }
+  // Same, the stop-the-world window delimited by events stw_begin / stw_end
+  // and holding only the gather (pos_final_stop).
+  PackRef at_final_stop(void* stream, int stw_begin, int stw_end) {
+    PackRef r;
+    check(pos_final_stop(ctx_, stream, stw_begin, stw_end, &r.offset, &r.bytes));
+    return r;
+  }
 
   void d2h(void* pinned_dst, const PackRef& p, void* stream = nullptr) {
     check(pos_d2h_async(ctx_, pinned_dst, p.offset, p.bytes, 0, stream));

@@ -126,6 +126,7 @@ SIGNATURES = {
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_stage_buffers": [P, P, U32, P, PU64, PU64],
     "pos_delta_copy_ex": [P, P, I32, PU64, PU64],
+    "pos_final_stop": [P, P, I32, I32, PU64, PU64],
     "pos_delta_prepare": [P, P, PU64, PU64],
     "pos_d2h_async": [P, P, U64, U64, U64, P],
     "pos_cache_info": [P, PU64, PU64],

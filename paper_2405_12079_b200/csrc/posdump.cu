@@ -303,6 +303,7 @@ struct pos_ctx {
   // x^(8 * last segment length of the tail chunk); valid_levels bitmask.
   uint32_t seg_levels = 1;
   DevArray<uint32_t> d_xseg, d_lastseg;
+  int delta_slots[2] = {-1, -1};  // pos_final_stop: the STW window's events (the delta timer)
   DevArray<uint64_t> d_result;  // async pre-copy: [n, total, overflow, n_items]
   std::set<uint64_t> dirty_set;
   bool dag_uploaded = false;

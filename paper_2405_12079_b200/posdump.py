@@ -450,11 +450,16 @@ class DumpEngine:
         return off.value, n.value
 
     # ---- STW delta-copy (at_final_stop, cr.hpp:599-621)
-    def at_final_stop(self, stream=None, stw_end_slot: int = -1) -> tuple[int, int]:
-        """STW delta pack: bulk gather (records event stw_end_slot when >= 0),
-        then the post-stop hash of the gathered copy."""
+    def at_final_stop(self, stream=None, stw_end_slot: int = -1, stw_begin_slot: int = -1) -> tuple[int, int]:
+        """STW delta pack: bulk gather, then the post-stop hash of the gathered
+        copy.  With stw_begin_slot >= 0 the window is exactly [event begin,
+        gather, event end] (pos_final_stop); otherwise event stw_end_slot
+        (when >= 0) is recorded after the gather (pos_delta_copy_ex)."""
         off, n = C.c_uint64(0), C.c_uint64(0)
-        check(lib().pos_delta_copy_ex(self.ctx, _s(stream), stw_end_slot, C.byref(off), C.byref(n)))
+        if stw_begin_slot >= 0:
+            check(lib().pos_final_stop(self.ctx, _s(stream), stw_begin_slot, stw_end_slot, C.byref(off), C.byref(n)))
+        else:
+            check(lib().pos_delta_copy_ex(self.ctx, _s(stream), stw_end_slot, C.byref(off), C.byref(n)))
         return off.value, n.value
 
     def prepare_final_stop(self, stream=None) -> tuple[int, int]:

@@ -282,10 +282,12 @@ def test_compact_pack_is_bit_exact(orc, cs):
     eng.close()
 
 
-@pytest.mark.parametrize("cs,offsets", [(4096, None), (65536, None), (65536, [0, 3, 0, 9])])
-def test_delta_copy_pack_and_digests(orc, cs, offsets):
+@pytest.mark.parametrize("cs,offsets,window", [(4096, None, False), (65536, None, False),
+                                                (65536, [0, 3, 0, 9], False), (65536, [0, 3, 0, 9], True)])
+def test_delta_copy_pack_and_digests(orc, cs, offsets, window):
     """at_final_stop (cr.hpp:599-621): whole DAG-flagged buffers, after the
-    pre-copy pack, ascending handle; digests refreshed from what was copied."""
+    pre-copy pack, ascending handle; digests refreshed from what was copied.
+    window: the engine-delimited STW window (pos_final_stop)."""
     sizes = [3 * cs, 5000, 100, 2 * cs + 33]
     p = Proc(orc, sizes, seed0=700, handles=[2, 4, 6, 8], offsets=offsets)
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
@@ -297,8 +299,10 @@ def test_delta_copy_pack_and_digests(orc, cs, offsets):
     pd.device_synchronize()
     assert eng.prepare_final_stop() == eng.prepare_final_stop()  # idempotent staging
     pd.device_synchronize()
-    off, n1 = eng.at_final_stop()
+    off, n1 = eng.at_final_stop(stw_begin_slot=3, stw_end_slot=4) if window else eng.at_final_stop()
     assert off == (n0 + 255) // 256 * 256
+    if window:
+        assert 0 < eng.event_elapsed(3, 4) == pytest.approx(eng.kernel_ms("delta"))
     got = download_cache(eng, off, n1)
     g_flags = np.concatenate([np.full(b.chunk_count(cs), b.handle in (4, 8), np.uint8) for b in p.bufs])
     want = opack(orc, list(zip(p.handles, p.host)), cs, g_flags, epoch=0, pflags=1)
