@@ -198,8 +198,11 @@ TEST_CASE("[gpu] dirty-bit checkpoint: pre-copy + final delta rebuild the state 
   REQUIRE(e.dirty_set() == std::set<BufferHandle>{2});
   b.write(0, b.size, 42);
   check(pos_device_sync());
-  PackRef fin = e.at_final_stop();
+  PackRef fin = e.at_final_stop(nullptr, 3, 4);  // STW window = [event 3, gather, event 4]
   REQUIRE(fin.offset >= pre.bytes);
+  float stw_ms = 0;
+  check(pos_event_elapsed(e.raw(), 3, 4, &stw_ms));
+  REQUIRE(stw_ms > 0);
   ship(fin);
   REQUIRE(captured[1] == a.host);
   REQUIRE(captured[2] == b.host);
