@@ -529,6 +529,25 @@ __device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* 
 
 enum : int { kModeHash = 0, kModeCopy = 1, kModeCached = 2 };
 
+// Phase stamps of k_hash_chunks for tools/hash_micro.cu (compiled there only):
+// per (CTA, warp), globaltimer at entry, tables ready, chunk record read,
+// CRC done, digest published -- for the warp's first item.
+#ifdef POS_HASH_PROF
+__device__ unsigned long long g_hash_prof[1024][16][5];
+#define POS_PROF(k, first)                                                              \
+  do {                                                                                  \
+    if ((first) && (threadIdx.x & 31) == 0 && blockIdx.x < 1024) {                      \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      g_hash_prof[blockIdx.x][threadIdx.x >> 5][k] = t_;                                \
+    }                                                                                   \
+  } while (0)
+#else
+#define POS_PROF(k, first) \
+  do {                     \
+  } while (0)
+#endif
+
 // kModeHash: every chunk -> digest, dirty flag, bitmap bit.
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
@@ -540,7 +559,9 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
+  POS_PROF(0, true);
   load_hash_tables(smem, p.tables);
+  POS_PROF(1, true);
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
   uint32_t tma_phase = 0;
@@ -612,10 +633,12 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
       for (uint64_t q = pa + (uint64_t)lane * 16384; q < pe; q += 32 * 16384)
         l2_prefetch(reinterpret_cast<const void*>(q), (uint32_t)(pe - q < 16384 ? pe - q : 16384));
     }
+    POS_PROF(2, round == 0);
     const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll, kTma>(small, p.xinv, lsel, lane, src + lo, n,
                                                   p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr,
                                                   p.pf_bytes == 1, (uint32_t)p.pad3, tma)
                          : 0u;
+    POS_PROF(3, round == 0);
     if (nseg == 1) {
       crc = r;
     } else {
@@ -655,6 +678,7 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
         if (dirty && p.q && !(p.dedup && (b.flags & kBufHasUpstream))) ship_push(p.q, p.q_seq, g);
       }
     }
+    POS_PROF(4, round == 0);
   }
 }
 

@@ -5,8 +5,10 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/hash_micro tools/hash_micro.cu
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
+#define POS_HASH_PROF 1
 #include "../paper_2405_12079_b200/csrc/kernels.cuh"
 
 using namespace posdump;
@@ -119,6 +121,40 @@ int main() {
                 do_flush ? "flush" : "warm ", t[t.size() / 2], t[0], ms * 1e3f / 20);
     return cudaGetLastError();
   };
+  // phase stamps of one flushed launch per size (POS_HASH_PROF)
+  static unsigned long long prof[1024][16][5];
+  for (uint32_t pf : {0u, 65536u, 16384u, 1u})
+  for (uint64_t n : {1ull, 148ull, 1526ull}) {
+    HashParams q = p;
+    q.n_items = n;
+    q.pf_bytes = pf;  // > 1: L2 bulk prefetch of the chunk's first pf bytes at its start; 1: sliding window
+    q.pad3 = 32;
+    for (int rep = 0; rep < 3; ++rep) {
+      std::memset(prof, 0, sizeof prof);
+      CK(cudaMemcpyToSymbol(g_hash_prof, prof, sizeof prof));
+      cudaMemsetAsync(flush, rep, FL, s);
+      k_hash_chunks<kModeHash, 512, 8><<<148, 512, kHashSmem, s>>>(q);
+      CK(cudaStreamSynchronize(s));
+    }
+    CK(cudaMemcpyFromSymbol(prof, g_hash_prof, sizeof prof));
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < 148; ++b)
+      for (int w = 0; w < 16; ++w)
+        if (prof[b][w][0]) t0 = std::min(t0, prof[b][w][0]);
+    std::vector<double> ph[5], chain;
+    for (int b = 0; b < 148; ++b)
+      for (int w = 0; w < 16; ++w) {
+        if (!prof[b][w][2]) continue;
+        for (int k = 0; k < 5; ++k) ph[k].push_back((prof[b][w][k] - t0) / 1e3);
+        chain.push_back((prof[b][w][3] - prof[b][w][2]) / 1e3);
+      }
+    auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    auto mx = [](const std::vector<double>& v) { return *std::max_element(v.begin(), v.end()); };
+    std::printf("pf=%-6u n=%-5llu warps %4zu | entry %5.2f/%5.2f tables %5.2f/%5.2f record %5.2f/%5.2f crc %5.2f/%5.2f "
+                "done %5.2f/%5.2f us (median/max from first entry) | chain %5.2f/%5.2f\n",
+                pf, (unsigned long long)n, chain.size(), med(ph[0]), mx(ph[0]), med(ph[1]), mx(ph[1]), med(ph[2]),
+                mx(ph[2]), med(ph[3]), mx(ph[3]), med(ph[4]), mx(ph[4]), med(chain), mx(chain));
+  }
   for (bool fl : {true, false}) {
     CK(timed("empty <<<148,512>>>", [&] { k_empty_512<<<148, 512, 0, s>>>(); }, fl));
     CK(timed("empty + 192 KiB smem", [&] { k_empty_smem<<<148, 512, kHashSmem, s>>>(); }, fl));
