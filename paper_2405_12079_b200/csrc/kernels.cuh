@@ -502,10 +502,12 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
 // the replicated table at 0x10000.
 constexpr uint32_t kRepSrcOff = kSmallTablesBytes;  // 4 KiB source, after the small tables
 
-__device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* tables) {
+// Split in two so that a kernel can overlap its own first global loads with
+// the tables' flight: issue (thread 0 starts the bulk copy) ... finish (wait,
+// replicate, block barrier).
+__device__ __forceinline__ void load_hash_tables_issue(uint8_t* smem, const uint32_t* tables) {
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   if (sbase + kSmallTablesBytes + 4096 + 64 > kRepAbs) __trap();  // layout assumption (reserved smem < 36 KiB)
-  uint32_t* rep = reinterpret_cast<uint32_t*>(smem + (kRepAbs - sbase));
   uint32_t* src = reinterpret_cast<uint32_t*>(smem + kRepSrcOff);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kRepSrcOff + 4096);
   if (threadIdx.x == 0) {
@@ -516,6 +518,13 @@ __device__ __forceinline__ void load_hash_tables(uint8_t* smem, const uint32_t* 
     bulk_g2s(src, tables, 4096, bar);                        // Z^512
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
+}
+
+__device__ __forceinline__ void load_hash_tables_finish(uint8_t* smem) {
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  uint32_t* rep = reinterpret_cast<uint32_t*>(smem + (kRepAbs - sbase));
+  uint32_t* src = reinterpret_cast<uint32_t*>(smem + kRepSrcOff);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kRepSrcOff + 4096);
   mbar_wait(bar, 0);
   // 4 consecutive lane slots of one entry hold the same word: 16-B stores
   for (int q = threadIdx.x; q < 32768 / 4; q += blockDim.x) {
@@ -560,7 +569,32 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
   constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
   POS_PROF(0, true);
-  load_hash_tables(smem, p.tables);
+  load_hash_tables_issue(smem, p.tables);
+  if (MODE == kModeHash) {
+    // Warm this warp's first chunk while the tables fly: its record (chunk
+    // map -> buffer: two dependent DRAM loads, ~1.2 us) and its first 4 KiB
+    // (one L2 prefetch per lane).  Measured: the record phase was 1.2 us of a
+    // 100 MB launch's ~27 us, serial after the 1.9 us prologue.
+    constexpr int W0 = kThreads / 32;
+    const uint32_t warp0 = threadIdx.x >> 5;
+    uint64_t it0;
+    if (p.nseg == 1) {
+      it0 = (uint64_t)warp0 * gridDim.x + blockIdx.x;
+    } else {
+      const uint32_t grp = warp0 / p.nseg;
+      it0 = ((uint64_t)grp * gridDim.x + blockIdx.x) * p.nseg + warp0 % p.nseg;
+    }
+    if (it0 < p.n_items * p.nseg && (W0 % p.nseg) == 0) {
+      const uint64_t g0 = p.item_base + it0 / p.nseg;
+      const uint2 cm0 = p.chunk_map[g0];
+      const DevBuf& b0 = p.bufs[cm0.x];
+      const uint64_t off0 = (uint64_t)cm0.y * p.chunk_size + (it0 % p.nseg) * p.seg_bytes;
+      const uint64_t pf = (threadIdx.x & 31) * 128ull;
+      if (off0 + pf < b0.size)  // stays inside the buffer
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b0.ptr + off0 + pf));
+    }
+  }
+  load_hash_tables_finish(smem);
   POS_PROF(1, true);
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
