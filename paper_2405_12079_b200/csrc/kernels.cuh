@@ -634,20 +634,27 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
     it = ((uint64_t)my_group * gridDim.x + blockIdx.x) * nseg + my_seg;
     stride = (uint64_t)gridDim.x * G * nseg;
   }
+  // kModeHash: the next item's chunk-map entry is loaded one item ahead (its
+  // DRAM latency hides under the current chunk instead of heading the next).
+  uint2 cm_next = make_uint2(0, 0);
+  if (!WORK && it < n_units) cm_next = p.chunk_map[p.item_base + (nseg == 1 ? it : it / nseg)];
   for (uint32_t round = 0; it < n_units; it += stride, ++round) {
     const uint64_t item = nseg == 1 ? it : it / nseg;
     const uint32_t seg = nseg == 1 ? 0u : my_seg;
     uint64_t g, dst_off = 0;
     uint32_t entry = 0;
+    uint2 cm;
     if (WORK) {
       uint4 w = p.work[item];
       g = w.x;
       entry = w.y;
       dst_off = (uint64_t)w.z | ((uint64_t)w.w << 32);
+      cm = p.chunk_map[g];
     } else {
       g = p.item_base + item;
+      cm = cm_next;
+      if (it + stride < n_units) cm_next = p.chunk_map[p.item_base + (nseg == 1 ? it + stride : (it + stride) / nseg)];
     }
-    const uint2 cm = p.chunk_map[g];
     const DevBuf& b = p.bufs[cm.x];
     const uint64_t start = (uint64_t)cm.y * p.chunk_size;
     const bool last = cm.y + 1 == b.nchunks;
