@@ -843,7 +843,8 @@ def main():
     ap.add_argument("--waves", type=int, default=0,
                     help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c4 8)")
     ap.add_argument("--mode", choices=["pack", "direct"], default="direct",
-                    help="pack: POSD pack D2H by the copy engine + host apply; direct: SM stores into the pinned image")
+                    help="pack: POSD pack D2H by the copy engine + host apply; direct: runs of shipped chunks "
+                         "copied straight into the pinned image (copy engine; POSDUMP_DIRECT_DRAIN=sm|queue: SM stores)")
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)

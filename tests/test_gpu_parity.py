@@ -312,6 +312,23 @@ def test_delta_copy_pack_and_digests(orc, cs, offsets, window):
     eng.close()
 
 
+def test_final_stop_window_errors(orc):
+    """pos_final_stop validates its event slots (InvalidArgument) before
+    touching the delta; a valid window then works on the same engine."""
+    cs = 4096
+    p = Proc(orc, [3 * cs, 100], seed0=900)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    eng.plan_precopy()
+    eng.record_dirty([1])
+    for begin, end in [(3, 3), (3, -1), (1000, 4), (3, 1000)]:
+        with pytest.raises(pd.SimError):
+            eng.at_final_stop(stw_begin_slot=begin, stw_end_slot=end)
+    off, n = eng.at_final_stop(stw_begin_slot=3, stw_end_slot=4)
+    assert n > 0 and eng.event_elapsed(3, 4) > 0
+    eng.close()
+
+
 def test_scatter_restores_state(orc):
     """materialize/load_complete (cr.hpp:1026-1084): packs applied in order
     reproduce the buffers."""
