@@ -813,11 +813,82 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
     return out
 
 
+def cpu_breakdown(wl: Workload, threads: int, sample_bytes: int) -> dict:
+    """SURVEY §8(d)'s CPU path timed function by function on the same bounded
+    sample, on 1 thread and on `threads`: the reference's crc32 per 64 KiB
+    chunk (crc32.hpp:26-34), its dump loop (crc32 + chunk_copied capture,
+    cr.hpp:481-504), and -- single-threaded, as in the reference --
+    write_image / read_image of the sample as Inline records
+    (image.hpp:136-361).  GB/s of sample bytes, best of 3."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle_ctypes import oracle, reference, Rec, Alloc
+    ref, orc = reference(), oracle()
+    if ref is None:
+        return {}
+    idx, acc = [], 0
+    for i, n in enumerate(wl.sizes):
+        if acc >= sample_bytes:
+            break
+        idx.append(i)
+        acc += n
+    bufs = []
+    for i in idx:
+        a = np.empty(wl.sizes[i], np.uint8)
+        orc.or_fill_bytes(9000 + i, a.ctypes.data, a.size)
+        bufs.append(a)
+
+    def best(fn, reps=3):
+        t = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            t.append(time.perf_counter() - t0)
+        return round(acc / min(t) / 1e9, 3)
+
+    def crc_buf(a):
+        for o in range(0, a.size, CHUNK):
+            ref.ref_crc32(a.ctypes.data + o, min(CHUNK, a.size - o))
+
+    def crc_all(nt):
+        if nt == 1:
+            for a in bufs:
+                crc_buf(a)
+        else:
+            with ThreadPoolExecutor(nt) as ex:
+                list(ex.map(crc_buf, bufs))
+
+    sizes = np.array([a.size for a in bufs], np.uint64)
+    ptrs = (C.c_void_p * len(bufs))(*[a.ctypes.data for a in bufs])
+    nch = sum((a.size + CHUNK - 1) // CHUNK for a in bufs)
+    prev, cur, fl = np.zeros(nch, np.uint32), np.zeros(nch, np.uint32), np.zeros(nch, np.uint8)
+    st = ref.ref_state_create(len(bufs), sizes.ctypes.data, ptrs, CHUNK)
+    out = {"sample": f"{len(bufs)} buffers, {acc} B", "threads": threads,
+           "crc32_per_chunk": {"1": best(lambda: crc_all(1)), str(threads): best(lambda: crc_all(threads))},
+           "dump_loop_all_dirty": {
+               "1": best(lambda: ref.ref_state_dump(st, prev.ctypes.data, 0, cur.ctypes.data, fl.ctypes.data, 1)),
+               str(threads): best(lambda: ref.ref_state_dump(st, prev.ctypes.data, 0, cur.ctypes.data,
+                                                             fl.ctypes.data, threads))}}
+    ref.ref_state_destroy(st)
+    recs = (Rec * len(bufs))()
+    for k, a in enumerate(bufs):
+        recs[k].handle, recs[k].kind = k + 1, 0
+        recs[k].inline_bytes, recs[k].inline_len = a.ctypes.data, a.nbytes
+    allocs = (Alloc * len(bufs))(*[Alloc(k + 1, 0x7000_0000_0000 + (k << 30), a.nbytes) for k, a in enumerate(bufs)])
+    args = [4096, None, 0, recs, len(bufs), allocs, len(bufs), None, 0, 0, len(bufs) + 1, 0, None, 0]
+    n = ref.ref_write_image(*args, None, 0)
+    img = np.empty(n, np.uint8)
+    out["write_image"] = best(lambda: ref.ref_write_image(*args, img.ctypes.data, n))
+    out["read_image"] = best(lambda: ref.ref_read_image_check(img.ctypes.data, n))
+    return out
+
+
 def run_reference(args, wl: Workload, world, rank):
     if rank != 0:
         return None
     threads = os.cpu_count() or 1
     v, ms, sample, kind = cpu_reference_run(wl, args.steps, args.warmup, threads, args.ref_sample_bytes)
+    breakdown = cpu_breakdown(wl, threads, min(args.ref_sample_bytes, 64 << 20))
     return {
         "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
@@ -827,6 +898,7 @@ def run_reference(args, wl: Workload, world, rank):
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_breakdown_gbps": breakdown,
     }
 
 
