@@ -44,3 +44,16 @@ def test_large_states(name, total):
 
 def test_aggregate_value_is_whole_job():
     assert bench.aggregate_value(8, 100_000_000, 1.0) == pytest.approx(800.0)
+
+
+def test_reference_cpu_breakdown():
+    """The reference arm's per-function CPU timings run the reference's own
+    code (oracle/_ref) on a small sample and report positive rates."""
+    from oracle_ctypes import reference
+    if reference() is None:
+        pytest.skip("oracle/_ref not built")
+    out = bench.cpu_breakdown(bench.Workload("c2"), 2, 2 << 20)
+    assert set(out) >= {"crc32_per_chunk", "dump_loop_all_dirty", "write_image", "read_image"}
+    assert all(v > 0 for v in out["crc32_per_chunk"].values())
+    assert all(v > 0 for v in out["dump_loop_all_dirty"].values())
+    assert out["write_image"] > 0 and out["read_image"] > 0
