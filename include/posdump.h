@@ -93,6 +93,14 @@ int pos_ctx_destroy(pos_ctx* ctx);
 /* snapshot_buffers_ = active_handles() (cr.hpp:346): the buffer set of the
  * dump, ascending handle.  Resets the epoch (next hash is "fresh"). */
 int pos_register_buffers(pos_ctx* ctx, const pos_buffer_desc* bufs, uint32_t n);
+/* The snapshot's buffer set changed mid-session (allocations join dirty,
+ * frees are dropped: cr.hpp:301-306, 709-716).  `bufs` (ascending handle)
+ * replaces the registered set; a buffer with an unchanged handle, address and
+ * size keeps its digest history, flags and host-image range (the pre-copy
+ * stays incremental for it); a new one joins fresh -- every chunk dirty until
+ * pos_commit_epoch -- and needs pos_register_image before a direct pre-copy;
+ * a missing one is never read again.  Synchronises the device. */
+int pos_update_buffer_set(pos_ctx* ctx, const pos_buffer_desc* bufs, uint32_t n);
 /* Refresh provenance / written bits of one registered buffer, e.g. after
  * note_h2d_provenance (process.hpp:505-522). */
 int pos_update_buffer(pos_ctx* ctx, const pos_buffer_desc* buf);

@@ -170,6 +170,26 @@ class DumpEngine {
   }
   const std::vector<GpuBuffer>& snapshot_buffers() const { return bufs_; }
 
+  // on_alloc (cr.hpp:298-306) / a buffer gone mid-session (cr.hpp:709-716):
+  // the snapshot's list changes; unchanged buffers keep their digest history,
+  // a new one joins dirty (recorded in dirty_set_, as on_alloc does).
+  void update_snapshot(std::vector<GpuBuffer> bufs, bool new_ones_dirty = true) {
+    std::sort(bufs.begin(), bufs.end(),
+              [](const GpuBuffer& a, const GpuBuffer& b) { return a.handle < b.handle; });
+    std::set<BufferHandle> old;
+    for (const auto& b : bufs_) old.insert(b.handle);
+    bufs_ = std::move(bufs);
+    std::vector<pos_buffer_desc> d;
+    for (const auto& b : bufs_) d.push_back(b.desc());
+    check(pos_update_buffer_set(ctx_, d.data(), static_cast<uint32_t>(d.size())));
+    std::set<BufferHandle> kept;
+    for (const auto& b : bufs_)
+      if (dirty_.count(b.handle) || (new_ones_dirty && !old.count(b.handle))) kept.insert(b.handle);
+    dirty_ = kept;
+    std::vector<uint64_t> hs(dirty_.begin(), dirty_.end());
+    if (!hs.empty()) check(pos_record_dirty(ctx_, hs.data(), static_cast<uint32_t>(hs.size())));
+  }
+
   // plan_precopy (cr.hpp:377-406): O2 digests + O1 verdicts + O3 pack.
   // Returns the pre-copy pack (at cache offset 0).
   PackRef plan_precopy(void* stream = nullptr) {

@@ -96,6 +96,7 @@ SIGNATURES = {
     "pos_ctx_create": [C.POINTER(pos_config), C.POINTER(P)],
     "pos_ctx_destroy": [P],
     "pos_register_buffers": [P, C.POINTER(pos_buffer_desc), U32],
+    "pos_update_buffer_set": [P, C.POINTER(pos_buffer_desc), U32],
     "pos_update_buffer": [P, C.POINTER(pos_buffer_desc)],
     "pos_num_chunks": [P, PU64],
     "pos_hash_chunks": [P, P],

@@ -43,6 +43,7 @@ enum : uint32_t {
   kBufHostUntouched = 2u,
   kBufWrittenSinceCkpt = 8u,
   kBufStaged = 16u,  // CoW-staged this epoch: its snapshot is the staged pack
+  kBufFresh = 32u,   // joined the snapshot mid-session (cr.hpp:301-306): every chunk dirty until committed
 };
 
 struct CopyItem {            // one contiguous copy: chunk -> pack, or pack -> chunk
@@ -711,7 +712,7 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
       } else if (staged) {
         p.flags[g] = 0;  // its snapshot is in the staging pack: nothing to ship
       } else if (p.flags) {
-        const bool dirty = !p.prev_valid || p.digest_prev[g] != crc;
+        const bool dirty = !p.prev_valid || (b.flags & kBufFresh) || p.digest_prev[g] != crc;
         p.flags[g] = dirty;
         if (dirty && p.bitmap) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
         // ship now unless O1 may still drop the buffer (provenance: the scan

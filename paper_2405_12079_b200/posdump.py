@@ -270,6 +270,15 @@ class DumpEngine:
         arr = (_lib.pos_buffer_desc * max(len(self.buffers), 1))(*[b.desc() for b in self.buffers])
         check(lib().pos_register_buffers(self.ctx, arr, len(self.buffers)))
 
+    def update_buffer_set(self, bufs: Iterable[GpuBuffer]) -> None:
+        """The snapshot's buffers changed mid-session (cr.hpp:301-306,
+        709-716): unchanged buffers keep their digest history and image
+        range; new ones join fresh (all chunks dirty until commit_epoch);
+        missing ones are dropped."""
+        self.buffers = sorted(bufs, key=lambda b: b.handle)
+        arr = (_lib.pos_buffer_desc * max(len(self.buffers), 1))(*[b.desc() for b in self.buffers])
+        check(lib().pos_update_buffer_set(self.ctx, arr, len(self.buffers)))
+
     def update_buffer(self, b: GpuBuffer) -> None:
         d = b.desc()
         check(lib().pos_update_buffer(self.ctx, C.byref(d)))

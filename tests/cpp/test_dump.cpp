@@ -220,6 +220,37 @@ TEST_CASE("[gpu] dirty-bit checkpoint: pre-copy + final delta rebuild the state 
   REQUIRE(write_image(img) == write_image(want));
 }
 
+TEST_CASE("[gpu] a buffer allocated mid-session joins dirty, a freed one is dropped") {  // cr.hpp:298-306
+  SimConfig cfg;
+  cfg.chunk_size = 4096;
+  cfg.cache_capacity = 4 << 20;
+  DumpEngine e(cfg);
+  DevBuf a(3 * 4096 + 5, 61), b(5000, 62), c(100, 63);
+  e.snapshot({GpuBuffer{1, a.ptr, a.size}, GpuBuffer{2, b.ptr, b.size}, GpuBuffer{3, c.ptr, c.size}});
+  std::map<BufferHandle, std::vector<uint8_t>> captured{
+      {1, std::vector<uint8_t>(a.size)}, {2, std::vector<uint8_t>(b.size)}, {3, std::vector<uint8_t>(c.size)}};
+  auto ship = [&](const PackRef& p) {
+    std::vector<uint8_t> pk = pinned_d2h(e, p);
+    apply_pack(pk.data(), pk.size(), captured, 2);
+  };
+  ship(e.plan_precopy());
+  e.end_checkpoint_session();
+  DevBuf d(2 * 4096, 64);  // allocated during the next session
+  a.write(4096 + 1, 7, 65);
+  check(pos_device_sync());
+  e.update_snapshot({GpuBuffer{1, a.ptr, a.size}, GpuBuffer{3, c.ptr, c.size}, GpuBuffer{4, d.ptr, d.size}});
+  REQUIRE(e.dirty_set() == std::set<BufferHandle>{4});
+  captured.erase(2);
+  captured[4] = std::vector<uint8_t>(d.size);
+  PackRef pre = e.plan_precopy();  // buffer 1's rewritten chunk only (4 is DAG-dirty)
+  ship(pre);
+  PackRef fin = e.at_final_stop();  // the new buffer, whole
+  ship(fin);
+  REQUIRE(captured[1] == a.host);
+  REQUIRE(captured[3] == c.host);
+  REQUIRE(captured[4] == d.host);
+}
+
 TEST_CASE("[gpu] restore scatter rejects corrupt packs and unknown handles") {
   SimConfig cfg;
   cfg.chunk_size = 4096;

@@ -755,6 +755,59 @@ def test_direct_precopy_into_image(orc, cs, waves, offsets, pageable):
 
 
 @pytest.mark.parametrize("cs", [4096, 1000])
+def test_buffer_set_changes_mid_session(orc, cs):
+    """A buffer freed and another allocated between checkpoints (cr.hpp:301-306,
+    709-716): pos_update_buffer_set keeps the surviving buffers incremental
+    (only their changed chunks ship), the new buffer ships whole, the freed
+    one is never read, and the image equals the device afterwards; a
+    committed epoch makes the new buffer incremental too."""
+    sizes = [3 * cs + 5, 5000, 100, 2 * cs + 33]
+    p = Proc(orc, sizes, seed0=5100)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
+    eng.register_buffers(p.bufs)
+    image = [np.zeros(n, np.uint8) for n in sizes]
+    eng.register_image(image)
+    ckpt, drain = pd.Stream(), pd.Stream()
+
+    def precopy():
+        eng.precopy_direct(waves=1, stream=ckpt, drain_stream=drain)
+        drain.synchronize()
+        ckpt.synchronize()
+        return eng.precopy_direct_result()[0]
+
+    assert precopy() == sum((n + cs - 1) // cs for n in sizes)
+    d0 = eng.digests()
+    eng.commit_epoch()
+    # buffer 2 is freed, buffer 5 allocated; buffer 1 rewritten in one chunk
+    p.write(0, cs + 3, 10, 501)
+    new = pd.DeviceMemory(3 * cs + 256)
+    pd.fill_bytes(new.ptr, 3 * cs, 502)
+    pd.device_synchronize()
+    new_host = mb(orc, 502, 3 * cs)
+    keep = [0, 2, 3]
+    bufs = [p.bufs[i] for i in keep] + [pd.GpuBuffer(handle=5, dev_ptr=new.ptr, size=3 * cs)]
+    eng.update_buffer_set(bufs)
+    # surviving buffers keep their digests (now the previous epoch's table)
+    nc = [(n + cs - 1) // cs for n in sizes]
+    base = np.cumsum([0] + nc)
+    kept_prev = np.concatenate([d0[base[i]:base[i + 1]] for i in keep])
+    assert eng.n_chunks == kept_prev.size + 3
+    with pytest.raises(pd.SimError):  # the new buffer has no image range yet
+        eng.precopy_direct(waves=1, stream=ckpt, drain_stream=drain)
+    image2 = [image[i] for i in keep] + [np.zeros(3 * cs, np.uint8)]
+    eng.register_image(image2)
+    assert precopy() == 1 + 3  # the rewritten chunk + the new buffer
+    hosts = [p.host[i] for i in keep] + [new_host]
+    for i, img in enumerate(image2):
+        assert np.array_equal(img, hosts[i]), f"buffer {bufs[i].handle}"
+    want = np.concatenate([odigests(orc, h, cs) for h in hosts])
+    assert np.array_equal(eng.digests(), want)
+    eng.commit_epoch()
+    assert precopy() == 0  # nothing changed: every buffer incremental now
+    eng.close()
+
+
+@pytest.mark.parametrize("cs", [4096, 1000])
 def test_h2d_provenance_on_device(orc, cs):
     """note_h2d_provenance (process.hpp:505-522) on the device, after
     test_api.cpp:76-98: a whole-buffer H2D records Upstream::crc ==
