@@ -101,6 +101,10 @@ int pos_register_buffers(pos_ctx* ctx, const pos_buffer_desc* bufs, uint32_t n);
  * pos_commit_epoch -- and needs pos_register_image before a direct pre-copy;
  * a missing one is never read again.  Synchronises the device. */
 int pos_update_buffer_set(pos_ctx* ctx, const pos_buffer_desc* bufs, uint32_t n);
+/* CheckpointTarget::fresh (cr.hpp:35, 396-401): the next round's target does
+ * not hold the previous round, so every chunk ships (the O2 skip is off until
+ * pos_commit_epoch; digests are still computed). */
+int pos_set_target_fresh(pos_ctx* ctx, int fresh);
 /* Refresh provenance / written bits of one registered buffer, e.g. after
  * note_h2d_provenance (process.hpp:505-522). */
 int pos_update_buffer(pos_ctx* ctx, const pos_buffer_desc* buf);

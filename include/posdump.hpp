@@ -170,6 +170,9 @@ class DumpEngine {
   }
   const std::vector<GpuBuffer>& snapshot_buffers() const { return bufs_; }
 
+  // CheckpointTarget::fresh (cr.hpp:35, 396): the next round ships every chunk.
+  void set_target_fresh(bool fresh = true) { check(pos_set_target_fresh(ctx_, fresh ? 1 : 0)); }
+
   // on_alloc (cr.hpp:298-306) / a buffer gone mid-session (cr.hpp:709-716):
   // the snapshot's list changes; unchanged buffers keep their digest history,
   // a new one joins dirty (recorded in dirty_set_, as on_alloc does).

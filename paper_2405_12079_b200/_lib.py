@@ -101,6 +101,7 @@ SIGNATURES = {
     "pos_num_chunks": [P, PU64],
     "pos_hash_chunks": [P, P],
     "pos_commit_epoch": [P],
+    "pos_set_target_fresh": [P, I32],
     "pos_read_digests": [P, P, U64, P],
     "pos_read_flags": [P, P, U64, P],
     "pos_read_bitmap": [P, P, U64, P],

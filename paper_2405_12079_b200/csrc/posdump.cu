@@ -290,6 +290,7 @@ struct pos_ctx {
   DevArray<uint32_t> d_digest[2];
   int cur = 0;
   bool prev_valid = false;
+  bool fresh_target = false;  // CheckpointTarget::fresh (cr.hpp:35): this round ships every chunk
   uint64_t epoch = 0;
   DevArray<uint8_t> d_flags;
   DevArray<uint32_t> d_bitmap;

@@ -293,6 +293,11 @@ class DumpEngine:
     def hash_chunks(self, stream=None) -> None:
         check(lib().pos_hash_chunks(self.ctx, _s(stream)))
 
+    def set_target_fresh(self, fresh: bool = True) -> None:
+        """CheckpointTarget::fresh (cr.hpp:35, 396): the next round ships
+        every chunk (until commit_epoch)."""
+        check(lib().pos_set_target_fresh(self.ctx, 1 if fresh else 0))
+
     def commit_epoch(self) -> None:
         check(lib().pos_commit_epoch(self.ctx))
 

@@ -804,6 +804,17 @@ def test_buffer_set_changes_mid_session(orc, cs):
     assert np.array_equal(eng.digests(), want)
     eng.commit_epoch()
     assert precopy() == 0  # nothing changed: every buffer incremental now
+    eng.commit_epoch()
+    # a fresh target (CheckpointTarget::fresh, cr.hpp:35,396) gets everything,
+    # the round after is incremental again
+    for im in image2:
+        im[:] = 0
+    eng.set_target_fresh()
+    assert precopy() == eng.n_chunks
+    for i, img in enumerate(image2):
+        assert np.array_equal(img, hosts[i])
+    eng.commit_epoch()
+    assert precopy() == 0
     eng.close()
 
 
