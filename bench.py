@@ -913,7 +913,7 @@ def main():
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
     ap.add_argument("--waves", type=int, default=0,
-                    help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c4 8)")
+                    help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c4 16)")
     ap.add_argument("--mode", choices=["pack", "direct"], default="direct",
                     help="pack: POSD pack D2H by the copy engine + host apply; direct: runs of shipped chunks "
                          "copied straight into the pinned image (copy engine; POSDUMP_DIRECT_DRAIN=sm|queue: SM stores)")
@@ -927,7 +927,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.waves <= 0:
-        args.waves = {"c1": 4, "c4": 8}.get(args.workload, 1)
+        args.waves = {"c1": 4, "c4": 16}.get(args.workload, 1)
     world, rank, local, dist = dist_setup()
     wl = Workload(args.workload)
     if args.impl == "reference":
