@@ -754,6 +754,42 @@ def test_direct_precopy_into_image(orc, cs, waves, offsets, pageable):
     eng.close()
 
 
+def test_direct_runs_never_span_allocations(orc):
+    """Separately allocated buffers that sit back to back in device memory,
+    imaged into one pinned range back to back: the copy-engine runs may not
+    be merged across the buffer boundary (a copy may not span two
+    allocations) -- the pre-copy and the delta drain still land every byte."""
+    cs = 4096
+    sizes = [3 * cs, 2 * cs, 4 * cs, cs]
+    mems = [pd.DeviceMemory(n) for n in sizes]
+    host = []
+    for i, (m, n) in enumerate(zip(mems, sizes)):
+        pd.fill_bytes(m.ptr, n, 600 + i)
+        host.append(mb(orc, 600 + i, n))
+    pd.device_synchronize()
+    bufs = [pd.GpuBuffer(handle=i + 1, dev_ptr=m.ptr, size=n) for i, (m, n) in enumerate(zip(mems, sizes))]
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(bufs)
+    pin = pd.PinnedHost(sum(sizes))
+    pin.array[:] = 0
+    image, o = [], 0
+    for n in sizes:
+        image.append(pin.array[o:o + n])
+        o += n
+    eng.register_image(image)
+    s, d = pd.Stream(), pd.Stream()
+    eng.record_dirty([3, 4])  # adjacent buffers through the delta drain too
+    eng.precopy_direct(waves=1, stream=s, drain_stream=d)
+    eng.at_final_stop(stream=s)
+    d.wait(s)
+    eng.delta_drain(stream=d)
+    d.synchronize()
+    s.synchronize()
+    for i, (img, h) in enumerate(zip(image, host)):
+        assert np.array_equal(img, h), f"buffer {i + 1}"
+    eng.close()
+
+
 @pytest.mark.parametrize("cs", [4096, 1000])
 def test_buffer_set_changes_mid_session(orc, cs):
     """A buffer freed and another allocated between checkpoints (cr.hpp:301-306,
