@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     uint64_t n_total, uint64_t* run_src, uint64_t* run_dst, uint64_t* run_len, TileStatus* status,
     TileCtl* ctl, uint32_t wpt) {
   __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_wr[kScanWarps];
-  __shared__ uint64_t s_pre[3], s_agg[3];
+  __shared__ uint64_t s_pre[3];
   __shared__ uint32_t s_tile, s_last;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -1282,7 +1282,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
                      : "memory");
         for (int q = 0; q < 3; ++q) s_pre[q] = pre[q];
       }
-      for (int q = 0; q < 3; ++q) s_agg[q] = agg[q];
     }
   }
   __syncthreads();
