@@ -323,7 +323,8 @@ class DumpEngine {
     check(pos_peer_cache_attach(ctx_, peer_device, bytes));
   }
 
-  // finalize_image's written_since_ckpt = false (cr.hpp:745): next epoch compares here.
+  // At finalize_image (cr.hpp:745, where the reference clears written_since_ckpt):
+  // this epoch's digests become the baseline the next epoch compares with.
   void end_checkpoint_session() {
     check(pos_commit_epoch(ctx_));
     dirty_.clear();
