@@ -851,6 +851,16 @@ def test_buffer_set_changes_mid_session(orc, cs):
         assert np.array_equal(img, hosts[i])
     eng.commit_epoch()
     assert precopy() == 0
+    eng.commit_epoch()
+    # same handle, moved allocation (re-allocated between checkpoints): fresh
+    moved = pd.DeviceMemory(3 * cs + 256)
+    pd.fill_bytes(moved.ptr, 3 * cs, 502)  # same bytes, new address
+    pd.device_synchronize()
+    bufs2 = bufs[:3] + [pd.GpuBuffer(handle=5, dev_ptr=moved.ptr, size=3 * cs)]
+    eng.update_buffer_set(bufs2)
+    eng.register_image(image2)
+    assert precopy() == 3  # its digests are unchanged, but it ships whole
+    assert np.array_equal(image2[3], new_host)
     eng.close()
 
 
