@@ -623,6 +623,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                        "l2": "flushed between steps (256 MiB memset)", "host_cpus": numa,
                        "value_counts": "checkpointed state bytes (incremental: only dirty chunks cross PCIe)"},
             "gpu_launches": int(statistics.mean(r["launches"] for r in res)),
+            "gpu_launches_counts": "libposdump kernels per step: the dump's (hash, O1, scan, staging, STW gather, "
+                                   "delta hash) plus the synthetic application's k_fill window launches",
             "roofline": {"bound": "hbm", "kernel": "k_hash_chunks", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
