@@ -972,6 +972,9 @@ def test_ondemand_restore_from_image(orc, pinned):
     with pytest.raises(pd.SimError) as ei:
         eng.restore_want(99)
     assert ei.value.errc == "InvalidLocator"
+    with pytest.raises(pd.SimError) as ei:  # the buffer set is pinned while the loader runs
+        eng.update_buffer_set(p.bufs)
+    assert ei.value.errc == "BadState"
     eng.restore_image_wait()
     for i in range(len(sizes)):
         assert np.array_equal(p.read(i), p.host[i]), f"buffer {i}"
