@@ -52,6 +52,18 @@ def test_invalid_config_rejected_before_device():
     assert e.value.errc == "InvalidArgument"
 
 
+def test_null_context_is_invalid_argument():
+    """Every context entry point checks its arguments before touching a
+    device: a null context is InvalidArgument (1 + Errc index 9)."""
+    lib = _lib.load()
+    inval = 1 + 9
+    assert lib.pos_update_buffer_set(None, None, 0) == inval
+    assert lib.pos_set_target_fresh(None, 1) == inval
+    assert lib.pos_final_stop(None, None, 3, 4, None, None) == inval
+    assert lib.pos_commit_epoch(None) == inval
+    assert lib.pos_record_dirty(None, None, 0) == inval
+
+
 def _mb(orc, seed, n):
     out = np.empty(n, np.uint8)
     orc.or_fill_bytes(seed, out.ctypes.data, n)
