@@ -1702,7 +1702,9 @@ __global__ void k_pack_items(const uint8_t* pack, uint64_t pack_bytes, const Dev
       else hi = mid;
     }
     CopyItem ci{0, 0, 0, 0};
-    if (lo >= nbufs || bufs[lo].handle != h) {
+    if ((off | payload_off) & 15) {  // payloads are 16-B padded by format: the bulk copy relies on it
+      atomicOr(err, 1u);
+    } else if (lo >= nbufs || bufs[lo].handle != h) {
       atomicOr(err, 2u);
     } else if ((uint64_t)c * chunk_size + len > bufs[lo].size || off + len > payload) {
       atomicOr(err, 2u);

@@ -18,6 +18,8 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <system_error>
+#include <stdexcept>
 #include <thread>
 #include <vector>
 
@@ -56,6 +58,15 @@ int guarded(F&& f) {
   } catch (const std::bad_alloc&) {
     g_last_error = "host allocation failed";
     return POS_E_OUT_OF_DEVICE_MEMORY;
+  } catch (const std::system_error& e) {  // std::thread / mutex
+    g_last_error = std::string("system error: ") + e.what();
+    return POS_E_BAD_STATE;
+  } catch (const std::exception& e) {  // out_of_range, length_error, ...
+    g_last_error = std::string("internal error: ") + e.what();
+    return POS_E_INVARIANT_VIOLATION;
+  } catch (...) {  // nothing crosses the C ABI
+    g_last_error = "unknown exception";
+    return POS_E_INVARIANT_VIOLATION;
   }
 }
 

@@ -1202,3 +1202,77 @@ def test_restore_from_reference_image(orc, ref, profile, seed, mode):
     for h, content in want.items():
         assert by_h[h].download().tobytes() == bytes(content), h
     eng.close()
+
+
+# ---------------------------------------------------------------------------
+# session-state hygiene (advisor round 1)
+
+def test_reregister_clears_image_and_pending_state(orc):
+    """register_image, then a new buffer set: the old image is gone, so a
+    direct pre-copy is BAD_STATE until an image is registered again."""
+    p = Proc(orc, [4096 * 3, 5000])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=4096, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    eng.register_image([np.zeros(b.size, np.uint8) for b in p.bufs])
+    eng.register_buffers(p.bufs)
+    with pytest.raises(pd.SimError) as ei:
+        eng.precopy_direct(waves=1)
+    assert ei.value.errc == "BadState"
+    img = [np.zeros(b.size, np.uint8) for b in p.bufs]
+    eng.register_image(img)
+    s, d = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=1, stream=s, drain_stream=d)
+    eng.precopy_direct_result()
+    d.synchronize()
+    for a, h in zip(img, p.host):
+        assert np.array_equal(a, h)
+    eng.close()
+
+
+def test_restore_begin_failure_leaves_no_loader(orc):
+    """A rejected on-demand restore leaves the context usable (no half-built
+    loader blocking buffer-set changes, no dangling gate)."""
+    p = Proc(orc, [4096 * 2, 4096])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=4096, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    bad = [np.zeros(p.bufs[0].size, np.uint8), np.zeros(p.bufs[1].size + 1, np.uint8)]
+    with pytest.raises(pd.SimError) as ei:
+        eng.restore_image_begin(bad)
+    assert ei.value.errc == "InvalidArgument"
+    eng.restore_gate(p.bufs[0].handle)  # no restore running: a no-op
+    eng.register_buffers(p.bufs)        # not BAD_STATE
+    good = [h.copy() for h in p.host]
+    for i in range(2):
+        p.zero(i)
+    eng.restore_image_begin(good)
+    eng.restore_image_wait()
+    for i in range(2):
+        assert np.array_equal(p.read(i), p.host[i])
+    eng.close()
+
+
+def test_scatter_rejects_misaligned_payloads(orc):
+    """POSD payloads are 16-B padded by format; a pack whose payload offset or
+    entry offset breaks that is CorruptImage, not a misaligned bulk copy."""
+    cs = 4096
+    p = Proc(orc, [cs * 2])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    good = opack(orc, [(1, p.host[0])], cs, np.ones(2, np.uint8))
+    for mutate in ("payload_off", "entry_off"):
+        bad = good.copy()
+        if mutate == "payload_off":
+            v = bad[24:32].view(np.uint64)
+            v[0] += 8
+        else:  # second entry's payload offset
+            v = bad[64 + 32 + 8:64 + 32 + 16].view(np.uint64)
+            v[0] += 4
+        dev = pd.DeviceMemory(bad.size)
+        dev.upload(bad)
+        with pytest.raises(pd.SimError) as ei:
+            eng.materialize(dev.ptr, bad.size)
+        assert ei.value.errc == "CorruptImage", mutate
+        with pytest.raises(pd.SimError) as ei:
+            eng.restore_packs([bad])
+        assert ei.value.errc == "CorruptImage", mutate
+    eng.close()
