@@ -3,31 +3,46 @@
 
 One step = one incremental dirty-bit checkpoint of the workload's buffer set
 (BASELINE.json metric "checkpoint dump GB/s per GPU (hash+compact+D2H) and
-stop-the-world ms"):
+stop-the-world ms"), default mode `direct`:
 
-  ckpt stream : k_hash_chunks (O2 digests + dirty bitmap) -> k_buffer_crc (O1)
-                -> k_pack_scan -> k_copy_bulk (O3 pack into the on-device cache)
-                -> [wait for the app stream: final stop] -> k_hash_chunks<copy>
-                (STW delta-copy of the DAG-flagged buffers)
-  copy stream : pinned D2H of the pre-copy pack (overlaps the STW window),
-                then of the delta pack
-  app stream  : the trace's kernels of the pre-copy window (their true write
-                sets are the DAG dirty set), running concurrently with the dump
+  ckpt stream : per wave of whole buffers: k_hash_chunks (O2 digests + dirty
+                flags) -> k_buffer_crc (O1) -> k_scan_tiles (ballot/prefix-sum
+                compaction of the shipped chunks into copy runs + a POSD index
+                pack in the on-device cache) ... [final stop: the application
+                drained AND the pre-copy complete] -> event, TMA bulk gather of
+                the DAG-dirty buffers into the cache (STW delta-copy), event
+                -> hash of the gathered copy
+  copy stream : cudaMemcpyBatchAsync of each wave's runs, live buffers ->
+                pinned host image (the checkpoint target's captured_), then the
+                delta's runs, cache -> image
+  app stream  : the application's kernels of the pre-copy window (their
+                write sets are the DAG dirty set), concurrent with the dump
 
 value = checkpointed state bytes / step time (device time, CUDA events:
-first dump kernel -> last D2H byte), aggregated over ranks as
-sum(bytes) / max(time).  stw_ms = final stop -> delta pack complete in the
-cache.  Inputs are resident in HBM when the timed region starts; L2 is
-flushed (a 256 MiB memset) between steps.
+first dump operation -> last byte in the host image), aggregated over ranks
+as sum(bytes) / max(time).  stw_ms = the final stop's window.  Inputs are
+resident in HBM when the timed region starts; L2 is flushed (a 256 MiB
+memset) before every step.
 
-Workloads (--workload): c2 (default, BASELINE configs[1]): the reference's
-own gen_workload trace of resnet-train-desk rescaled to ~100 MB
-(tests/golden/c2_resnet_trace.json); c1 (configs[0]): 64 x 16 MiB, 64 KiB
-chunks, 10% random chunk rewrites per epoch.
+Workloads (--workload; BASELINE.json configs): c5 (default, configs[4], the
+metric's own configuration): a 120 GB per-GPU training state, 960 x 125 MB,
+every tensor rewritten per optimizer step, the step's last 1 GB written
+during the pre-copy; c1 (configs[0]): 64 x 16 MiB, 10% random chunk rewrites;
+c2 (configs[1]): the reference's own gen_workload trace of resnet-train-desk
+rescaled to ~100 MB (tests/golden/c2_resnet_trace.json); c3 (configs[2]):
+Llama-3-8B bf16 + fp32 Adam state, 112 GB; c4 (configs[3]): 40 GB paged KV
+cache, append-only, then restore + delta replay.  Large states (c3-c5) are
+verified end to end: the device state is dropped, restored from the host
+image, and every chunk digest must equal the checkpoint's.
+
+--gpus N: one process per GPU (re-executed under torch.distributed.run when
+not already launched that way); each rank checkpoints its own state, no
+collective on the data path ("scaling": "weak").
 
 --impl reference times the reference's own CPU implementation of the path
 (oracle/_ref: gpucrsim's crc32 per chunk + chunk_copied capture, compiled
-from /root/reference) on all host cores, same workload and metric.
+from /root/reference) on all host cores, on a >= 1 GiB prefix of the same
+state, same metric and config.
 """
 from __future__ import annotations
 
@@ -95,7 +110,8 @@ class Workload:
             self.params = set()
             self.phases = []
             self.desc = (f"Llama-3 8B bf16 training state (params bf16 + fp32 master + Adam m,v; "
-                         f"{len(self.sizes)} buffers, {sum(self.sizes)} B), Adam step rewrites all")
+                         f"{len(self.sizes)} buffers, {sum(self.sizes)} B), Adam step rewrites all; "
+                         "the step's last >= 1 GB is written during the pre-copy")
         elif name == "c5":
             # config 5: a 120 GB per-GPU training state (960 tensors of 125 MB),
             # every tensor rewritten per step, checkpointed concurrently on
@@ -103,8 +119,8 @@ class Workload:
             self.sizes = [125_000_000] * 960
             self.params = set()
             self.phases = []
-            self.desc = ("120 GB per-GPU state (960 x 125 MB), all rewritten per step, cache-cycled pre-copy "
-                         "through the NVLink peer-GPU cache")
+            self.desc = ("120 GB per-GPU training state (960 x 125 MB tensors), every tensor rewritten per "
+                         "optimizer step; the step's last 1 GB is written during the pre-copy")
         elif name == "c4":
             # LLM inference KV cache: 32 layers x {K, V} paged tensors, 40 GB;
             # 16-token blocks of 8 KV heads x 128 dims bf16 = 32 KiB per block
@@ -126,6 +142,20 @@ class Workload:
             raise SystemExit(f"unknown workload {name}")
         self.total = sum(self.sizes)
         self.n_iter = max(1, len(self.phases) // 2)
+        # Training states (c3/c5): the checkpoint is triggered while the tail
+        # of the optimizer step is still running -- the last tensors (>= 1 GB)
+        # are written by application kernels DURING the pre-copy.  They are
+        # in the DAG from submission, so the pre-copy leaves them to the
+        # stop-the-world delta-copy (record_dirty, cr.hpp:901-931; at_final_stop,
+        # cr.hpp:599-621).
+        self.win = set()
+        if name in ("c3", "c5"):
+            acc = 0
+            for h in range(len(self.sizes), 0, -1):
+                if acc >= 1 << 30:
+                    break
+                self.win.add(h)
+                acc += self.sizes[h - 1]
 
     def epoch_writes(self, e: int):
         if self.name == "c4":  # append-only: block slots (e * S + s) mod nblocks
@@ -135,8 +165,8 @@ class Workload:
                 for h in range(1, len(self.sizes) + 1):
                     out.append((h, blk * self.block, self.block, mix64(mix64(e, s), h)))
             return out
-        if self.name in ("c3", "c5"):  # the optimizer step rewrites every tensor
-            return [(h, 0, n, mix64(e, h)) for h, n in enumerate(self.sizes, start=1)]
+        if self.name in ("c3", "c5"):  # the optimizer step rewrites every tensor (its tail: window())
+            return [(h, 0, n, mix64(e, h)) for h, n in enumerate(self.sizes, start=1) if h not in self.win]
         if self.name == "c1":
             nch = self.total // CHUNK
             rng = np.random.default_rng(e)
@@ -156,7 +186,9 @@ class Workload:
     def window(self, e: int):
         """Kernels of the next iteration's compute phase (stream 1 and 2
         kernels are serialised on one app stream)."""
-        if self.name in ("c1", "c3", "c4", "c5"):
+        if self.name in ("c3", "c5"):  # the optimizer step's tail: one kernel per tensor
+            return [[(h, mix64(mix64(e + 1000003, h), h))] for h in sorted(self.win)]
+        if self.name in ("c1", "c4"):
             return []
         it = (e + 1) % self.n_iter
         ph = self.phases[2 * it]
@@ -165,6 +197,13 @@ class Workload:
 
 # ---------------------------------------------------------------------------
 # helpers
+
+_T0 = time.time()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the driver reads only stdout's JSON line)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 def measured_peaks():
     try:
@@ -287,11 +326,10 @@ def cpu_reference_run(wl: Workload, steps: int, warmup: int, threads: int, sampl
         idx.append(i)
         acc += n
     sizes = [wl.sizes[i] for i in idx]
-    contents = []
-    for i in idx:
-        a = np.empty(wl.sizes[i], np.uint8)
-        orc.or_fill_bytes(7000 + i, a.ctypes.data, a.size)
-        contents.append(a)
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(threads)  # untimed input generation (ctypes drops the GIL)
+    contents = [np.empty(wl.sizes[i], np.uint8) for i in idx]
+    list(pool.map(lambda ia: orc.or_fill_bytes(7000 + ia[0], ia[1].ctypes.data, ia[1].size), zip(idx, contents)))
     nch = sum((n + CHUNK - 1) // CHUNK for n in sizes)
     prev = np.zeros(nch, np.uint32)
     cur = np.zeros(nch, np.uint32)
@@ -306,17 +344,24 @@ def cpu_reference_run(wl: Workload, steps: int, warmup: int, threads: int, sampl
     sel = {i + 1 for i in idx}
     for e in range(1, warmup + steps + 1):
         prev[:] = cur
-        for h, off, n, seed in wl.epoch_writes(e):
-            if h in sel:
+        groups: dict[int, list] = {}  # one host thread per buffer: write_content is per-buffer state
+        for w in wl.epoch_writes(e):
+            if w[0] in sel:
+                groups.setdefault(w[0], []).append(w)
+
+        def apply(ws):
+            for h, off, n, seed in ws:
                 buf = np.empty(n, np.uint8)
                 orc.or_fill_bytes(seed, buf.ctypes.data, n)
                 ref.ref_state_write(st, idx.index(h - 1), off, buf.ctypes.data, n)
+        list(pool.map(apply, groups.values()))
         t0 = time.perf_counter()
         ref.ref_state_dump(st, prev.ctypes.data, 1, cur.ctypes.data, flags.ctypes.data, threads)
         t1 = time.perf_counter()
         if e > warmup:
             times.append(t1 - t0)
     ref.ref_state_destroy(st)
+    pool.shutdown()
     ms = statistics.median(times) * 1e3
     return acc / (ms * 1e-3) / 1e9, ms, f"{len(sizes)} of {len(wl.sizes)} buffers ({acc} B) per step", kind
 
@@ -354,6 +399,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     pd.check(pd.lib().pos_set_device(local))
 
     total = wl.total
+    log(f"{wl.name}: {len(wl.sizes)} buffers, {total} B; allocating device state")
     mem = pd.DeviceMemory(total + 256 * len(wl.sizes))
     bufs, off = [], 0
     for i, n in enumerate(wl.sizes):
@@ -385,8 +431,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         for b in bufs:
             img_offs.append(o)
             o += (b.size + 255) // 256 * 256
-        img_pin = pd.PinnedHost(max(o, 1))
-        img_pin.array[:] = 0
+        log(f"allocating the pinned host image ({o} B)")
+        img_pin = pd.PinnedHost(max(o, 1), image=True)  # zero-filled huge pages, pinned + mapped
+        log("host image ready")
         host_image = [img_pin.array[a:a + b.size] for a, b in zip(img_offs, bufs)]
         eng.register_image(host_image)
         pins = []
@@ -465,6 +512,12 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         eng.record_dirty(dag_writes)
         def final_stop():  # at_final_stop (cr.hpp:599-621): drain the app, STW gather
             eng.stream_wait_event(2, ckpt)
+            if direct:
+                # The direct pre-copy reads the LIVE buffers: the final stop
+                # comes once it is complete (check_precopy_done -> final_stop,
+                # cr.hpp:532-597), so the application never resumes over
+                # chunks still being copied.
+                eng.stream_wait_event(8, ckpt)
             if args.trace:  # device-clock cross-check of the window (adds two operations to it)
                 eng.event_record(3, ckpt)
                 eng.stamp(3, ckpt)
@@ -540,11 +593,14 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         return r
 
     # epoch 0: fresh full checkpoint (untimed) seeds digests + host image
+    log("epoch 0 (full checkpoint)")
     checkpoint(0, True)
     e = 1
     for _ in range(args.warmup):
+        log(f"warm-up epoch {e}")
         checkpoint(e, False)
         e += 1
+    log("timed steps")
     barrier(dist, local)
     res = []
     with ClockSampler(local) as clk:
@@ -552,20 +608,32 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             res.append(checkpoint(e, False))
             e += 1
     barrier(dist, local)
+    log("e2e steps")
     e2e_res = []
     for _ in range(max(3, min(args.steps, 10))):
         e2e_res.append(checkpoint(e, True))
         e += 1
-    # verify the host image against the device (bit-exact), buffer by buffer
-    ok = args.no_host_apply or all(np.array_equal(img, mem.download(b.size, offset=b.dev_ptr - mem.ptr))
-                                   for b, img in zip(bufs, host_image))
-    restore = restore_measure(eng, pd, wl, bufs, host_image, mem, e) if (wl.name == "c4" and direct) else None
+    # Image parity.  (1) 512 random chunks: host image bytes == device bytes;
+    # (2) small states: every buffer byte for byte; large states (c3/c4/c5):
+    # the device state is thrown away and restored from the host image, and
+    # every chunk digest after the restore equals the checkpoint's (the whole
+    # image, at 2^-32 per chunk), then a delta pack is replayed (scatter).
+    log("image parity")
+    sample_ok = image_sample_check(pd, bufs, host_image, mem, 512, seed=e)
+    full = wl.total <= (4 << 30)
+    ok = sample_ok and (args.no_host_apply or not full or all(
+        np.array_equal(img, mem.download(b.size, offset=b.dev_ptr - mem.ptr)) for b, img in zip(bufs, host_image)))
+    restore = (restore_measure(eng, pd, wl, bufs, host_image, mem, e)
+               if (wl.name in ("c3", "c4", "c5") and direct) else None)
+    if restore is not None:
+        ok = ok and restore["digests_match_checkpoint"] and restore["delta_replay"]["bit_exact"]
 
     step_ms = sum(r["ms"] for r in res) / len(res)
     stw_ms = statistics.median(r["stw_ms"] for r in res)
     hash_ms = statistics.mean(r["hash_ms"] for r in res)
     e2e_ms = statistics.median(r["wall_ms"] for r in e2e_res)
     d2h_bytes = statistics.mean(r["precopy_bytes"] + r["delta_bytes"] for r in res)
+    delta_bytes = statistics.mean(r["delta_bytes"] for r in res)
     step_ms, stw_ms, e2e_ms = all_max(dist, [step_ms, stw_ms, e2e_ms], local)
 
     # host-link peak: best of 5 plain pinned D2H copies of 256 MiB (CUDA events)
@@ -577,7 +645,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         pd.check(pd.lib().pos_memcpy(pin.ptr, flush.ptr, link_n, D2H, int(copy)))
         eng.event_record(7, copy)
         link_peak = max(link_peak, link_n / (eng.event_elapsed(6, 7) * 1e-3) / 1e9)
-    d2h_achieved = statistics.mean(r["precopy_bytes"] / (r["d2h_ms"] * 1e-3) / 1e9 for r in res)
+    d2h_precopy = statistics.mean(r["precopy_bytes"] / (r["d2h_ms"] * 1e-3) / 1e9 for r in res)
+    d2h_step = d2h_bytes / (step_ms * 1e-3) / 1e9
 
     n_chunks = eng.n_chunks
     alg_bytes = total + 9 * n_chunks  # read B; digest prev read + cur write (8 B) + flag (1 B) per chunk
@@ -588,17 +657,21 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     tpath = os.path.join(ROOT, "profiles", f"hash_traffic_{wl.name}.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    stw_gbps = 2 * delta_bytes / (stw_ms * 1e-3) / 1e9 if stw_ms > 0 else 0.0
 
     out = None
     if rank == 0:
         value = aggregate_value(world, total, step_ms)
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
+            log("CPU baseline (oracle/_ref)")
             try:
                 threads = os.cpu_count() or 1
-                v, ms, sample, kind = cpu_reference_run(wl, 2, 1, threads, min(total, 128 << 20))
+                v, ms, sample, kind = cpu_reference_run(wl, 3, 1, threads, min(total, args.ref_sample_bytes))
                 cpu = {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-                       "sample": sample + "; crc32 per 64 KiB chunk + chunk_copied capture of dirty chunks"}
+                       "cpu_model": cpu_model(),
+                       "sample": sample + "; crc32 per 64 KiB chunk + chunk_copied capture of dirty chunks, "
+                                          "median of 3 steps after 1 warm-up"}
             except SystemExit as ex:
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": str(ex)}
         out = {
@@ -610,18 +683,21 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             "warmup": args.warmup,
             "ms_per_step": round(step_ms, 4),
             "stw_ms": round(stw_ms, 4),
-            "stw_window": "event -> TMA gather of the DAG-dirty buffers -> event, on the dump stream once the "
-                          "application stream drained (pos_final_stop); hashing of the copy is after the stop",
+            "stw_window": ("[event, TMA bulk gather of the DAG-dirty buffers into the on-device cache, event] on "
+                           "the dump stream, once the application drained and the pre-copy was complete "
+                           "(pos_final_stop); the delta's hash and D2H run after the stop"),
             **({"stw_device_clock_ms": round(statistics.median(r["stw_dev_ms"] for r in res), 4)} if args.trace else {}),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": wl.desc, "chunk_size": CHUNK, "state_bytes_per_gpu": total,
-                       "d2h_bytes_per_step": int(d2h_bytes), "parallelism": f"replicas{world}",
-                       "l2": "flushed between steps (256 MiB memset)", "host_cpus": numa,
-                       "value_counts": "checkpointed state bytes (incremental: only dirty chunks cross PCIe)"},
+            "config": bench_config(wl, world),
+            "run": {
+                "d2h_bytes_per_step": int(d2h_bytes), "stw_delta_bytes": int(delta_bytes),
+                "l2": "flushed between steps (256 MiB memset)", "host_cpus": numa,
+                "mode": ("direct: hash -> O1 -> scan per wave, copy-engine runs from the live buffers into the "
+                         "pinned host image" if direct else "pack: POSD packs in the cache, D2H + host apply")},
             "gpu_launches": int(statistics.mean(r["launches"] for r in res)),
             "gpu_launches_counts": "libposdump kernels per step: the dump's (hash, O1, scan, staging, STW gather, "
                                    "delta hash) plus the synthetic application's k_fill window launches",
@@ -629,13 +705,19 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": round(hash_ms, 5),
+                         "launch_ms_counts": "sum of every wave's hash launch (CUDA events on the dump stream)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                         "note": ("dominant HBM kernel of the dump; the step itself is bound by the host leg "
-                                  "(copy-engine runs into the pinned image in direct mode): see host_link")},
-            "host_link": {"bound": "pcie", "achieved": round(d2h_achieved, 2), "peak": round(link_peak, 2),
-                          "unit": "GB/s", "frac": round(d2h_achieved / link_peak, 4),
-                          "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run",
-                          "achieved_over": "pre-copy host leg (first byte -> last byte of the pre-copy)"},
+                         "note": ("dominant HBM kernel of the dump; the step itself is bound by the host link "
+                                  "(copy-engine runs into the pinned image): see host_link")},
+            "host_link": {"bound": "pcie", "achieved": round(d2h_step, 2), "peak": round(link_peak, 2),
+                          "unit": "GB/s", "frac": round(d2h_step / link_peak, 4),
+                          "achieved_over": "whole step: every byte that crossed PCIe / step time",
+                          "precopy_leg_gbps": round(d2h_precopy, 2),
+                          "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run"},
+            "stw_gather": {"bound": "hbm", "bytes": int(delta_bytes), "alg_bytes": int(2 * delta_bytes),
+                           "achieved": round(stw_gbps, 1), "peak": peak, "unit": "GB/s",
+                           "frac": round(stw_gbps / peak, 4) if peak else None,
+                           "note": "read + write of the DAG-dirty buffers over the whole STW window (launch incl.)"},
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
                           for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "delta_hash_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
@@ -645,23 +727,40 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                     "how": ("host wall clock around the DumpEngine calls until every byte is in the host image "
                             "(direct: the copy engine writes the pinned image; pack: D2H + host-side pack apply)")},
             "image_parity": bool(ok),
+            "image_parity_how": ("512 random chunks byte-compared with the device" +
+                                 ("; every buffer byte-compared" if full else
+                                  "; whole image: device state lost, restored from the image, every chunk "
+                                  "digest == the checkpoint's")),
             **({"restore": restore} if restore else {}),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
     eng.close()
+    img_pin = None
     return out
 
 
+def image_sample_check(pd, bufs, host_image, mem, n, seed):
+    """n random 64 KiB-aligned ranges: host image bytes == device bytes."""
+    rng = np.random.default_rng(seed)
+    for _ in range(n):
+        i = int(rng.integers(len(bufs)))
+        b = bufs[i]
+        off = int(rng.integers((b.size + CHUNK - 1) // CHUNK)) * CHUNK
+        ln = min(CHUNK, b.size - off)
+        if not np.array_equal(host_image[i][off:off + ln], mem.download(ln, offset=b.dev_ptr - mem.ptr + off)):
+            return False
+    return True
+
+
 def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
-    """KV-cache failover (BASELINE config 4): the device state is lost
-    (zeroed), the checkpoint image is loaded back on demand (pos_restore_image_*:
-    loads in buffer order, one layer's K gated first as the first replayed
-    decode kernel would), then a delta pack of the next decode burst is
-    replayed with the scatter kernel (delta-restore).  Checks: digests after
-    the restore == the checkpoint's digests (every chunk), and the scattered
-    delta == the live writes."""
-    from paper_2405_12079_b200.posdump import D2H  # noqa: F401
+    """Failover (BASELINE configs 3-5): the device state is lost (zeroed),
+    the checkpoint image is loaded back on demand (pos_restore_image_*: loads
+    in buffer order, a buffer in the middle gated first as the first replayed
+    kernel would), then a delta pack of the next writes (c4: the next decode
+    burst; c3/c5: the optimizer tail) is replayed with the scatter kernel
+    (delta-restore).  Checks: digests after the restore == the checkpoint's
+    digests (every chunk), and the scattered delta == the live writes."""
     eng.hash_chunks()  # the state as of the last checkpoint (nothing written since)
     digests_ckpt = eng.digests()
     total = sum(b.size for b in bufs)
@@ -670,7 +769,7 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
     pd.device_synchronize()
     h2d, app = pd.Stream(), pd.Stream(priority=1)
     order = [b.handle for b in bufs]
-    gate_h = bufs[len(bufs) // 2].handle  # a layer in the middle of the load order
+    gate_h = bufs[len(bufs) // 2].handle  # a buffer in the middle of the load order
     eng.event_record(10, h2d)
     t0 = time.perf_counter()
     eng.restore_image_begin(host_image, order=order, h2d_stream=h2d)
@@ -683,23 +782,30 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
     gate_ms = eng.event_elapsed(10, 11)
     eng.hash_chunks()
     restored_ok = bool(np.array_equal(eng.digests(), digests_ckpt))
-    # delta-restore replay: the next burst's appends as a POSD pack (pack mode),
+    # delta-restore replay: the next writes as a POSD pack (pack mode),
     # scattered back onto the restored state
     eng.commit_epoch()
-    writes = wl.epoch_writes(e)
     by_handle = {b.handle: b for b in bufs}
+    if wl.name == "c4":
+        writes = wl.epoch_writes(e)
+    else:  # the optimizer tail's tensors, rewritten
+        writes = [(h, 0, by_handle[h].size, mix64(e + 7, h)) for h in sorted(wl.win)]
     pd.fill_batch([(by_handle[h].dev_ptr + o, n, s) for h, o, n, s in writes])
     pd.device_synchronize()
     pack_bytes = eng.plan_precopy()
     cache_ptr, _ = eng.cache()
-    want = [mem.download(n, offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in writes[:64]]
+    probe = writes[:64]
+    want = [mem.download(min(n, 1 << 20), offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in probe]
     for h, o, n, _ in writes:
         pd.check(pd.lib().pos_memset(by_handle[h].dev_ptr + o, 0, n, None))
     pd.device_synchronize()
     eng.materialize(cache_ptr, pack_bytes)
     pd.device_synchronize()
     scatter_ms = eng.kernel_ms("scatter")
-    got = [mem.download(n, offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in writes[:64]]
+    got = [mem.download(min(n, 1 << 20), offset=by_handle[h].dev_ptr - mem.ptr + o) for h, o, n, _ in probe]
+    eng.hash_chunks()  # every chunk of the replayed state, not only the probes
+    replay_dig = eng.digests()
+    eng.commit_epoch()
     delta_ok = all(np.array_equal(a, b) for a, b in zip(want, got))
     payload = sum(n for _, _, n, _ in writes)
     peak = measured_peaks().get("hbm_gbs", FALLBACK_HBM)
@@ -709,7 +815,41 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
             "first_gated_buffer_ms": round(gate_ms, 3), "digests_match_checkpoint": restored_ok,
             "delta_replay": {"pack_bytes": pack_bytes, "payload_bytes": payload, "scatter_ms": round(scatter_ms, 4),
                              "scatter_gbps": round(sc, 1), "roofline_frac": round(sc / peak, 4),
-                             "alg_bytes": "2 x payload (read pack, write buffers)", "bit_exact": bool(delta_ok)}}
+                             "alg_bytes": "2 x payload (read pack, write buffers)", "bit_exact": bool(delta_ok),
+                             "no_stray_writes": bool(
+                                 int(np.count_nonzero(replay_dig != digests_ckpt)) <= pack_entries(writes))}}
+
+
+def pack_entries(writes) -> int:
+    return sum((n + CHUNK - 1) // CHUNK + 1 for _, _, n, _ in writes)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                name = line.split(":", 1)[1].strip()
+                break
+        else:
+            name = "unknown"
+        fam = mod = "?"
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("cpu family"):
+                fam = line.split(":", 1)[1].strip()
+            elif line.startswith("model") and not line.startswith("model name"):
+                mod = line.split(":", 1)[1].strip()
+            if fam != "?" and mod != "?":
+                break
+        return f"{name} (family {fam} model {mod}), {os.cpu_count()} logical CPUs"
+    except OSError:
+        return "unknown"
+
+
+def bench_config(wl: Workload, world: int) -> dict:
+    """The config dict both arms print (the driver compares them)."""
+    cfg = {"workload": wl.desc, "workload_id": wl.name, "chunk_size": CHUNK, "state_bytes_per_gpu": wl.total,
+           "buffers": len(wl.sizes), "parallelism": f"replicas{world}"}
+    return cfg
 
 
 def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
@@ -792,10 +932,9 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "stw_ms": round(stw_ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": wl.desc, "chunk_size": CHUNK, "state_bytes_per_gpu": total,
-                       "d2h_bytes_per_step": int(d2h), "packs_per_step": res[-1]["packs"],
-                       "parallelism": f"replicas{world}", "host_cpus": numa,
-                       "mode": "cache-cycled pre-copy (pos_precopy_stream), app idle at the checkpoint"},
+            "config": bench_config(wl, world),
+            "run": {"d2h_bytes_per_step": int(d2h), "packs_per_step": res[-1]["packs"], "host_cpus": numa,
+                    "mode": "cache-cycled pre-copy (pos_precopy_stream), app idle at the checkpoint"},
             "stages_ms": {"hash_waves_ms": round(statistics.mean(r["hash_ms"] for r in res), 3)},
             **({"peer_cache": {"device": peer, "bytes": int(args.peer_cache_gb * 1e9),
                                "capture_ms": round(statistics.mean(r["capture_ms"] for r in res), 3),
@@ -895,48 +1034,72 @@ def run_reference(args, wl: Workload, world, rank):
         "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": wl.desc, "chunk_size": CHUNK, "parallelism": "host cores"},
+        "config": bench_config(wl, world),
+        "run": {"executes": "rank 0 only, on the host cores", "cpu_model": cpu_model()},
         "impl": "reference",
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "cpu_breakdown_gbps": breakdown,
     }
 
 
+def relaunch_under_torchrun(n: int) -> None:
+    """`bench.py --gpus N` without a torchrun environment: re-exec as N ranks
+    (one process per GPU) on this node."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c5",
+                    help="c5 (default): BASELINE configs[4], the metric's own configuration (120 GB per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", action="store_true", help="per-step device timeline on stderr")
     ap.add_argument("--no-host-apply", action="store_true", help="diagnostic: skip the host image apply")
     ap.add_argument("--waves", type=int, default=0,
-                    help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c4 16)")
-    ap.add_argument("--mode", choices=["pack", "direct"], default="direct",
-                    help="pack: POSD pack D2H by the copy engine + host apply; direct: runs of shipped chunks "
-                         "copied straight into the pinned image (copy engine; POSDUMP_DIRECT_DRAIN=sm|queue: SM stores)")
+                    help="pre-copy pipeline waves (0 = the workload's default: c2 1, c1 4, c3/c4/c5 16)")
+    ap.add_argument("--mode", choices=["pack", "direct", "stream"], default="direct",
+                    help="direct: runs of shipped chunks copied by the copy engine straight into the pinned host "
+                         "image; pack: POSD packs D2H + host apply; stream: cache-cycled packs (c3/c5, with "
+                         "--peer-cache-gb through a peer GPU's HBM)")
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
-    ap.add_argument("--ref-sample-bytes", type=int, default=128 << 20)
+    ap.add_argument("--ref-sample-bytes", type=int, default=1 << 30,
+                    help="CPU reference: bounded sample (a prefix of the buffer set) of at least this many bytes")
     ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
     ap.add_argument("--peer-cache-gb", type=float, default=0.0,
-                    help="c3: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
+                    help="--mode stream: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if os.environ.get("BENCH_WATCHDOG_S"):  # diagnostics: every thread's stack if the run hangs
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["BENCH_WATCHDOG_S"]), exit=True)
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and env_world is None:
+        relaunch_under_torchrun(args.gpus)
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank per GPU")
     if args.waves <= 0:
-        args.waves = {"c1": 4, "c4": 16}.get(args.workload, 1)
+        args.waves = {"c1": 4, "c3": 16, "c4": 16, "c5": 16}.get(args.workload, 1)
     world, rank, local, dist = dist_setup()
     wl = Workload(args.workload)
     if args.impl == "reference":
         out = run_reference(args, wl, world, rank)
-    elif wl.name in ("c3", "c5"):
-        if wl.name == "c5" and args.peer_cache_gb == 0:
-            args.peer_cache_gb = 16.0
+    elif args.mode == "stream":
+        if wl.name not in ("c3", "c5"):
+            raise SystemExit("--mode stream is for the states larger than the cache (c3, c5)")
         out = run_gpu_stream(args, wl, world, rank, local, dist)
     else:
         out = run_gpu(args, wl, world, rank, local, dist)

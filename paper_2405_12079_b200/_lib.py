@@ -158,6 +158,8 @@ SIGNATURES = {
     "pos_dev_malloc": [U64, PU64],
     "pos_dev_free": [U64],
     "pos_host_malloc_pinned": [U64, C.POINTER(P)],
+    "pos_host_image_alloc": [U64, U32, C.POINTER(P)],
+    "pos_host_image_free": [P],
     "pos_host_free_pinned": [P],
     "pos_memcpy": [U64, U64, U64, I32, P],
     "pos_memset": [U64, I32, U64, P],

@@ -5,9 +5,11 @@
 // launch plumbing.  There is no CPU path: every operation on buffer bytes is
 // a kernel from kernels.cuh, and a missing device is an error.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <functional>
@@ -182,6 +184,7 @@ struct CrcTables {
     xinv.ensure(xi.size());
     ck(cudaMemcpy(tables.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "upload tables");
     ck(cudaMemcpy(xinv.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice), "upload xinv");
+    ck(cudaStreamSynchronize(cudaStreamLegacy), "upload sync");
     ck(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
     set_hash_smem<kModeHash>();
     set_hash_smem<kModeCopy>();
@@ -374,6 +377,8 @@ struct pos_ctx {
   cudaEvent_t copied[kMaxWaves] = {};
   cudaEvent_t wave_hash[kMaxWaves][2] = {};
   uint32_t waves_last = 0;                          // waves of the last pre-copy (hash timing)
+  bool wave_used[kMaxWaves] = {};                   // wave_hash slot holds a launch of this pre-copy
+  float hash_acc_ms = 0;                            // hash time of slots reused within the pre-copy
   uint64_t scan_seq = 0, slot_seq[kMaxWaves] = {};  // host-mirror sequence numbers
   // cache-cycled pre-copy (pos_precopy_stream): 2 cache regions, 2 pinned landing slots
   PinnedArray<uint8_t> h_land[2];
@@ -407,6 +412,14 @@ void check_launch(const char* what) {
 }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// Host-side setup writes device tables with cudaMemcpy / cudaMemset on the
+// legacy stream, which does NOT order with the library's non-blocking
+// streams: cudaMemset and pageable cudaMemcpy may return before the device
+// write lands.  Every setup path ends here, before any kernel can read them
+// (measured: a tile-status memset that landed after the scan launched
+// deadlocked its look-back while application kernels kept the GPU busy).
+void upload_barrier() { ck(cudaStreamSynchronize(cudaStreamLegacy), "upload sync"); }
 
 // cudaMemcpyBatchAsync flags of the host leg (POSDUMP_CE_OVERLAP=1: prefer
 // overlap with compute).

@@ -74,18 +74,27 @@ class DeviceMemory:
 
 
 class PinnedHost:
-    """Page-locked host memory (cudaHostAlloc) viewed as a numpy array."""
+    """Page-locked host memory viewed as a numpy array: cudaHostAlloc, or with
+    image=True the huge-page image allocator (pos_host_image_alloc: pinned +
+    mapped, zero-filled, ~10x faster to allocate at 100+ GB)."""
 
-    def __init__(self, nbytes: int):
+    def __init__(self, nbytes: int, image: bool = False, threads: int = 0):
         p = C.c_void_p(0)
-        check(lib().pos_host_malloc_pinned(max(nbytes, 1), C.byref(p)))
+        self.image = image
+        if image:
+            check(lib().pos_host_image_alloc(max(nbytes, 1), threads, C.byref(p)))
+        else:
+            check(lib().pos_host_malloc_pinned(max(nbytes, 1), C.byref(p)))
         self.ptr, self.nbytes = p.value, nbytes
         self.array = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(self.ptr))[:nbytes]
 
     def close(self):
         if self.ptr:
             self.array = None
-            lib().pos_host_free_pinned(self.ptr)
+            if self.image:
+                lib().pos_host_image_free(self.ptr)
+            else:
+                lib().pos_host_free_pinned(self.ptr)
             self.ptr = 0
 
     def __del__(self):

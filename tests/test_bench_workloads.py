@@ -33,13 +33,35 @@ def test_c2_trace_is_the_reference_resnet_desk():
                                         ("c5", 120_000_000_000)])
 def test_large_states(name, total):
     wl = bench.Workload(name)
-    assert wl.total == total and wl.window(1) == []
+    assert wl.total == total
     w = wl.epoch_writes(1)
     if name == "c4":  # 256 sequences append one 32 KiB block per layer tensor
+        assert wl.window(1) == []
         assert len(w) == 256 * 64 and all(n == 32768 for _, _, n, _ in w)
         assert sum(n for _, _, n, _ in w) / total < 0.02
-    else:  # an optimizer step rewrites every tensor
-        assert sum(n for _, _, n, _ in w) == total
+    else:  # an optimizer step rewrites every tensor; its tail (>= 1 GiB) runs during the pre-copy
+        win = {h for k in wl.window(1) for h, _ in k}
+        assert win == wl.win and sum(wl.sizes[h - 1] for h in win) >= 1 << 30
+        assert sum(wl.sizes[h - 1] for h in win) < 0.03 * total
+        assert {h for h, _, _, _ in w}.isdisjoint(win)
+        assert sum(n for _, _, n, _ in w) + sum(wl.sizes[h - 1] for h in win) == total
+        assert wl.window(1) != wl.window(2)  # fresh bytes every step
+
+
+def test_both_arms_print_the_same_config():
+    """The driver compares the two arms' config dicts."""
+    for name in ("c1", "c5"):
+        wl = bench.Workload(name)
+        assert bench.bench_config(wl, 1) == bench.bench_config(bench.Workload(name), 1)
+        assert "workload" in bench.bench_config(wl, 1)
+
+
+def test_gpus_flag_must_match_world(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2"])
+    with pytest.raises(SystemExit) as ei:
+        bench.main()
+    assert "WORLD_SIZE" in str(ei.value)
 
 
 def test_aggregate_value_is_whole_job():
