@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define POSDUMP_ABI_VERSION 1
+#define POSDUMP_ABI_VERSION 2
 
 enum {
   POS_OK = 0,
@@ -63,6 +63,11 @@ typedef struct pos_config {
   double staging_fraction;   /* staging_fraction (config.hpp:35); 0 => 1/16 */
   int32_t device;            /* CUDA ordinal */
   int32_t dedup;             /* dedup (config.hpp:36) */
+  double dirty_threshold_frac; /* dirty_threshold_frac (config.hpp:32): DAG retention; 0 => 0.25 */
+  int32_t trust_written_bit; /* O2 at buffer granularity first (plan_precopy, cr.hpp:396-401): a buffer
+                                registered with written_since_ckpt == 0 is neither hashed nor shipped
+                                in an incremental round -- exact when the caller tracks every write */
+  int32_t pad;
 } pos_config;
 
 /* One active allocation of the checkpointed process: the fields of
@@ -394,6 +399,61 @@ typedef struct pos_image_desc {
 /* Byte-identical to gpucrsim::write_image.  *size always receives the image
  * size; bytes are written when cap >= size. */
 int pos_image_write(const pos_image_desc* img, uint8_t* out, uint64_t cap, uint64_t* size);
+
+/* ---- finalize_image (cr.hpp:680-764) ----------------------------------- */
+/* One snapshot buffer still live at finalize (a dirty-bit image drops the
+ * buffers freed during the session and the caller leaves them out,
+ * cr.hpp:709-716). */
+typedef struct pos_finalize_buf {
+  uint64_t handle, base, size;     /* its AllocEntry (image.hpp:60-64) */
+  const uint8_t* inline_bytes;     /* captured_[h] (cr.hpp:738-740): the host image range the dump wrote */
+  uint64_t up_host_addr, up_len;   /* dedup_snapshot_[h]: the Upstream scan_dedup saw (cr.hpp:436) */
+  uint32_t up_crc;
+  uint32_t has_upstream;
+  int32_t dedup_ok;                /* scan_dedup's verdict (dedup_ok_, cr.hpp:441); -1: the context's device O1 verdict */
+  uint32_t dirty;                  /* h in dirty_set_ */
+  uint32_t recompute_eligible;     /* recompute_eligible(h) (cr.hpp:938-951): decided by the kernel DAG */
+  uint32_t n_recompute;
+  const uint64_t* recompute_nodes; /* pending_writers(h) (dag.hpp:234-243) */
+  uint32_t precopy_survived;       /* retention_ && fully_copied && !final_outstanding (cr.hpp:741) */
+  uint32_t pad;
+} pos_finalize_buf;
+
+/* CrMetrics (cr.hpp:69-119): the fields the dump path accounts.  For a
+ * dirty-bit checkpoint bytes_precopy + bytes_dirty + bytes_dedup_saved ==
+ * the sum of the image's allocation sizes (tests/test_harness.cpp:99-112). */
+typedef struct pos_metrics {
+  uint64_t bytes_precopy;          /* buffer bytes whose concurrent copy survived */
+  uint64_t bytes_dirty;            /* buffer bytes re-copied at the final stop */
+  uint64_t bytes_dedup_saved;
+  uint64_t bytes_recompute_saved;
+  uint64_t image_bytes;            /* GPU section + DAG section */
+  uint64_t image_file_bytes;
+  uint64_t dirty_count;            /* |dirty_set_| at the final stop */
+  uint64_t retention_dirty_count;
+  uint32_t retention;              /* the DAG-retention threshold was crossed (cr.hpp:921-929) */
+  uint32_t n_inline, n_dedup, n_recompute;
+} pos_metrics;
+
+/* finalize_image: the record kind of every buffer -- DedupRef when the O1
+ * verdict holds, the buffer is not in dirty_set_ and dedup_consistent (a
+ * chained crc32 over the image's host pages equals the Upstream crc,
+ * cr.hpp:692-708); Recompute when dirty and recompute-eligible; else Inline
+ * from captured_ -- then the POSI image (write_image, byte-identical) into
+ * out (*size always receives the image size; bytes are written when cap >=
+ * size) and the session metrics.  `host_side` carries what the CPU side and
+ * the DAG contribute: page_size, host pages, stream ids, cursor,
+ * next_handle / next_base and the DAG bytes (its recs / allocs must be
+ * empty).  ctx may be NULL when no verdict is taken from a device. */
+int pos_finalize_image(pos_ctx* ctx, const pos_image_desc* host_side, const pos_finalize_buf* bufs, uint32_t n,
+                       uint8_t* out, uint64_t cap, uint64_t* size, pos_metrics* metrics);
+/* The context's metrics of the current session (final stop + finalize). */
+int pos_get_metrics(pos_ctx* ctx, pos_metrics* metrics);
+/* at_final_stop's exclusions (cr.hpp:608-613): buffers of dirty_set_ the
+ * final stop does NOT re-copy -- freed before the stop, recompute-eligible,
+ * or (under DAG retention) already fully copied.  Replaces the previous
+ * list; cleared by pos_commit_epoch. */
+int pos_set_stop_exclusions(pos_ctx* ctx, const uint64_t* handles, uint32_t n);
 
 /* read_image (image.hpp:209-361): validate a POSI image on the host -- the
  * reference's checks in its order; POS_E_CORRUPT_IMAGE with the reader

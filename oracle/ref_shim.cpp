@@ -14,12 +14,31 @@
 #include <thread>
 #include <vector>
 
+#include <array>
+#include <deque>
+#include <fstream>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <utility>
+
+#include <json.hpp>
+
+// ref_checkpoint_session reads CrEngine session state that finalize_image
+// consumes but the class keeps private (final_outstanding_, retention_,
+// dedup_snapshot_); every library header is included above, so only the
+// reference's own classes see this.
+#define private public
 #include "gpucrsim/buffer.hpp"
 #include "gpucrsim/crc32.hpp"
 #include "gpucrsim/image.hpp"
 #include "gpucrsim/rng.hpp"
 #include "gpucrsim/workload.hpp"
 #include "gpucrsim/scenario.hpp"
+#undef private
 
 #include <sstream>
 
@@ -234,6 +253,117 @@ uint64_t ref_checkpoint_image(const char* profile, uint64_t total_bytes, uint64_
   std::vector<uint8_t> bytes = write_image(img);
   if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
   return bytes.size();
+}
+
+// The reference engine's finalize_image INPUTS for one checkpoint (the state
+// cr.hpp:680-764 reads), so a test can derive the record kinds itself:
+// checkpoint_at's flow (scenario.hpp:63-78) with resume_after = false, so the
+// process stays exactly as finalize_image saw it when `done` runs.  Blob
+// (little endian): "SESS", u32 n, u64 image_len, image bytes, 8 x u64
+// metrics {bytes_precopy, bytes_dirty, bytes_dedup_saved,
+// bytes_recompute_saved, image_bytes, image_file_bytes, dirty_count,
+// retention}, then per allocation of the image: u64 handle, base, size;
+// u32 has_upstream; u64 up_host_addr, up_len; u32 up_crc, host_untouched;
+// i32 dedup_ok (-1: not scanned); u32 dirty, recompute_eligible, n_pending;
+// u64 pending[n_pending]; u64 content_len; content.  Returns the blob size.
+static bool shim_recompute_eligible(GpuProcess& p, BufferHandle h) {  // restates cr.hpp:938-951
+  auto first = p.dag().first_pending_accessor(h);
+  if (!first) return false;
+  const KernelNode& n = p.dag().at(*first);
+  if (n.kind == ApiKind::LaunchOpaque) return false;
+  bool writes = std::find(n.spec_writes.begin(), n.spec_writes.end(), h) != n.spec_writes.end();
+  bool reads = std::find(n.spec_reads.begin(), n.spec_reads.end(), h) != n.spec_reads.end();
+  if (!writes || reads) return false;
+  for (uint64_t id : p.dag().pending_in_order()) {
+    if (id == *first) break;
+    if (p.dag().at(id).kind == ApiKind::LaunchOpaque) return false;
+  }
+  return true;
+}
+
+static std::vector<ApiCall> shim_trace(const char* profile, uint64_t total_bytes, uint64_t seed) {
+  if (std::string(profile) == "fuzz") return gen_fuzz_trace(seed);
+  WorkloadProfile p = profile_by_name(profile, seed);
+  if (total_bytes) p.total_bytes = total_bytes;
+  return gen_workload(p);
+}
+
+uint64_t ref_checkpoint_session(const char* profile, uint64_t total_bytes, uint64_t seed, int mode, uint8_t* out,
+                                uint64_t cap) {
+  std::vector<ApiCall> trace = shim_trace(profile, total_bytes, seed);
+  SimConfig cfg;
+  SimCell cell(cfg, trace);
+  std::vector<uint8_t> blob;
+  auto put = [&](const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    blob.insert(blob.end(), b, b + n);
+  };
+  auto u32 = [&](uint32_t v) { put(&v, 4); };
+  auto u64 = [&](uint64_t v) { put(&v, 8); };
+  bool fired = false;
+  std::set<BufferHandle> recopied;  // final_outstanding_ as at_final_stop left it
+  auto fire = [&] {
+    cell.cr.checkpoint(static_cast<CrMode>(mode), CheckpointTarget{}, [&](CheckpointImage img) {
+      fired = true;
+      std::vector<uint8_t> bytes = write_image(img);
+      const CrMetrics& m = cell.cr.metrics;
+      put("SESS", 4);
+      u32(static_cast<uint32_t>(img.meta.allocs.size()));
+      u64(bytes.size());
+      put(bytes.data(), bytes.size());
+      for (uint64_t v : {m.bytes_precopy, m.bytes_dirty, m.bytes_dedup_saved, m.bytes_recompute_saved,
+                         m.image_bytes, m.image_file_bytes, m.dirty_count, (uint64_t)m.retention})
+        u64(v);
+      const CrEngine& cr = cell.cr;
+      for (const auto& a : img.meta.allocs) {
+        const GpuBuffer& b = cell.proc.device().at(a.handle);
+        u64(a.handle);
+        u64(a.base);
+        u64(a.size);
+        // dedup_snapshot_ (cr.hpp:436) when scanned, else the live provenance
+        auto ds = cr.dedup_snapshot_.find(a.handle);
+        const std::optional<Upstream> up =
+            ds != cr.dedup_snapshot_.end() ? std::optional<Upstream>(ds->second) : b.upstream;
+        u32(up ? 1 : 0);
+        u64(up ? up->host_addr : 0);
+        u64(up ? up->len : 0);
+        u32(up ? up->crc : 0);
+        u32(up ? (cell.proc.host().range_write_seq(up->host_addr, up->len) <= up->host_write_seq) : 0);
+        const auto& v = cell.cr.dedup_verdicts();
+        auto it = v.find(a.handle);
+        u32(static_cast<uint32_t>(it == v.end() ? -1 : (it->second ? 1 : 0)));
+        u32(cell.cr.dirty_set().count(a.handle) ? 1 : 0);
+        // bit 0: recompute_eligible; bit 1: re-copied at the final stop
+        // (final_outstanding_); bit 2: retention_ && fully_copied && not
+        // re-copied (its pre-copy survived, cr.hpp:741)
+        // (recorded right after at_final_stop ran; retention_ itself is
+        // reset before `done`, metrics.retention keeps it)
+        const bool outstanding = recopied.count(a.handle) > 0;
+        u32((shim_recompute_eligible(cell.proc, a.handle) ? 1u : 0u) | (outstanding ? 2u : 0u) |
+            (m.retention && b.fully_copied() ? 4u : 0u));
+        std::vector<uint64_t> pw = cell.proc.dag().pending_writers(a.handle);
+        u32(static_cast<uint32_t>(pw.size()));
+        for (uint64_t id : pw) u64(id);
+        u64(b.size);
+        put(b.content().data(), b.size);
+      }
+    }, /*resume_after=*/false);
+  };
+  if (!trace.empty() && default_trigger(trace) <= trace.back().seq)
+    cell.runner->set_trigger(default_trigger(trace), fire);
+  else
+    cell.runner->on_finished = fire;
+  cell.runner->start();
+  bool stopped = false;
+  while (cell.clk.step())  // event by event: catch the final stop's re-copy set
+    if (!stopped && cell.cr.phase_ >= CrEngine::Phase::Final && cell.cr.mode_ != CrMode::None &&
+        cell.cr.drained_at_ != 0) {  // at_final_stop has run (it stamps drained_at_)
+      stopped = true;
+      recopied = cell.cr.final_outstanding_;
+    }
+  if (!fired) return 0;
+  if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size());
+  return blob.size();
 }
 
 }  // extern "C"

@@ -8,5 +8,5 @@ from .posdump import (  # noqa: F401
     CheckpointImage, CorruptImageError, DeviceMemory, DumpEngine, GpuBuffer, GpuBufferRec,
     NoDeviceError, PinnedHost, SimConfig, SimError, Stream, Upstream, apply_pack_host, crc32,
     crc32_update, device_count, device_synchronize, fill_batch, fill_bytes, parse_pack,
-    read_image_check, write_image, lib, check,
+    read_image_check, write_image, lib, check, FinalizeBuf, finalize_image,
 )

@@ -45,7 +45,8 @@ class NoDeviceError(SimError):
 class pos_config(C.Structure):
     _fields_ = [("chunk_size", C.c_uint64), ("page_size", C.c_uint64),
                 ("cache_capacity", C.c_uint64), ("staging_fraction", C.c_double),
-                ("device", C.c_int32), ("dedup", C.c_int32)]
+                ("device", C.c_int32), ("dedup", C.c_int32),
+                ("dirty_threshold_frac", C.c_double), ("trust_written_bit", C.c_int32), ("pad", C.c_int32)]
 
 
 class pos_buffer_desc(C.Structure):
@@ -78,6 +79,22 @@ class pos_image_desc(C.Structure):
                 ("stream_ids", C.c_void_p), ("n_streams", C.c_uint32),
                 ("cursor", C.c_uint64), ("next_handle", C.c_uint64), ("next_base", C.c_uint64),
                 ("dag_bytes", C.c_void_p), ("dag_len", C.c_uint64)]
+
+
+class pos_finalize_buf(C.Structure):
+    _fields_ = [("handle", C.c_uint64), ("base", C.c_uint64), ("size", C.c_uint64),
+                ("inline_bytes", C.c_void_p), ("up_host_addr", C.c_uint64), ("up_len", C.c_uint64),
+                ("up_crc", C.c_uint32), ("has_upstream", C.c_uint32), ("dedup_ok", C.c_int32),
+                ("dirty", C.c_uint32), ("recompute_eligible", C.c_uint32), ("n_recompute", C.c_uint32),
+                ("recompute_nodes", C.c_void_p), ("precopy_survived", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class pos_metrics(C.Structure):
+    _fields_ = [("bytes_precopy", C.c_uint64), ("bytes_dirty", C.c_uint64), ("bytes_dedup_saved", C.c_uint64),
+                ("bytes_recompute_saved", C.c_uint64), ("image_bytes", C.c_uint64),
+                ("image_file_bytes", C.c_uint64), ("dirty_count", C.c_uint64),
+                ("retention_dirty_count", C.c_uint64), ("retention", C.c_uint32), ("n_inline", C.c_uint32),
+                ("n_dedup", C.c_uint32), ("n_recompute", C.c_uint32)]
 
 
 P = C.c_void_p
@@ -152,6 +169,9 @@ SIGNATURES = {
     "pos_launch_count": [P, PU64],
     "pos_last_kernel_ms": [P, C.c_char_p, C.POINTER(C.c_float)],
     "pos_image_write": [C.POINTER(pos_image_desc), P, U64, PU64],
+    "pos_finalize_image": [P, C.POINTER(pos_image_desc), P, U32, P, U64, PU64, C.POINTER(pos_metrics)],
+    "pos_get_metrics": [P, C.POINTER(pos_metrics)],
+    "pos_set_stop_exclusions": [P, P, U32],
     "pos_pack_apply_host": [P, U64, P, P, P, U32, U32],
     "pos_device_count": [C.POINTER(C.c_int)],
     "pos_set_device": [I32],

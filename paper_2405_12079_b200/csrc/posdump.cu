@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "image_writer.h"
 #include "image_reader.h"
+#include "host_crc.h"
 
 using namespace posdump;
 
@@ -321,6 +322,8 @@ struct pos_ctx {
   int delta_slots[2] = {-1, -1};  // pos_final_stop: the STW window's events (the delta timer)
   DevArray<uint64_t> d_result;  // async pre-copy: [n, total, overflow, n_items]
   std::set<uint64_t> dirty_set;
+  std::set<uint64_t> stop_excluded;  // at_final_stop's exclusions (pos_set_stop_exclusions)
+  pos_metrics metrics{};             // CrMetrics of the session (final stop + finalize)
   bool dag_uploaded = false;
   uint64_t dirty_version = 0;
   // STW delta staged ahead of the stop (pos_delta_prepare)
@@ -546,3 +549,4 @@ int pos_abi_version(void) { return POSDUMP_ABI_VERSION; }
 #include "delta.inc"
 #include "restore.inc"
 #include "util.inc"
+#include "finalize.inc"

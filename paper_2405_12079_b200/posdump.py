@@ -244,6 +244,8 @@ class SimConfig:
     staging_fraction: float = 1.0 / 16.0
     dedup: bool = True
     cache_capacity: int = 0  # explicit O3 cache size; 0 => staging_capacity of the device
+    dirty_threshold_frac: float = 0.25  # DAG retention (config.hpp:32)
+    trust_written_bit: bool = False  # buffer-level O2 first (cr.hpp:396-401): clean buffers are not hashed
 
 
 class DumpEngine:
@@ -256,6 +258,8 @@ class DumpEngine:
         c.cache_capacity = cfg.cache_capacity
         c.staging_fraction = cfg.staging_fraction
         c.device, c.dedup = device, 1 if cfg.dedup else 0
+        c.dirty_threshold_frac = cfg.dirty_threshold_frac
+        c.trust_written_bit = 1 if cfg.trust_written_bit else 0
         ctx = C.c_void_p(0)
         check(lib().pos_ctx_create(C.byref(c), C.byref(ctx)))
         self.ctx = ctx.value
@@ -342,6 +346,17 @@ class DumpEngine:
         return {b.handle: bool(v) for b, v in zip(self.buffers, ver) if b.upstream is not None}
 
     # ---- DAG write sets (record_dirty, cr.hpp:901-931)
+    def metrics(self) -> dict:
+        """CrMetrics of the session (cr.hpp:69-119): final stop + finalize."""
+        m = _lib.pos_metrics()
+        check(lib().pos_get_metrics(self.ctx, C.byref(m)))
+        return {k: int(getattr(m, k)) for k in METRIC_KEYS}
+
+    def set_stop_exclusions(self, handles: Iterable[int]) -> None:
+        """at_final_stop's exclusions (cr.hpp:608-613)."""
+        a = np.array(sorted(set(handles)), dtype=np.uint64)
+        check(lib().pos_set_stop_exclusions(self.ctx, a.ctypes.data if a.size else None, a.size))
+
     def record_dirty(self, handles: Iterable[int]) -> None:
         a = np.array(list(handles), dtype=np.uint64)
         check(lib().pos_record_dirty(self.ctx, a.ctypes.data if a.size else None, a.size))
@@ -635,6 +650,82 @@ def read_image_check(data: bytes) -> int:
         err.offset = off.value
         raise err
     return 0
+
+
+@dataclass
+class FinalizeBuf:
+    """finalize_image's per-buffer inputs (cr.hpp:715-746): the captured bytes
+    and what the session decided about the buffer."""
+    handle: int
+    base: int
+    size: int
+    inline_bytes: Optional[np.ndarray] = None  # captured_[h]
+    upstream: Optional[tuple] = None  # dedup_snapshot_: (host_addr, len, crc)
+    dedup_ok: Optional[bool] = None  # None: the engine's device O1 verdict
+    dirty: bool = False
+    recompute_eligible: bool = False
+    recompute_nodes: list = field(default_factory=list)  # pending_writers(h)
+    precopy_survived: bool = False
+
+
+METRIC_KEYS = ("bytes_precopy", "bytes_dirty", "bytes_dedup_saved", "bytes_recompute_saved", "image_bytes",
+               "image_file_bytes", "dirty_count", "retention_dirty_count", "retention", "n_inline", "n_dedup",
+               "n_recompute")
+
+
+def _image_desc(img: CheckpointImage, keep: list, with_records: bool = True):
+    pages = (_lib.pos_image_page * max(len(img.host_pages), 1))()
+    for i, (idx, data) in enumerate(img.host_pages):
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8))
+        if a.nbytes != img.page_size:
+            raise SimError(_lib.CODES["InvariantViolation"], "host page size mismatch")
+        keep.append(a)
+        pages[i].index, pages[i].bytes = idx, a.ctypes.data
+    keep.append(pages)
+    streams = np.array(img.stream_ids, dtype=np.uint64)
+    dag = np.frombuffer(img.dag_bytes, dtype=np.uint8) if img.dag_bytes else np.zeros(0, np.uint8)
+    keep += [streams, dag]
+    d = _lib.pos_image_desc()
+    d.page_size = img.page_size
+    d.pages, d.n_pages = C.cast(pages, C.c_void_p), len(img.host_pages)
+    d.stream_ids, d.n_streams = (streams.ctypes.data if streams.size else None), streams.size
+    d.cursor, d.next_handle, d.next_base = img.cursor, img.next_handle, img.next_base
+    d.dag_bytes, d.dag_len = (dag.ctypes.data if dag.size else None), dag.size
+    return d
+
+
+def finalize_image(host_side: CheckpointImage, bufs: Sequence[FinalizeBuf], engine=None) -> tuple[bytes, dict]:
+    """finalize_image (cr.hpp:680-764) through pos_finalize_image: record kinds,
+    dedup_consistent over the image's host pages, the POSI bytes and the
+    session metrics.  host_side supplies the host pages, meta and DAG bytes."""
+    keep: list = []
+    d = _image_desc(host_side, keep)
+    arr = (_lib.pos_finalize_buf * max(len(bufs), 1))()
+    for i, b in enumerate(bufs):
+        f = arr[i]
+        f.handle, f.base, f.size = b.handle, b.base, b.size
+        if b.inline_bytes is not None:
+            a = np.ascontiguousarray(np.asarray(b.inline_bytes, dtype=np.uint8).ravel())
+            keep.append(a)
+            f.inline_bytes = a.ctypes.data
+        if b.upstream is not None:
+            f.up_host_addr, f.up_len, f.up_crc = b.upstream
+            f.has_upstream = 1
+        f.dedup_ok = -1 if b.dedup_ok is None else int(bool(b.dedup_ok))
+        f.dirty, f.recompute_eligible = int(b.dirty), int(b.recompute_eligible)
+        f.precopy_survived = int(b.precopy_survived)
+        if b.recompute_nodes:
+            a = np.array(b.recompute_nodes, dtype=np.uint64)
+            keep.append(a)
+            f.recompute_nodes, f.n_recompute = a.ctypes.data, a.size
+    ctx = engine.ctx if engine is not None else None
+    size = C.c_uint64(0)
+    m = _lib.pos_metrics()
+    check(lib().pos_finalize_image(ctx, C.byref(d), arr, len(bufs), None, 0, C.byref(size), C.byref(m)))
+    out = np.empty(size.value, dtype=np.uint8)
+    check(lib().pos_finalize_image(ctx, C.byref(d), arr, len(bufs), out.ctypes.data, out.nbytes, C.byref(size),
+                                   C.byref(m)))
+    return out.tobytes(), {k: int(getattr(m, k)) for k in METRIC_KEYS}
 
 
 def write_image(img: CheckpointImage) -> bytes:

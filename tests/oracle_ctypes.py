@@ -52,6 +52,7 @@ _REF = {
     "ref_state_captured": (None, [P, U32, P]),
     "ref_gen_workload": (U64, [C.c_char_p, U64, U64, U64, U64, P, U64]),
     "ref_checkpoint_image": (U64, [C.c_char_p, U64, U64, I32, P, U64]),
+    "ref_checkpoint_session": (U64, [C.c_char_p, U64, U64, I32, P, U64]),
 }
 
 
@@ -138,3 +139,40 @@ def ref_image(ref, desc):
     out = np.empty(n, np.uint8)
     ref.ref_write_image(*args, out.ctypes.data, n)
     return out.tobytes()
+
+
+def ref_session(ref, profile: str, seed: int, mode: int, total_bytes: int = 0) -> dict:
+    """The reference CrEngine's finalize_image inputs for one checkpoint
+    (ref_checkpoint_session): the image it wrote, its CrMetrics, and per
+    allocation the device bytes, Upstream, O1 verdict, dirty bit,
+    recompute eligibility and pending writers."""
+    import struct
+    n = ref.ref_checkpoint_session(profile.encode(), total_bytes, seed, mode, None, 0)
+    buf = C.create_string_buffer(n)
+    ref.ref_checkpoint_session(profile.encode(), total_bytes, seed, mode, buf, n)
+    b = buf.raw[:n]
+    assert b[:4] == b"SESS"
+    nb, ilen = struct.unpack_from("<IQ", b, 4)
+    o = 16
+    image = b[o:o + ilen]
+    o += ilen
+    keys = ["bytes_precopy", "bytes_dirty", "bytes_dedup_saved", "bytes_recompute_saved", "image_bytes",
+            "image_file_bytes", "dirty_count", "retention"]
+    metrics = dict(zip(keys, struct.unpack_from("<8Q", b, o)))
+    o += 64
+    bufs = []
+    for _ in range(nb):
+        h, base, size, has_up, up_addr, up_len, up_crc, untouched, ok, dirty, rec, npw = struct.unpack_from(
+            "<QQQIQQIIiIII", b, o)
+        o += struct.calcsize("<QQQIQQIIiIII")
+        pending = list(struct.unpack_from(f"<{npw}Q", b, o))
+        o += 8 * npw
+        (clen,) = struct.unpack_from("<Q", b, o)
+        o += 8
+        content = b[o:o + clen]
+        o += clen
+        bufs.append(dict(handle=h, base=base, size=size, has_upstream=bool(has_up), up_host_addr=up_addr,
+                         up_len=up_len, up_crc=up_crc, host_untouched=bool(untouched), dedup_ok=ok,
+                         dirty=bool(dirty), recompute_eligible=bool(rec & 1), final_recopy=bool(rec & 2),
+                         precopy_survived=bool(rec & 4), pending=pending, content=content))
+    return {"image": image, "metrics": metrics, "bufs": bufs}

@@ -527,63 +527,75 @@ def test_pipelined_precopy_matches_single_pack(orc, waves):
 
 @pytest.mark.parametrize("profile,seed,mode", [
     ("gpt2-infer-desk", 1, 3),    # inference: parameters H2D-loaded -> DedupRef records
-    ("resnet-train-desk", 1, 3),  # training: every buffer Inline / Recompute
+    ("resnet-train-desk", 1, 3),  # training under DAG retention
     ("fuzz", 7, 3),
     ("fuzz", 8, 1),               # stop-the-world image
-    ("ppo-train-desk", 2, 3),
+    ("ppo-train-desk", 2, 3),     # a Recompute record
 ])
 def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode):
-    """Drop-in parity at engine level: the reference's CrEngine checkpoints a
-    trace (checkpoint_at, scenario.hpp:63-78); its image's device state at the
-    cut is loaded onto the GPU, our dump path (O2 + O1 + O3 + D2H + host apply)
-    produces the Inline payloads, our O1 verdict agrees with every DedupRef,
-    and the streaming writer emits the reference image byte for byte."""
-    import ctypes as C
-    from posi import dedup_bytes, read_posi
-    n = ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, None, 0)
-    buf = C.create_string_buffer(n)
-    ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, buf, n)
-    want = buf.raw[:n]
-    img = read_posi(want)
-    allocs = {h: size for h, base, size in img["meta"]["allocs"]}
-    mems, bufs, kinds = [], [], {}
-    for r in img["recs"]:
-        h, size = r["handle"], allocs[r["handle"]]
-        kinds[h] = r["kind"]
-        if r["kind"] == 2:
-            continue  # Recompute: regenerated by DAG replay (out of the dump path)
-        content = r["inline"] if r["kind"] == 0 else dedup_bytes(img, r, size)
-        m = pd.DeviceMemory(size)
-        m.upload(np.frombuffer(content, np.uint8))
-        b = pd.GpuBuffer(handle=h, dev_ptr=m.ptr, size=size)
-        if r["kind"] == 1:  # H2D provenance with an untouched host range
-            b.upstream = pd.Upstream(r["crc"], True)
+    """Drop-in parity at engine level (P3 + P4): the reference CrEngine
+    checkpoints a trace (checkpoint_at's flow, scenario.hpp:63-78); the
+    device state at its cut is loaded onto the GPU with the session's
+    provenance and DAG decisions (dirty_set_, recompute eligibility, final
+    stop re-copies).  OUR path then does the rest: O2 + O1 verdicts on the
+    device, the direct pre-copy into a pinned image, the STW delta + drain,
+    and pos_finalize_image picks every record kind from the device verdicts
+    and writes the image -- byte for byte the reference's, with the same
+    CrMetrics.  Nothing is read from the reference's output image except the
+    host-side sections (host pages, DAG, meta)."""
+    from oracle_ctypes import ref_session
+    from posi import read_posi
+    from test_finalize import host_side
+    sess = ref_session(ref, profile, seed, mode)
+    img = read_posi(sess["image"])
+    mems, bufs = [], []
+    for r in sess["bufs"]:
+        m = pd.DeviceMemory(r["size"])
+        m.upload(np.frombuffer(r["content"], np.uint8))
+        b = pd.GpuBuffer(handle=r["handle"], dev_ptr=m.ptr, size=r["size"])
+        if r["has_upstream"]:  # note_h2d_provenance's record (process.hpp:505-522)
+            b.upstream = pd.Upstream(r["up_crc"], r["host_untouched"])
         mems.append(m)
         bufs.append(b)
+    pd.device_synchronize()
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=64 << 20))
     eng.register_buffers(bufs)
-    nbytes = eng.plan_precopy()
+    image = [np.zeros(b.size, np.uint8) for b in bufs]
+    eng.register_image(image)
+    by_h = {r["handle"]: r for r in sess["bufs"]}
+    # the DAG's view: buffers re-copied at the final stop are dirty during the
+    # pre-copy; recompute-eligible dirty ones are dirty AND skipped by the stop
+    recopy = [h for h, r in by_h.items() if r["final_recopy"]]
+    recompute = [h for h, r in by_h.items() if r["dirty"] and r["recompute_eligible"]]
+    eng.record_dirty(recopy + recompute)
+    eng.set_stop_exclusions(recompute)
+    s, d = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=2, stream=s, drain_stream=d)
+    eng.precopy_direct_result()
+    d.synchronize()
+    eng.at_final_stop(stream=s)
+    d.wait(s)
+    eng.delta_drain(stream=d)
+    d.synchronize()
+    s.synchronize()
     verdicts = eng.dedup_verdicts()
-    assert all(verdicts[h] for h, k in kinds.items() if k == 1)
-    captured = [np.zeros(b.size, np.uint8) for b in eng.buffers]
-    pd.apply_pack_host(download_cache(eng, 0, nbytes), [b.handle for b in eng.buffers], captured)
-    by_h = {b.handle: c for b, c in zip(eng.buffers, captured)}
-    out = pd.CheckpointImage(page_size=img["page_size"])
-    out.host_pages = img["pages"]
-    for r in img["recs"]:
-        if r["kind"] == 0:
-            out.gpu_records.append(pd.GpuBufferRec(r["handle"], 0, inline_bytes=by_h[r["handle"]]))
-        elif r["kind"] == 1:
-            out.gpu_records.append(pd.GpuBufferRec(r["handle"], 1, dedup_first_page=r["first_page"],
-                                                   dedup_page_count=r["page_count"],
-                                                   dedup_offset=r["offset"], dedup_crc=r["crc"]))
-        else:
-            out.gpu_records.append(pd.GpuBufferRec(r["handle"], 2, recompute_nodes=r["nodes"]))
-    out.dag_bytes = bytes(img["dag"])
-    m = img["meta"]
-    out.stream_ids, out.allocs = m["streams"], [tuple(a) for a in m["allocs"]]
-    out.cursor, out.next_handle, out.next_base = m["cursor"], m["next_handle"], m["next_base"]
-    assert pd.write_image(out) == want
+    for h, r in by_h.items():  # P3: the device O1 verdict == scan_dedup's (cr.hpp:416-445)
+        if r["dedup_ok"] >= 0 and not r["dirty"]:
+            assert verdicts[h] == (r["dedup_ok"] == 1), h
+    fb = [pd.FinalizeBuf(handle=r["handle"], base=r["base"], size=r["size"], inline_bytes=a,
+                         upstream=(r["up_host_addr"], r["up_len"], r["up_crc"]) if r["has_upstream"] else None,
+                         dedup_ok=None, dirty=r["dirty"], recompute_eligible=r["recompute_eligible"],
+                         recompute_nodes=r["pending"], precopy_survived=r["precopy_survived"])
+          for r, a in zip(sess["bufs"], image)]
+    out, m = pd.finalize_image(host_side(img), fb, engine=eng)
+    assert out == sess["image"]
+    want = sess["metrics"]
+    for k in ("bytes_precopy", "bytes_dirty", "bytes_dedup_saved", "bytes_recompute_saved", "image_bytes",
+              "image_file_bytes"):
+        assert m[k] == want[k], k
+    assert eng.metrics()["image_file_bytes"] == len(out)
+    if mode == 3:  # closure identity (tests/test_harness.cpp:99-112)
+        assert m["bytes_precopy"] + m["bytes_dirty"] + m["bytes_dedup_saved"] == sum(b.size for b in bufs)
     eng.close()
 
 
