@@ -103,6 +103,19 @@ void or_fill_bytes(uint64_t seed, uint8_t* out, size_t n) {
   }
 }
 
+/* Bytes [off, off+n) of fill_bytes(seed) over a buffer of at least off+n
+ * bytes (rng.hpp:43-54): byte i is byte i%8 of the (i/8+1)-th next(), i.e.
+ * the SplitMix64 state seed + (i/8+1)*gamma (rng.hpp:15-20) -- random access
+ * into a state the size of a GPU without generating its prefix. */
+void or_fill_bytes_at(uint64_t seed, uint64_t off, uint8_t* out, size_t n) {
+  for (size_t i = 0; i < n;) {
+    const uint64_t w = (off + i) / 8;
+    uint64_t st = seed + w * 0x9e3779b97f4a7c15ull;
+    const uint64_t v = or_splitmix_next(&st);
+    for (unsigned k = (unsigned)((off + i) % 8); k < 8 && i < n; ++k) out[i++] = (uint8_t)(v >> (8 * k));
+  }
+}
+
 /* include/gpucrsim/rng.hpp:63-70 */
 uint64_t or_fnv1a(const void* data, size_t n, uint64_t h) {
   const uint8_t* p = (const uint8_t*)data;

@@ -35,6 +35,8 @@ uint32_t or_crc32_combine(uint32_t crc_a, uint32_t crc_b, uint64_t len_b);
 uint64_t or_splitmix_next(uint64_t* state);
 uint64_t or_mix64(uint64_t a, uint64_t b);
 void or_fill_bytes(uint64_t seed, uint8_t* out, size_t n);
+/* bytes [off, off+n) of fill_bytes(seed) (random access by SplitMix64 state) */
+void or_fill_bytes_at(uint64_t seed, uint64_t off, uint8_t* out, size_t n);
 uint64_t or_fnv1a(const void* data, size_t n, uint64_t h);
 
 /* ---- chunk geometry: include/gpucrsim/buffer.hpp:44-49, :119 ----------- */

@@ -366,4 +366,74 @@ uint64_t ref_checkpoint_session(const char* profile, uint64_t total_bytes, uint6
   return blob.size();
 }
 
+// ---- P5: restore parity (scenario.hpp:51-90, process.hpp:65-90) ----------
+
+uint64_t ref_fnv1a_u64(uint64_t v, uint64_t h) { return fnv1a_u64(v, h); }
+
+// StateSnapshot::hash (process.hpp:76-89) of a state given as arrays:
+// buffers (ascending handle) and host pages (only non-zero ones count).
+uint64_t ref_snapshot_hash(uint32_t nb, const uint64_t* handles, const uint64_t* bases, const uint64_t* sizes,
+                           const uint8_t* const* contents, uint32_t np, const uint64_t* idx,
+                           const uint8_t* const* pages, uint64_t page_size) {
+  StateSnapshot s;
+  for (uint32_t i = 0; i < nb; ++i) {
+    StateSnapshot::Buf b;
+    b.base = bases[i];
+    b.size = sizes[i];
+    b.content.assign(contents[i], contents[i] + sizes[i]);
+    s.buffers[handles[i]] = std::move(b);
+  }
+  for (uint32_t i = 0; i < np; ++i) {
+    std::vector<uint8_t> v(pages[i], pages[i] + page_size);
+    if (std::any_of(v.begin(), v.end(), [](uint8_t x) { return x != 0; })) s.pages[idx[i]] = std::move(v);
+  }
+  return s.hash();
+}
+
+// restore_state(read_image(img), cfg, Full).hash() (scenario.hpp:81-90).
+uint64_t ref_restore_hash(const uint8_t* img, uint64_t n) {
+  SimConfig cfg;
+  return restore_state(read_image(std::vector<uint8_t>(img, img + n)), cfg, RestoreKind::Full).hash();
+}
+
+// plain_final_state(trace, cfg, limit).hash() (scenario.hpp:51-58).
+uint64_t ref_plain_hash(const char* profile, uint64_t total_bytes, uint64_t seed, uint64_t limit) {
+  SimConfig cfg;
+  return plain_final_state(shim_trace(profile, total_bytes, seed), cfg, limit).hash();
+}
+
+// The delta-restore replay plan of an image (replay_pending, cr.hpp:1099-1101):
+// its DAG's pending nodes in order.  Per node: u32 kind (ApiKind), u32
+// name_len, name, u64 seq, u64 dst, u64 src, u64 bytes, u32 nr, u64
+// true_reads[nr], u32 nw, u64 true_writes[nw].  Returns the blob size.
+uint64_t ref_replay_plan(const uint8_t* img, uint64_t n, uint8_t* out, uint64_t cap) {
+  CheckpointImage im = read_image(std::vector<uint8_t>(img, img + n));
+  std::vector<uint8_t> blob;
+  auto put = [&](const void* p, size_t k) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    blob.insert(blob.end(), b, b + k);
+  };
+  auto u32 = [&](uint32_t v) { put(&v, 4); };
+  auto u64 = [&](uint64_t v) { put(&v, 8); };
+  if (!im.dag_bytes.empty()) {
+    KernelDag dag = KernelDag::deserialize(im.dag_bytes);
+    for (uint64_t id : dag.pending_in_order()) {
+      const KernelNode& k = dag.at(id);
+      u32(static_cast<uint32_t>(k.kind));
+      u32(static_cast<uint32_t>(k.name.size()));
+      put(k.name.data(), k.name.size());
+      u64(k.seq);
+      u64(k.args.size() > 0 ? k.args[0].v : 0);
+      u64(k.args.size() > 1 ? k.args[1].v : 0);
+      u64(k.bytes);
+      u32(static_cast<uint32_t>(k.true_reads.size()));
+      for (auto h : k.true_reads) u64(h);
+      u32(static_cast<uint32_t>(k.true_writes.size()));
+      for (auto h : k.true_writes) u64(h);
+    }
+  }
+  if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size());
+  return blob.size();
+}
+
 }  // extern "C"

@@ -76,7 +76,7 @@ struct HashParams {
   uint8_t* flags;
   uint32_t* bitmap;
   int prev_valid;
-  int pad1;
+  int skip_clean;            // buffer-level O2 first (cr.hpp:396-401): !written_since_ckpt => not hashed
   // COPY mode
   const uint4* work;         // {g, entry, dst_off lo, dst_off hi}
   uint8_t* pack;             // pack base
@@ -657,6 +657,19 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
       if (it + stride < n_units) cm_next = p.chunk_map[p.item_base + (nseg == 1 ? it + stride : (it + stride) / nseg)];
     }
     const DevBuf& b = p.bufs[cm.x];
+    // plan_precopy's O2 branch (cr.hpp:396-401): a buffer nothing wrote since
+    // the last checkpoint is captured without a copy -- and, trusting the
+    // bit, without a hash: its digests carry over, nothing ships.  (Every
+    // warp of a segment group takes the same branch: no barrier is skipped
+    // by half a group.)
+    if (!WORK && p.skip_clean && p.prev_valid &&
+        !(b.flags & (kBufWrittenSinceCkpt | kBufFresh | kBufStaged))) {
+      if (lane == 31 && (nseg == 1 || my_seg == 0)) {
+        p.digest_cur[g] = p.digest_prev[g];
+        if (p.flags) p.flags[g] = 0;
+      }
+      continue;
+    }
     const uint64_t start = (uint64_t)cm.y * p.chunk_size;
     const bool last = cm.y + 1 == b.nchunks;
     const uint64_t len = last ? b.size - start : p.chunk_size;
@@ -759,6 +772,12 @@ __device__ __forceinline__ uint32_t warp_fold_buffer(const DevBuf& b, const uint
     crc = __shfl_sync(0xffffffffu, crc, 0);
   }
   return multmodp(b.x8_tail, crc) ^ d[nfull];
+}
+
+// finalize_image clears written_since_ckpt of every buffer (cr.hpp:745).
+__global__ void k_clear_written(DevBuf* bufs, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) bufs[i].flags &= ~kBufWrittenSinceCkpt;
 }
 
 // O1: whole-buffer CRC (crc32_combine fold of the chunk digests, one warp

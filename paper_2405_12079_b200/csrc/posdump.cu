@@ -215,6 +215,7 @@ struct CrcTables {
     ck(cudaFuncGetAttributes(&fa, k_pack_items), "load k_pack_items");
     ck(cudaFuncGetAttributes(&fa, k_buffer_crc), "load k_buffer_crc");
     ck(cudaFuncGetAttributes(&fa, k_note_upstream), "load k_note_upstream");
+    ck(cudaFuncGetAttributes(&fa, k_clear_written), "load k_clear_written");
     ck(cudaFuncGetAttributes(&fa, k_fill), "load k_fill");
     ck(cudaFuncGetAttributes(&fa, k_stage_in), "load k_stage_in");
     ck(cudaFuncGetAttributes(&fa, k_stamp), "load k_stamp");

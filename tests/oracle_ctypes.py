@@ -24,6 +24,7 @@ _ORACLE = {
     "or_splitmix_next": (U64, [C.POINTER(U64)]),
     "or_mix64": (U64, [U64, U64]),
     "or_fill_bytes": (None, [U64, P, C.c_size_t]),
+    "or_fill_bytes_at": (None, [U64, U64, P, C.c_size_t]),
     "or_fnv1a": (U64, [P, C.c_size_t, U64]),
     "or_chunk_count": (U32, [U64, U64]),
     "or_chunk_bytes": (U64, [U64, U64, U32]),
@@ -53,6 +54,11 @@ _REF = {
     "ref_gen_workload": (U64, [C.c_char_p, U64, U64, U64, U64, P, U64]),
     "ref_checkpoint_image": (U64, [C.c_char_p, U64, U64, I32, P, U64]),
     "ref_checkpoint_session": (U64, [C.c_char_p, U64, U64, I32, P, U64]),
+    "ref_fnv1a_u64": (U64, [U64, U64]),
+    "ref_snapshot_hash": (U64, [U32, P, P, P, P, U32, P, P, U64]),
+    "ref_restore_hash": (U64, [P, U64]),
+    "ref_plain_hash": (U64, [C.c_char_p, U64, U64, U64]),
+    "ref_replay_plan": (U64, [P, U64, P, U64]),
 }
 
 
@@ -176,3 +182,33 @@ def ref_session(ref, profile: str, seed: int, mode: int, total_bytes: int = 0) -
                          dirty=bool(dirty), recompute_eligible=bool(rec & 1), final_recopy=bool(rec & 2),
                          precopy_survived=bool(rec & 4), pending=pending, content=content))
     return {"image": image, "metrics": metrics, "bufs": bufs}
+
+
+API_KINDS = ["Malloc", "Free", "MemcpyH2D", "MemcpyD2H", "MemcpyD2D", "LaunchKnown", "LaunchOpaque",
+             "StreamCreate", "StreamDestroy", "DeviceSynchronize", "StreamSynchronize", "GetDevice"]
+
+
+def ref_replay_plan(ref, image: bytes) -> list:
+    """Pending DAG nodes of an image, in replay order (replay_pending)."""
+    import struct
+    src = C.create_string_buffer(image, len(image))
+    n = ref.ref_replay_plan(src, len(image), None, 0)
+    buf = C.create_string_buffer(max(n, 1))
+    ref.ref_replay_plan(src, len(image), buf, n)
+    b, o, out = buf.raw[:n], 0, []
+    while o < n:
+        kind, ln = struct.unpack_from("<II", b, o)
+        o += 8
+        name = b[o:o + ln]
+        o += ln
+        seq, dst, srcp, nbytes = struct.unpack_from("<QQQQ", b, o)
+        o += 32
+        (nr,) = struct.unpack_from("<I", b, o)
+        reads = list(struct.unpack_from(f"<{nr}Q", b, o + 4))
+        o += 4 + 8 * nr
+        (nw,) = struct.unpack_from("<I", b, o)
+        writes = list(struct.unpack_from(f"<{nw}Q", b, o + 4))
+        o += 4 + 8 * nw
+        out.append(dict(kind=API_KINDS[kind], name=name, seq=seq, dst=dst, src=srcp, bytes=nbytes,
+                        reads=reads, writes=writes))
+    return out

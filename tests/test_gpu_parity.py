@@ -1288,3 +1288,106 @@ def test_scatter_rejects_misaligned_payloads(orc):
             eng.restore_packs([bad])
         assert ei.value.errc == "CorruptImage", mutate
     eng.close()
+
+
+@pytest.mark.parametrize("trust", [True, False])
+def test_buffer_level_o2_skip(orc, trust):
+    """plan_precopy's O2 branch (cr.hpp:396-401) with trust_written_bit: in an
+    incremental round a buffer with written_since_ckpt == 0 is neither hashed
+    nor shipped (its digests carry over), even if its bytes changed behind
+    the engine's back -- the bit is trusted, as the reference trusts it.
+    finalize clears the bit (cr.hpp:745); a written buffer is hashed at chunk
+    granularity.  Without trust every chunk is hashed (the CRC decides)."""
+    cs = 4096
+    p = Proc(orc, [cs * 8, cs * 8 + 100, cs * 3], seed0=7100)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20, trust_written_bit=trust))
+    eng.register_buffers(p.bufs)
+    eng.hash_chunks()
+    d0 = eng.digests()
+    eng.commit_epoch()                      # epoch 0 done: every written bit cleared
+    p.write(0, cs * 2, cs, 7200)            # buffer 0: written and reported
+    p.bufs[0].written_since_ckpt = True
+    eng.update_buffer(p.bufs[0])
+    p.write(1, cs * 5, 10, 7201)            # buffer 1: changed, NOT reported
+    pd.device_synchronize()
+    eng.hash_chunks()
+    flags = eng.flags()
+    dig = eng.digests()
+    base1, base2 = 8, 8 + 9
+    want0 = odigests(orc, p.host[0], cs)
+    assert np.array_equal(dig[:8], want0) and list(np.nonzero(flags[:8])[0]) == [2]
+    if trust:  # buffer 1 was not hashed: previous digests, nothing to ship
+        assert np.array_equal(dig[base1:base2], d0[base1:base2]) and not flags[base1:base2].any()
+    else:
+        assert np.array_equal(dig[base1:base2], odigests(orc, p.host[1], cs))
+        assert list(np.nonzero(flags[base1:base2])[0]) == [5]
+    assert not flags[base2:].any()
+    eng.commit_epoch()
+    eng.hash_chunks()  # nothing written since: with trust, nothing hashed at all
+    assert not eng.flags().any() or not trust
+    eng.close()
+
+
+@pytest.mark.parametrize("profile,seed,mode", [
+    ("gpt2-infer-desk", 1, 3),    # DedupRef records, nothing pending
+    ("resnet-train-desk", 1, 3),  # 35 retained kernels to replay
+    ("fuzz", 7, 3),               # opaque + known kernels pending
+    ("fuzz", 8, 1),               # stop-the-world image
+    ("ppo-train-desk", 2, 3),     # a Recompute record, 591 kernels pending
+])
+def test_restore_state_parity(ref, profile, seed, mode):
+    """P5: the state after OUR restore (pos_image_restore:
+    Inline + DedupRef scattered onto device buffers, Recompute left to the
+    replay) followed by the delta-restore replay of the image's pending
+    kernels (replay_pending, cr.hpp:1099-1101; each kernel's effect =
+    apply_kernel_effect, process.hpp:244-261: FNV-1a of name, seq and the
+    read set's DEVICE bytes, then k_fill of every write with
+    mix64(digest, h)) hashes (StateSnapshot::hash, process.hpp:76-89) to
+    restore_state(img, Full) AND to plain_final_state(trace, cursor)
+    (scenario.hpp:51-90)."""
+    import ctypes as C
+    from oracle_ctypes import ref_replay_plan
+    from posi import read_posi
+    n = ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, None, 0)
+    raw = C.create_string_buffer(n)
+    ref.ref_checkpoint_image(profile.encode(), 0, seed, mode, raw, n)
+    img_bytes = raw.raw[:n]
+    im = read_posi(img_bytes)
+    allocs = sorted(im["meta"]["allocs"])
+    mems, bufs, dev = [], [], {}
+    for h, base, size in allocs:
+        m = pd.DeviceMemory(size)
+        pd.check(pd.lib().pos_memset(m.ptr, 0, size, None))
+        mems.append(m)
+        bufs.append(pd.GpuBuffer(handle=h, dev_ptr=m.ptr, size=size))
+        dev[h] = m
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=1 << 20))
+    eng.register_buffers(bufs)
+    loaded, recompute = eng.restore_image(img_bytes)
+    kinds = [r["kind"] for r in im["recs"]]
+    assert loaded == kinds.count(0) + kinds.count(1) and recompute == kinds.count(2)
+    plan = ref_replay_plan(ref, img_bytes)
+    assert all(p["kind"] in ("LaunchKnown", "LaunchOpaque") for p in plan)
+    for p in plan:  # the application's replay of its pending kernels
+        digest = ref.ref_fnv1a(p["name"], len(p["name"]), ref.ref_fnv1a_u64(p["seq"], 0xCBF29CE484222325))
+        for h in sorted(p["reads"]):
+            c = dev[h].download()
+            digest = ref.ref_fnv1a_u64(h, digest)
+            digest = ref.ref_fnv1a(c.ctypes.data, c.size, digest)
+        pd.fill_batch([(dev[h].ptr, dev[h].nbytes, ref.ref_mix64(digest, h)) for h in sorted(p["writes"])])
+        pd.device_synchronize()
+    contents = [dev[h].download() for h, _, _ in allocs]
+    handles = np.array([h for h, _, _ in allocs], np.uint64)
+    bases = np.array([b for _, b, _ in allocs], np.uint64)
+    sizes = np.array([s for _, _, s in allocs], np.uint64)
+    cptrs = (C.c_void_p * max(len(allocs), 1))(*[c.ctypes.data for c in contents])
+    pages = [np.frombuffer(b, np.uint8) for _, b in im["pages"]]
+    pidx = np.array([i for i, _ in im["pages"]], np.uint64)
+    pptrs = (C.c_void_p * max(len(pages), 1))(*[p.ctypes.data for p in pages])
+    ours = ref.ref_snapshot_hash(len(allocs), handles.ctypes.data, bases.ctypes.data, sizes.ctypes.data, cptrs,
+                                 len(pages), pidx.ctypes.data if pages else None, pptrs, im["page_size"])
+    src = C.create_string_buffer(img_bytes, len(img_bytes))
+    assert ours == ref.ref_restore_hash(src, len(img_bytes))
+    assert ours == ref.ref_plain_hash(profile.encode(), 0, seed, im["meta"]["cursor"])
+    eng.close()
