@@ -458,8 +458,10 @@ int pos_set_stop_exclusions(pos_ctx* ctx, const uint64_t* handles, uint32_t n);
 /* read_image (image.hpp:209-361): validate a POSI image on the host -- the
  * reference's checks in its order; POS_E_CORRUPT_IMAGE with the reader
  * offset of its CorruptImageError in *corrupt_offset.  The DAG section is
- * opaque here (its structure belongs to the kernel DAG): a corrupt DAG body,
- * and recompute nodes missing from a non-empty DAG, are not detected. */
+ * checked as KernelDag::deserialize reads it (dag.hpp:322-387: node and edge
+ * records, kinds, lengths, trailing bytes; a bad structure reports offset 0
+ * like read_image's "dag: ..." rethrow) and every Recompute node must be a
+ * kernel of it. */
 int pos_image_check(const uint8_t* img, uint64_t size, uint64_t* corrupt_offset);
 /* Restore from a POSI image (read_image + install/materialize, cr.hpp:
  * 1026-1030, dedup_content image.hpp:364-376): validate it in full (dedup

@@ -1,12 +1,11 @@
 // image_reader.h -- POSI v1 reader with read_image's validation
 // (include/gpucrsim/image.hpp:209-361, ByteReader bytes.hpp:43-98): the same
 // checks in the same order, failing with the reader position the reference's
-// CorruptImageError carries.  The DAG section is kept as opaque bytes: its
-// internal structure belongs to the kernel DAG (out of scope), so a corrupt
-// DAG body and "recompute node missing from a non-empty dag" are not detected
-// here (with an empty DAG every recompute node is missing, as in the
-// reference).  DedupRef checksums are verified when `verify_dedup` is set
-// (host CRC-32, crc32.hpp:26-34).
+// CorruptImageError carries.  The DAG section's structure is validated as
+// KernelDag::deserialize does (posi_check_dag) and recompute nodes must exist
+// in it; the DAG itself is not rebuilt (the kernel DAG is out of scope).
+// DedupRef checksums are verified when `verify_dedup` is set (host CRC-32,
+// crc32.hpp:26-34).
 #pragma once
 #include <cstdint>
 #include <cstring>
@@ -99,6 +98,65 @@ class PosiReader {
   const uint8_t* d_;
   uint64_t n_, pos_ = 0;
 };
+
+// The KDAG section's structure, as read_image checks it through
+// KernelDag::deserialize (dag.hpp:322-387; image.hpp:309-319): node records
+// (buffer u64 | kernel: id, seq, stream, api kind < 12, name, duration,
+// bytes, args x 12 B, four u64 vectors, state <= 2), each exactly its
+// declared length, then the edge table (kind <= 2) and nothing after it.
+// A bounded read that runs out fails like the reference's ByteReader -- a
+// CorruptImageError at the position inside the DAG bytes, rethrown as is;
+// a structural error is CorruptDag, which read_image reports at offset 0 as
+// "dag: ...".  Returns the kernel node ids (the recompute lists' domain).
+inline std::set<uint64_t> posi_check_dag(const uint8_t* d, uint64_t n) {
+  PosiReader rd(d, n);
+  auto corrupt_dag = [](const std::string& why) -> void { throw PosiCorrupt{0, "dag: " + why}; };
+  auto vec = [&rd]() {
+    const uint32_t k = rd.load<uint32_t>();
+    if ((uint64_t)k * 8 > rd.remaining()) rd.fail("vector length past end");
+    rd.take((uint64_t)k * 8);
+  };
+  if (std::memcmp(rd.take(4), "KDAG", 4) != 0) corrupt_dag("bad magic");
+  if (rd.load<uint32_t>() != 1) corrupt_dag("unsupported version");
+  const uint32_t count = rd.load<uint32_t>();
+  std::set<uint64_t> ids;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t len = rd.load<uint32_t>();
+    if (len > rd.remaining()) corrupt_dag("node record past end");
+    const uint64_t end = rd.pos() + len;
+    const uint8_t kind = rd.u8();
+    if (kind == 0) {
+      rd.load<uint64_t>();
+    } else if (kind == 1) {
+      const uint64_t id = rd.load<uint64_t>();
+      rd.load<uint64_t>();  // seq
+      rd.load<uint64_t>();  // stream
+      if (rd.u8() >= 12) corrupt_dag("bad api kind");
+      const uint32_t name = rd.load<uint32_t>();
+      if (name > rd.remaining()) rd.fail("string length past end");
+      rd.take(name);
+      rd.load<uint64_t>();  // duration
+      rd.load<uint64_t>();  // bytes
+      const uint32_t na = rd.load<uint32_t>();
+      if ((uint64_t)na * 12 > rd.remaining()) corrupt_dag("arg vector past end");
+      rd.take((uint64_t)na * 12);
+      for (int v = 0; v < 4; ++v) vec();  // spec reads/writes, true reads/writes
+      if (rd.u8() > 2) corrupt_dag("bad node state");
+      ids.insert(id);
+    } else {
+      corrupt_dag("bad node kind");
+    }
+    if (rd.pos() != end) corrupt_dag("node record length mismatch");
+  }
+  const uint32_t ne = rd.load<uint32_t>();
+  if ((uint64_t)ne * 17 > rd.remaining()) corrupt_dag("edge table past end");
+  for (uint32_t i = 0; i < ne; ++i) {
+    rd.take(16);
+    if (rd.u8() > 2) corrupt_dag("bad edge kind");
+  }
+  if (rd.remaining() != 0) corrupt_dag("trailing bytes");
+  return ids;
+}
 
 // Dedup content of record r (image.hpp:364-376) into out (size bytes).
 inline bool posi_dedup_bytes(const PosiImage& img, const PosiRecord& r, uint64_t size, uint8_t* out) {
@@ -209,6 +267,11 @@ inline PosiImage posi_read(const uint8_t* bytes, uint64_t size, bool verify_dedu
     if (a.size == 0) rd.fail("zero-size allocation");
     if (!allocs.emplace(a.handle, &a).second) rd.fail("duplicate allocation entry");
   }
+  std::set<uint64_t> dag_nodes;
+  if (img.dag_len) {
+    dag_nodes = posi_check_dag(img.dag, img.dag_len);
+    if (dag_nodes.empty()) rd.fail("dag flag set but dag has no kernels");
+  }
   std::vector<uint8_t> scratch;
   for (const auto& r : img.recs) {
     auto it = allocs.find(r.handle);
@@ -229,7 +292,8 @@ inline PosiImage posi_read(const uint8_t* bytes, uint64_t size, bool verify_dedu
       }
     } else {
       if (r.nodes.empty()) rd.fail("empty recompute list");
-      if (img.dag_len == 0) rd.fail("recompute node missing from dag");
+      for (uint64_t id : r.nodes)
+        if (!dag_nodes.count(id)) rd.fail("recompute node missing from dag");
     }
   }
   return img;

@@ -180,11 +180,65 @@ def _ours_check(data: bytes) -> int:
         return 1 + e.offset
 
 
+def test_read_image_check_dag_section_matches_reference(ref):
+    """read_image's DAG validation (image.hpp:309-319 -> KernelDag::deserialize,
+    dag.hpp:322-387; recompute nodes, :355-356): the reference engine's own
+    images (real KDAG sections, Recompute records) and ~3000 mutations
+    confined to their DAG section or the recompute node ids -- same
+    accept/reject, same CorruptImageError offset (DAG-relative for a
+    truncated read, 0 for a structural error, the image end for the
+    cross-section checks).  Plus 300 images with random DAG bytes."""
+    import struct
+    from oracle_ctypes import ref_image
+    from posi import read_posi
+    rng = np.random.default_rng(91)
+    cases = []
+    for prof, seed, mode in [("resnet-train-desk", 1, 3), ("fuzz", 7, 3), ("ppo-train-desk", 2, 3),
+                             ("gpt2-infer-desk", 1, 3)]:
+        n = ref.ref_checkpoint_image(prof.encode(), 0, seed, mode, None, 0)
+        buf = C.create_string_buffer(n)
+        ref.ref_checkpoint_image(prof.encode(), 0, seed, mode, buf, n)
+        data = buf.raw[:n]
+        cases.append(data)
+        dag_len, meta_len = struct.unpack_from("<QQ", data, 40)
+        dag_lo = n - meta_len - dag_len
+        for _ in range(700 if dag_len else 0):
+            b = bytearray(data)
+            k = int(rng.integers(0, 4))
+            i = dag_lo + int(rng.integers(0, dag_len))
+            if k == 0:
+                b[i] ^= 1 << int(rng.integers(0, 8))
+            elif k == 1:  # small length fields: make a count/len word large or small
+                b[i] = int(rng.integers(0, 256))
+            elif k == 2:  # a word of the header region of a node record
+                j = dag_lo + int(rng.integers(0, min(dag_len, 64)))
+                b[j] ^= 0xFF
+            else:  # a recompute node id (Recompute records only exist in ppo)
+                im = read_posi(data)
+                rec = [r for r in im["recs"] if r["kind"] == 2]
+                if not rec:
+                    continue
+                pos = data.index(struct.pack("<Q", rec[0]["nodes"][0]), 64)
+                b[pos] ^= 1
+            cases.append(bytes(b))
+    for _ in range(300):
+        d = _random_desc(rng)
+        d["dag"] = bytes(rng.integers(0, 256, int(rng.integers(1, 40)), dtype=np.uint8)).hex()
+        cases.append(ref_image(ref, d))
+    n_bad = 0
+    for c in cases:
+        arr = np.frombuffer(c, np.uint8)
+        want = ref.ref_read_image_check(arr.ctypes.data, arr.size)
+        assert _ours_check(c) == want, len(c)
+        n_bad += want != 0
+    assert n_bad > 500
+
+
 def test_read_image_check_matches_reference(orc, ref):
-    """read_image (image.hpp:209-361): on 300 writer-generated images (no DAG:
-    its body is opaque to us) and ~4000 corruptions of them -- byte flips,
-    truncations, appended bytes -- our validator accepts exactly what the
-    reference accepts and reports the same CorruptImageError offset."""
+    """read_image (image.hpp:209-361): on 300 writer-generated images and ~4000
+    corruptions of them -- byte flips, truncations, appended bytes -- our
+    validator accepts exactly what the reference accepts and reports the
+    same CorruptImageError offset (DAG sections: the test above)."""
     from oracle_ctypes import ref_image
     rng = np.random.default_rng(77)
     n_valid = n_checked = 0
