@@ -51,11 +51,11 @@ inline int run(int argc, char** argv) {
   static void MC_CAT(mc_test_, __LINE__)()
 #define MC_STR2(x) #x
 #define MC_STR(x) MC_STR2(x)
-#define REQUIRE(expr)                                                                       \
-  do {                                                                                      \
-    if (!(expr)) throw minicatch::Failure(__FILE__ ":" MC_STR(__LINE__) ": REQUIRE(" #expr ")"); \
+#define REQUIRE(...)                                                                                   \
+  do {                                                                                                 \
+    if (!(__VA_ARGS__)) throw minicatch::Failure(__FILE__ ":" MC_STR(__LINE__) ": REQUIRE(" #__VA_ARGS__ ")"); \
   } while (0)
-#define REQUIRE_FALSE(expr) REQUIRE(!(expr))
+#define REQUIRE_FALSE(...) REQUIRE(!(__VA_ARGS__))
 #define REQUIRE_THROWS_AS(expr, type)                                                          \
   do {                                                                                         \
     bool mc_ok = false;                                                                        \
@@ -66,4 +66,4 @@ inline int run(int argc, char** argv) {
     }                                                                                          \
     if (!mc_ok) throw minicatch::Failure(__FILE__ ":" MC_STR(__LINE__) ": no " #type " from " #expr); \
   } while (0)
-#define REQUIRE_NOTHROW(expr) (void)(expr)
+#define REQUIRE_NOTHROW(...) (void)(__VA_ARGS__)
