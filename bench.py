@@ -425,8 +425,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # just read costs ~30% of the link).
     direct = args.mode == "direct"
     if direct:
-        # The checkpoint image itself is pinned + mapped: k_copy_host stores
-        # every shipped chunk at its place (chunk_copied, cr.hpp:499-501).
+        # The checkpoint image itself is pinned + mapped: the copy engine moves
+        # every shipped chunk to its place (chunk_copied, cr.hpp:499-501).
         img_offs, o = [], 0
         for b in bufs:
             img_offs.append(o)
@@ -442,8 +442,6 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
-    # direct mode: the drain kernel (k_copy_host) must win SM slots over queued
-    # application blocks too, so its stream shares the dump's priority
     ckpt, app = pd.Stream(priority=args.ckpt_priority), pd.Stream()
     copy = pd.Stream(priority=args.drain_priority if args.drain_priority >= 0 else
                      (args.ckpt_priority if args.mode == "direct" else 0))
@@ -552,11 +550,6 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         copy.synchronize()
         ckpt.synchronize()
         if direct:
-            if args.trace:
-                import ctypes as C
-                qs = (C.c_uint64 * 14)()
-                pd.lib().pos_debug_ship_queue(eng.ctx, qs)
-                print(json.dumps({"ship_queue": list(qs)}), file=sys.stderr, flush=True)
             _, pre_payload = eng.precopy_direct_result()
             dpay = sum(by_handle[h].size for h in dag_writes)
         # host image = the checkpoint target (captured_); inside the e2e wall
@@ -649,14 +642,19 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     d2h_step = d2h_bytes / (step_ms * 1e-3) / 1e9
 
     n_chunks = eng.n_chunks
-    alg_bytes = total + 9 * n_chunks  # read B; digest prev read + cur write (8 B) + flag (1 B) per chunk
+    # per hash launch (one per wave): read B; digest prev read + cur write (8 B) + flag (1 B) per chunk
+    n_launch = max(1, min(args.waves, len(wl.sizes))) if direct else max(1, args.waves)
+    alg_bytes = (total + 9 * n_chunks) / n_launch
+    launch_ms = hash_ms / n_launch
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs", FALLBACK_HBM)
-    achieved = alg_bytes / (hash_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"hash_traffic_{wl.name}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        tj = json.load(open(tpath))
+        traffic = (round(tj["traffic_over_alg"] * alg_bytes) if "traffic_over_alg" in tj
+                   else tj.get("dram_bytes_per_launch"))
     stw_gbps = 2 * delta_bytes / (stw_ms * 1e-3) / 1e9 if stw_ms > 0 else 0.0
 
     out = None
@@ -703,9 +701,12 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                                    "delta hash) plus the synthetic application's k_fill window launches",
             "roofline": {"bound": "hbm", "kernel": "k_hash_chunks", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
-                         "launch_ms": round(hash_ms, 5),
-                         "launch_ms_counts": "sum of every wave's hash launch (CUDA events on the dump stream)",
+                         "traffic": traffic, "alg_bytes_per_launch": int(alg_bytes),
+                         "launch_ms": round(launch_ms, 5), "launches_per_step": n_launch,
+                         "launch_ms_counts": ("mean over the step's hash launches (one per wave; CUDA events on "
+                                              "the dump stream around each)"),
+                         "traffic_source": ("dram__bytes_read+write of one wave-sized launch under ncu --set full "
+                                            "(profiles/r2/ncu_hash_c5wave.json), per algorithmic byte"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                          "note": ("dominant HBM kernel of the dump; the step itself is bound by the host link "
                                   "(copy-engine runs into the pinned image): see host_link")},

@@ -221,30 +221,25 @@ int pos_precopy_pipelined(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, v
  * Pinned memory is used as is; pageable ranges are pinned and mapped here
  * (and unpinned at pos_ctx_destroy).  Re-register after pos_register_buffers. */
 int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* sizes, uint32_t n);
-/* Pre-copy straight into the registered image: per wave (<= 16 groups of
- * whole buffers) hash -> O1 -> scan on ckpt_stream; the host leg then moves
- * every eligible chunk to its place in the image on drain_stream.  Host leg
- * (POSDUMP_DIRECT_DRAIN): "ce" (default) -- the scan writes maximal runs of
- * shipped chunks into mapped pinned memory and the copy engine moves them
- * (cudaMemcpyBatchAsync); the call returns once every wave's runs are
- * submitted (it waits for each wave's scan, not for the copies).  "queue" --
- * the hash pushes chunks to a ship queue drained by SM stores while hashing
- * continues; "sm" -- SM stores after each scan; both return after
- * enqueueing.  No compaction pass, no host-side apply; the cache keeps an
- * index-only POSD pack per wave (header + entries, flag 2). */
+/* Pre-copy straight into the registered image (enqueue_buffer_copy /
+ * chunk_copied, cr.hpp:447-504): per wave (<= 16 groups of whole buffers) on
+ * ckpt_stream the hash (O2), k_buffer_crc (O1) and the tiled scan, which
+ * writes maximal runs of shipped chunks into mapped pinned memory and an
+ * index-only POSD pack (header + entries, flag 2) into the cache; the host
+ * submits each wave's runs to the copy engine on drain_stream the moment the
+ * scan lands (runs >= 4 MiB as plain copies, the rest as one
+ * cudaMemcpyBatchAsync), so every eligible chunk moves from the live buffer
+ * to image + ci*chunk_size with no gather and no host apply.  Returns once
+ * every wave's runs are submitted (it waits for the scans, not the copies). */
 int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                        void* drain_stream);
 /* Chunks and payload bytes the last pos_precopy_direct shipped, and the end
  * of its index packs in the cache (waits for the scans only). */
 int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_bytes,
                               uint64_t* index_bytes);
-/* Diagnostics of the direct pre-copy's ship queue: {tail, head, done,
- * exited, watchdog error, current sequence, 8 debug words}. */
-int pos_debug_ship_queue(pos_ctx* ctx, uint64_t* out14);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) moved into the image on
- * `stream`: copy-engine runs merged where both sides are contiguous (default),
- * or k_copy_host in the SM drain modes. */
+ * `stream` as copy-engine runs, merged where both sides are contiguous. */
 int pos_delta_drain(pos_ctx* ctx, void* stream);
 
 /* ---- CoW staging (gate_cow / stage_buffers, cr.hpp:806-888) ------------- */

@@ -141,7 +141,6 @@ SIGNATURES = {
     "pos_precopy_direct": [P, I32, U32, P, P],
     "pos_precopy_direct_result": [P, PU64, PU64, PU64],
     "pos_delta_drain": [P, P],
-    "pos_debug_ship_queue": [P, P],
     "pos_delta_copy": [P, P, PU64, PU64],
     "pos_stage_buffers": [P, P, U32, P, PU64, PU64],
     "pos_delta_copy_ex": [P, P, I32, PU64, PU64],

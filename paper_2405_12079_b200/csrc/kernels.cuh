@@ -1,15 +1,23 @@
 // kernels.cuh -- sm_100a kernels of the buffer-dump hot path.
 //
-//   k_hash_chunks<MODE>  O2 digest + dirty bitmap (kModeHash), digest + gather
-//                        into a POSD pack (kModeCopy), or digest of chunks
-//                        already gathered into a pack (kModeCached: the STW
-//                        delta is a pure bulk gather; its hashing runs after)
+//   k_hash_chunks<MODE>  O2 digest + dirty flags (kModeHash), digest + gather
+//                        into a POSD pack (kModeCopy: CoW staging), or digest
+//                        of chunks already gathered into a pack (kModeCached:
+//                        the STW delta is a pure bulk gather; its hashing
+//                        runs after the stop)
 //   k_buffer_crc         O1: whole-buffer CRC folded from chunk digests + verdict
-//   k_pack_scan          deterministic (handle, chunk)-ordered pack layout
+//   k_note_upstream      note_h2d_provenance's CRC, folded on the device
+//   k_scan_tiles         direct pre-copy: ballot/prefix-sum compaction of the
+//                        shipped chunks into copy-engine runs + a POSD index
+//                        pack, decoupled look-back over many CTAs
+//   k_pack_scan          pack modes: one-CTA compaction (+ fused O1) of the
+//                        (handle, chunk)-ordered pack layout and its copy items
 //   k_copy_bulk          TMA bulk copies (cp.async.bulk) staged through smem
-//   k_copy_simt          16-B vector / byte copy for unaligned items
+//   k_copy_simt          16-B vector / byte copies (unaligned items)
 //   k_pack_items         restore: POSD entries -> scatter copy items
+//   k_stage_in           SM loads of the staged STW delta layout
 //   k_fill               fill_bytes(seed) (rng.hpp:43-54) into device memory
+//   k_clear_written      finalize's written_since_ckpt reset
 //
 // See DESIGN.md for the data layout and the roofline of each kernel.
 #pragma once
@@ -88,30 +96,6 @@ struct HashParams {
   uint64_t item_base;        // hash mode: first global chunk of this launch
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
   const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
-  // > 0: before hashing its unit, a warp asks L2 for the unit's first
-  // pf_bytes with TMA bulk prefetches (16 KiB per lane), so a single-round
-  // launch (every warp holds one chunk) has the whole list in flight at once.
-  uint32_t pf_bytes;
-  uint32_t pad2;
-  // Ship queue (direct pre-copy): a dirty, eligible chunk of a buffer without
-  // provenance is pushed the moment its digest is known; k_drain_queue warps
-  // running beside the hash store it into the host image.
-  struct ShipQueue* q;
-  unsigned long long q_seq;
-  int dedup;
-  int pad3;
-};
-
-// Device ship queue: slots are tagged with the pre-copy's sequence number,
-// so no memset is needed between pre-copies; only {tail, head} are reset.
-struct ShipQueue {
-  unsigned long long tail;   // slots claimed by producers
-  unsigned long long head;   // slots claimed by drain warps
-  unsigned long long done;   // sequence number of the last finished producer pass
-  unsigned long long exited; // drain CTAs gone; the last one resets tail/head for the next pre-copy
-  unsigned long long* slots; // (seq << 32) | global chunk
-  unsigned long long error;  // watchdog: seq of a drain that gave up waiting (never 0 for a real seq)
-  unsigned long long dbg[8]; // diagnostics: watchdog slot/tail/done, globaltimer stamps
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -120,31 +104,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-// Every push of this launch (and of earlier launches) precedes `done`.
-__device__ __forceinline__ void publish_done(ShipQueue* q, unsigned long long seq) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    q->dbg[6] = globaltimer_ns();
-    __threadfence();
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&q->done), "l"(seq) : "memory");
-  }
-}
-
-__device__ __forceinline__ void ship_push(ShipQueue* q, unsigned long long seq, uint64_t g) {
-  const unsigned long long i = atomicAdd(&q->tail, 1ull);
-  if (i == 0) q->dbg[5] = globaltimer_ns();
-  const unsigned long long v = (seq << 32) | g;
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(q->slots + i), "l"(v) : "memory");
-}
-
 // Hash kernel geometry.
 constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
 constexpr int kStepBytes = 512;              // one warp step: 32 lanes x 16 B
-constexpr int kUnrollDefault = 8;            // warp steps per batch (4 KiB per warp)
-constexpr int kPrefetchSteps = 32;           // L2 bulk-prefetch distance (16 KiB per warp)
-// Measured (tools/read_micro.cu): the bulk L2 prefetch lifts a lone warp from
-// 9.2 to 11.6 GB/s but costs ~4% when every warp streams, so it is off.
-constexpr bool kL2Prefetch = false;
+constexpr int kUnroll = 8;                   // warp steps per batch (4 KiB per warp)
 constexpr uint32_t kRepTableBytes = 131072;  // lane-replicated Z^512: 4 x 256 x 32 lanes x 4 B
 constexpr uint32_t kSmallTablesBytes = 6 * 4096;
 // The replicated table sits at ABSOLUTE shared address 0x10000, so the PRMT
@@ -153,12 +116,6 @@ constexpr uint32_t kSmallTablesBytes = 6 * 4096;
 // window (which begins at the ~1 KiB reserved offset).
 constexpr uint32_t kRepAbs = 0x10000;
 constexpr uint32_t kHashSmem = 0x30000;
-// kTma variant: 16 x 4 KiB TMA slots -- 8 in the gap below the replicated
-// table (after the small tables, the Z^512 source and the mbarriers), 8 after
-// it -- and one mbarrier per warp.
-constexpr uint32_t kTmaBarOff = kSmallTablesBytes + 4096 + 64;  // 16 x 8 B
-constexpr uint32_t kTmaSlotLoOff = 0x7400;                       // 29 KiB
-constexpr uint32_t kHashSmemTma = 0x38000;
 
 // ---------------------------------------------------------------------------
 // Load helpers.
@@ -169,11 +126,6 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
-}
-
-// TMA bulk prefetch of [p, p+bytes) into L2 (16-B aligned, bytes % 16 == 0).
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
@@ -284,21 +236,9 @@ __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
 // with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
 // which leaves a register that starts at 0 unchanged.  COPY: every loaded
 // vector is also stored at dst (only when src is 16-B aligned).
-// TMA stage of the three-stage pipeline (kTma): a 4 KiB shared-memory slot
-// per warp filled by cp.async.bulk, beside the two register batches.
-struct TmaStage {
-  uint8_t* slot;      // kUnroll * 512 bytes, 128-B aligned
-  uint64_t* bar;      // this warp's mbarrier
-  uint32_t* phase;    // its parity (persists across chunks)
-};
-
-template <bool COPY, int kUnroll, bool kRoll, bool kTma = false>
-__device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
-                                               const uint32_t* xinv, uint32_t lsel, int lane,
-                                               uint64_t src, uint64_t len, uint32_t k_len,
-                                               uint8_t* dst, bool pf = kL2Prefetch,
-                                               uint32_t pf_steps = kPrefetchSteps,
-                                               TmaStage tma = TmaStage{nullptr, nullptr, nullptr}) {
+template <bool COPY>
+__device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint32_t* xinv, uint32_t lsel, int lane,
+                                               uint64_t src, uint64_t len, uint32_t k_len, uint8_t* dst) {
   const uint64_t a0 = src & ~15ull;
   const uint64_t lead = src - a0;
   const uint64_t end = lead + len;
@@ -319,17 +259,10 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
   }
   const uint64_t full_end = nblk - 1;  // steps [blk, full_end) are fully inside
   // Software-pipelined batches of kUnroll steps, ping-ponging between two
-  // register buffers (the next batch's loads are in flight while this batch's
-  // lookups run), plus a TMA bulk prefetch into L2 kPrefetchSteps ahead so the
-  // LDGs mostly hit L2.
-  auto prefetch = [&](uint64_t from_blk) {
-    if (pf && lane == 0 && from_blk * kStepBytes < end) {
-      uint64_t lo = from_blk * kStepBytes;
-      uint64_t hi = (from_blk + kUnroll) * kStepBytes;
-      hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
-      if (hi > lo) l2_prefetch(reinterpret_cast<const void*>(a0 + lo), (uint32_t)(hi - lo));
-    }
-  };
+  // register buffers: the next batch's loads are in flight while this
+  // batch's lookups run.  (Measured and dropped: an L2 bulk prefetch ahead of
+  // every warp, a rolling ring, a third TMA-filled shared-memory stage -- equal
+  // or slower, profiles/r1/tune_sweep1.txt.)
   auto load_batch = [&](uint4 (&buf)[kUnroll], uint64_t at) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) buf[u] = ldg_stream(base + (at + u) * 32);
@@ -344,112 +277,17 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small,
       c3 = adv512(lsel, c3 ^ buf[u].w);
     }
   };
-  if (pf && lane == 0) {  // head of the chunk
-    uint64_t hi = (uint64_t)pf_steps * kStepBytes;
-    hi = hi < (end & ~15ull) ? hi : (end & ~15ull);
-    if (hi) l2_prefetch(reinterpret_cast<const void*>(a0), (uint32_t)hi);
-  }
-  if (kRoll) {
-    // Rolling pipeline: a ring of kUnroll in-flight steps; the load for step
-    // i + kUnroll is issued the moment step i's registers are read, so the
-    // warp keeps a constant kUnroll x 512 B in flight instead of draining a
-    // whole batch before refilling it.
-    const uint64_t nsteps = full_end - blk;
-    uint4 ring[kUnroll];
-#pragma unroll
-    for (int j = 0; j < kUnroll; ++j)
-      if ((uint64_t)j < nsteps) ring[j] = ldg_stream(base + (blk + j) * 32);
-    uint64_t done = 0;
-    while (done + kUnroll <= nsteps) {
-#pragma unroll
-      for (int j = 0; j < kUnroll; ++j) {
-        const uint4 v = ring[j];
-        const uint64_t nxt = done + kUnroll + j;
-        if (nxt < nsteps) ring[j] = ldg_stream(base + (blk + nxt) * 32);
-        if (vec_copy) stg_stream(dbase + (blk + done + j) * 32, v);
-        c0 = adv512(lsel, c0 ^ v.x);
-        c1 = adv512(lsel, c1 ^ v.y);
-        c2 = adv512(lsel, c2 ^ v.z);
-        c3 = adv512(lsel, c3 ^ v.w);
-      }
-      done += kUnroll;
-    }
-#pragma unroll
-    for (int j = 0; j < kUnroll; ++j) {
-      if (done + j < nsteps) {
-        const uint4 v = ring[j];
-        if (vec_copy) stg_stream(dbase + (blk + done + j) * 32, v);
-        c0 = adv512(lsel, c0 ^ v.x);
-        c1 = adv512(lsel, c1 ^ v.y);
-        c2 = adv512(lsel, c2 ^ v.z);
-        c3 = adv512(lsel, c3 ^ v.w);
-      }
-    }
-    blk = full_end;
-  }
-  if (kTma && !COPY && blk + 3 * kUnroll <= full_end) {
-    // Three-stage pipeline: batches rotate through register buffers A, B and
-    // the warp's shared-memory slot S (filled by one TMA bulk copy), so two
-    // batches (8 KiB) are in flight while the third is hashed -- twice the
-    // register-only ping-pong, without more registers.
-    uint4 bufA[kUnroll], bufB[kUnroll];
-    const uint64_t nb = (full_end - blk) / kUnroll;
-    constexpr uint32_t kBatchBytes = kUnroll * kStepBytes;
-    auto tma_issue = [&](uint64_t batch) {
-      if (lane == 0) {
-        // the slot's earlier generic-proxy reads before this async-proxy write
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(tma.bar, kBatchBytes);
-        bulk_g2s(tma.slot, reinterpret_cast<const void*>(a0 + (blk + batch * kUnroll) * kStepBytes),
-                 kBatchBytes, tma.bar);
-      }
-    };
-    auto run_slot = [&]() {
-      mbar_wait(tma.bar, *tma.phase & 1u);
-      *tma.phase ^= 1u;
-      const uint32_t sa = smem_addr(tma.slot) + lane * 16;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        uint4 v;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "r"(sa + u * kStepBytes));
-        c0 = adv512(lsel, c0 ^ v.x);
-        c1 = adv512(lsel, c1 ^ v.y);
-        c2 = adv512(lsel, c2 ^ v.z);
-        c3 = adv512(lsel, c3 ^ v.w);
-      }
-      __syncwarp();  // every lane has read the slot before lane 0 refills it
-    };
-    load_batch(bufA, blk);
-    load_batch(bufB, blk + kUnroll);
-    tma_issue(2);
-    uint64_t i = 0;
-    for (; i + 3 <= nb; i += 3) {
-      run_batch(bufA, blk + i * kUnroll);
-      if (i + 3 < nb) load_batch(bufA, blk + (i + 3) * kUnroll);
-      run_batch(bufB, blk + (i + 1) * kUnroll);
-      if (i + 4 < nb) load_batch(bufB, blk + (i + 4) * kUnroll);
-      run_slot();
-      if (i + 5 < nb) tma_issue(i + 5);
-    }
-    if (i < nb) run_batch(bufA, blk + i * kUnroll);
-    if (i + 1 < nb) run_batch(bufB, blk + (i + 1) * kUnroll);
-    blk += nb * kUnroll;
-  }
-  if (!kRoll && blk + kUnroll <= full_end) {
+  if (blk + kUnroll <= full_end) {
     uint4 bufA[kUnroll], bufB[kUnroll];
     load_batch(bufA, blk);
     for (;;) {
       const bool moreB = blk + 2 * kUnroll <= full_end;
       if (moreB) load_batch(bufB, blk + kUnroll);
-      prefetch(blk + pf_steps);
       run_batch(bufA, blk);
       blk += kUnroll;
       if (!moreB) break;
       const bool moreA = blk + 2 * kUnroll <= full_end;
       if (moreA) load_batch(bufA, blk + kUnroll);
-      prefetch(blk + pf_steps);
       run_batch(bufB, blk);
       blk += kUnroll;
       if (!moreA) break;
@@ -561,11 +399,12 @@ __device__ unsigned long long g_hash_prof[1024][16][5];
 // kModeHash: every chunk -> digest, dirty flag, bitmap bit.
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
-template <int MODE, int kThreads = kHashThreads, int kUnroll = kUnrollDefault, bool kRoll = false,
-          bool kTma = false>
-// <= 120 registers: 16 warps x 3840 leave 4096 registers of the SM for the
-// drain CTAs (k_drain_queue / k_copy_host) to run beside the hash.
-__global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 384 ? 168 : 255)) k_hash_chunks(HashParams p) {
+// One CTA of kHashThreads per SM (the replicated table takes 192 KiB of
+// shared memory); <= 120 registers leave room for the small scan / copy
+// CTAs of the other streams on the same SM.
+template <int MODE>
+__global__ void __maxnreg__(120) k_hash_chunks(HashParams p) {
+  constexpr int kThreads = kHashThreads;
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -599,21 +438,6 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
   POS_PROF(1, true);
   const uint32_t* small = reinterpret_cast<const uint32_t*>(smem);
   const int lane = threadIdx.x & 31;
-  uint32_t tma_phase = 0;
-  TmaStage tma{nullptr, nullptr, &tma_phase};
-  if (kTma) {
-    const int wi = threadIdx.x >> 5;
-    const uint32_t sbase = smem_addr(smem);
-    const uint32_t hi_off = (kRepAbs - sbase) + 0x20000;  // just past the replicated table
-    tma.slot = smem + (wi < 8 ? kTmaSlotLoOff + wi * 4096u : hi_off + (wi - 8) * 4096u);
-    tma.bar = reinterpret_cast<uint64_t*>(smem + kTmaBarOff) + wi;
-    if (lane == 0) {
-      if (kTmaSlotLoOff + 8 * 4096u > kRepAbs - sbase || hi_off + 8 * 4096u > kHashSmemTma) __trap();
-      mbar_init(tma.bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-  }
   const uint32_t lsel = (uint32_t)lane * 4 | kRepAbs;
   // nseg == 1: item i goes to CTA i % grid, warp (i / grid) % W, so a short
   // list still spreads over every SM.  nseg > 1: the nseg segments of a chunk
@@ -682,16 +506,9 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
     // at the segment end.
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
-    if (p.pf_bytes > 1 && n) {
-      const uint64_t pa = (src + lo + 15) & ~15ull;
-      const uint64_t pe = (src + lo + (n < p.pf_bytes ? n : p.pf_bytes)) & ~15ull;
-      for (uint64_t q = pa + (uint64_t)lane * 16384; q < pe; q += 32 * 16384)
-        l2_prefetch(reinterpret_cast<const void*>(q), (uint32_t)(pe - q < 16384 ? pe - q : 16384));
-    }
     POS_PROF(2, round == 0);
-    const uint32_t r = n ? warp_crc32<COPY, kUnroll, kRoll, kTma>(small, p.xinv, lsel, lane, src + lo, n,
-                                                  p.nseg == 1 ? k_len : 0u, COPY ? dst + lo : nullptr,
-                                                  p.pf_bytes == 1, (uint32_t)p.pad3, tma)
+    const uint32_t r = n ? warp_crc32<COPY>(small, p.xinv, lsel, lane, src + lo, n, p.nseg == 1 ? k_len : 0u,
+                                            COPY ? dst + lo : nullptr)
                          : 0u;
     POS_PROF(3, round == 0);
     if (nseg == 1) {
@@ -728,9 +545,6 @@ __global__ void __maxnreg__(kThreads >= 512 ? (kTma ? 128 : 120) : (kThreads >= 
         const bool dirty = !p.prev_valid || (b.flags & kBufFresh) || p.digest_prev[g] != crc;
         p.flags[g] = dirty;
         if (dirty && p.bitmap) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
-        // ship now unless O1 may still drop the buffer (provenance: the scan
-        // pushes the O1 losers); DAG-dirty buffers are skipped by the drain
-        if (dirty && p.q && !(p.dedup && (b.flags & kBufHasUpstream))) ship_push(p.q, p.q_seq, g);
       }
     }
     POS_PROF(4, round == 0);
@@ -845,9 +659,8 @@ __global__ void k_note_upstream(DevBuf* bufs, uint32_t i, const uint32_t* digest
 // contiguous range of rounds; two block barriers join the warp totals.
 // Bitmap word k is written by the launch holding its last existing chunk
 // (earlier launches' flags are final by then), so waves need no memset.
-// 512 threads x 64 registers: half an SM, so the scan can start on an SM
-// that also hosts ship-queue drain CTAs (a full-register-file CTA could not,
-// and waited for the drain -- measured).
+// 512 threads x 64 registers: half an SM, so the scan starts beside a
+// running hash CTA of the next wave.
 constexpr int kScanThreads = 512;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr uint32_t kCandSlots = 1024;  // O1 candidate list (the rest is walked)
@@ -864,18 +677,10 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     // fused O1 (whole-buffer CRC + verdict for buffers [vb0, vb1) with upstream provenance):
     uint32_t vb0, uint32_t vb1, const uint32_t* tcs, const uint32_t* xfold, int dedup, uint32_t* crc_out,
     uint8_t* verdict_out, uint64_t fixed_base /* ~0 = at *cursor; cursor (if set) is advanced */,
-    int direct /* items target DevBuf::image; the pack keeps header + entries only */,
-    uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total,
-    ShipQueue* q /* direct + queue: push eligible chunks of provenance buffers; publish done */,
-    unsigned long long q_seq, int last_wave,
-    // direct + copy engine: maximal runs of eligible chunks (within a buffer
-    // and a 32-chunk bitmap word) as SoA {src, dst, bytes} in mapped pinned
-    // memory -- the argument arrays of cudaMemcpyBatchAsync
-    uint64_t* run_src, uint64_t* run_dst, uint64_t* run_len) {
+    uint32_t* bitmap /* dirty bitmap words to (re)build, or null */, uint64_t n_total) {
   __shared__ uint32_t tz[1024];  // Z^chunk_size
-  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_wr[kScanWarps], s_tot[4];
+  __shared__ uint64_t s_wn[kScanWarps], s_wb[kScanWarps], s_tot[3];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (q && t == 0) q->dbg[7] = globaltimer_ns();
   const uint32_t lt = (1u << lane) - 1u;
   if (vb1 > vb0) {
     // Candidates (upstream provenance) into a smem list in one parallel pass,
@@ -931,13 +736,12 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   struct Lane {
     uint2 cm;
     uint32_t mask;   // ballot of eligible lanes
-    uint32_t start;  // eligible lanes that begin a run (predecessor not eligible or another buffer)
     uint64_t len;    // this lane's chunk length (0 if not eligible)
   };
   auto look = [&](uint64_t k, bool with_bitmap) -> Lane {
     const uint64_t g = 32 * k + lane;
     const bool in = g >= chunk_lo && g < chunk_hi;
-    Lane L{make_uint2(0, 0), 0u, 0u, 0};
+    Lane L{make_uint2(0, 0), 0u, 0};
     uint8_t f = 0;
     if (in) {
       L.cm = chunk_map[g];
@@ -952,9 +756,6 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       }
     }
     L.mask = __ballot_sync(0xffffffffu, el);
-    const uint32_t prev_buf = __shfl_up_sync(0xffffffffu, L.cm.x, 1);
-    const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && prev_buf == L.cm.x);
-    L.start = L.mask & ~(L.mask & (L.mask << 1) & same);
     if (with_bitmap && bitmap) {
       const uint64_t last = (32 * k + 31 < n_total ? 32 * k + 31 : n_total - 1);
       if (last >= chunk_lo && last < chunk_hi) {  // this launch owns word k
@@ -965,7 +766,6 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     }
     return L;
   };
-  auto padded = [&](uint64_t len) { return direct ? len : (len + 15) & ~15ull; };
   auto warp_sum = [&](uint64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -973,10 +773,9 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   };
   // Pass 1: per-warp totals (entries, padded payload bytes).
   Lane keep[kScanKeep];
-  uint64_t wn = 0, wb = 0, wr = 0;
+  uint64_t wn = 0, wb = 0;
   auto count = [&](const Lane& L) {
     wn += __popc(L.mask);
-    wr += __popc(L.start);
     wb += warp_sum(L.len ? (L.len + 15) & ~15ull : 0);
   };
 #pragma unroll
@@ -991,35 +790,27 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   if (lane == 0) {
     s_wn[warp] = wn;
     s_wb[warp] = wb;
-    s_wr[warp] = wr;
   }
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the warp totals
     uint64_t n = lane < kScanWarps ? s_wn[lane] : 0, b = lane < kScanWarps ? s_wb[lane] : 0;
-    uint64_t r = lane < kScanWarps ? s_wr[lane] : 0;
-    uint64_t in_n = n, in_b = b, in_r = r;
+    uint64_t in_n = n, in_b = b;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint64_t an = __shfl_up_sync(0xffffffffu, in_n, o), ab = __shfl_up_sync(0xffffffffu, in_b, o);
-      const uint64_t ar = __shfl_up_sync(0xffffffffu, in_r, o);
       if (lane >= o) {
         in_n += an;
         in_b += ab;
-        in_r += ar;
       }
     }
     if (lane < kScanWarps) {
       s_wn[lane] = in_n - n;
       s_wb[lane] = in_b - b;
-      s_wr[lane] = in_r - r;
     }
     const uint64_t N = __shfl_sync(0xffffffffu, in_n, 31), B = __shfl_sync(0xffffffffu, in_b, 31);
-    const uint64_t R = __shfl_sync(0xffffffffu, in_r, 31);
     if (lane == 0) {
       const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
-      // Direct: entries keep the offsets a payload would have, but nothing is
-      // stored behind them (header payload_bytes = 0, kPackFlagDirect).
-      const uint64_t total = direct ? kPackHeader + kPackEntry * N : payload_off + B;
+      const uint64_t total = payload_off + B;
       const bool overflow = base + total > cache_capacity;
       result[0] = N;
       result[1] = total;
@@ -1027,33 +818,28 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       result[3] = overflow ? 0 : N;  // items for the copy kernel
       result[4] = base;
       result[6] = B;
-      result[7] = R;
+      result[7] = 0;
       if (!overflow && cursor) *cursor = base + (total + kPackAlign - 1) / kPackAlign * kPackAlign;
-      if (result_host && (!run_src || overflow)) {  // copy-engine runs: published after pass 2
+      if (result_host) {
         result_host[0] = N;
         result_host[1] = total;
         result_host[2] = overflow;
         result_host[3] = overflow ? 0 : N;
         result_host[4] = base;
         result_host[6] = B;
-        result_host[7] = R;
+        result_host[7] = 0;
         __threadfence_system();
         result_host[5] = seq;
         __threadfence_system();
-        if (q) q->dbg[3] = globaltimer_ns();  // diagnostics: after the system fences
       }
       s_tot[0] = N;
       s_tot[1] = B;
       s_tot[2] = overflow;
-      s_tot[3] = R;
     }
   }
   __syncthreads();
   const uint64_t N = s_tot[0], B = s_tot[1];
-  if (s_tot[2]) {  // overflow: nothing more to ship from here; let the drain finish
-    if (q && last_wave) publish_done(q, q_seq);
-    return;
-  }
+  if (s_tot[2]) return;  // overflow: the host reports StagingExhausted
   const uint64_t payload_off = (kPackHeader + kPackEntry * N + kPackAlign - 1) / kPackAlign * kPackAlign;
   if (t == 0) {
     uint32_t* h = reinterpret_cast<uint32_t*>(pack);
@@ -1061,33 +847,17 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
     h[1] = 1;
     *reinterpret_cast<uint64_t*>(pack + 8) = chunk_size;
     h[4] = (uint32_t)N;
-    h[5] = pack_flags | (direct ? kPackFlagDirect : 0u);
-    *reinterpret_cast<uint64_t*>(pack + 24) = direct ? kPackHeader + kPackEntry * N : payload_off;
-    *reinterpret_cast<uint64_t*>(pack + 32) = direct ? 0 : B;
+    h[5] = pack_flags;
+    *reinterpret_cast<uint64_t*>(pack + 24) = payload_off;
+    *reinterpret_cast<uint64_t*>(pack + 32) = B;
     *reinterpret_cast<uint64_t*>(pack + 40) = epoch;
-    *reinterpret_cast<uint64_t*>(pack + 48) = direct ? kPackHeader + kPackEntry * N : payload_off + B;
+    *reinterpret_cast<uint64_t*>(pack + 48) = payload_off + B;
     *reinterpret_cast<uint64_t*>(pack + 56) = 0;
   }
-  if (!direct)
-    for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
+  for (uint64_t i = kPackHeader + kPackEntry * N + t; i < payload_off; i += kScanThreads) pack[i] = 0;
   // Pass 2: entries + copy items at the warp's base.
-  uint64_t e = s_wn[warp], off = s_wb[warp], rb = s_wr[warp];
+  uint64_t e = s_wn[warp], off = s_wb[warp];
   auto emit = [&](uint64_t k, const Lane& L) {
-    if (run_src) {  // runs: a start lane covers its run's chunks up to the first gap in the word
-      const uint32_t cont = L.mask & ~L.start;
-      const uint32_t rest = lane < 31 ? cont >> (lane + 1) : 0u;
-      const int nrun = __ffs(~rest);  // chunks in the run (>= 1)
-      const int last = lane + nrun - 1 < 31 ? lane + nrun - 1 : 31;
-      const uint64_t last_len = __shfl_sync(0xffffffffu, L.len, last);
-      if (L.start >> lane & 1) {
-        const DevBuf& b = bufs[L.cm.x];
-        const uint64_t ri = rb + __popc(L.start & lt);
-        run_src[ri] = b.ptr + (uint64_t)L.cm.y * chunk_size;
-        run_dst[ri] = b.image + (uint64_t)L.cm.y * chunk_size;
-        run_len[ri] = (uint64_t)(nrun - 1) * chunk_size + last_len;
-      }
-      rb += __popc(L.start);
-    }
     const uint64_t pl = L.len ? (L.len + 15) & ~15ull : 0;
     uint64_t incl = pl;  // inclusive prefix of the round's padded lengths
 #pragma unroll
@@ -1104,16 +874,12 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
       ent[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)my_off,
                           (uint32_t)(my_off >> 32));
       ent[1] = make_uint4(L.cm.y, (uint32_t)L.len, digests[g], 0u);
-      if (q) {  // the hash shipped every other eligible chunk already
-        if (dedup && (b.flags & kBufHasUpstream)) ship_push(q, q_seq, g);
-      } else {
-        CopyItem ci;
-        ci.src = b.ptr + (uint64_t)L.cm.y * chunk_size;
-        ci.dst = direct ? b.image + (uint64_t)L.cm.y * chunk_size : (uint64_t)pack + payload_off + my_off;
-        ci.len = L.len;
-        ci.padded = padded(L.len);
-        items[my_e] = ci;
-      }
+      CopyItem ci;
+      ci.src = b.ptr + (uint64_t)L.cm.y * chunk_size;
+      ci.dst = (uint64_t)pack + payload_off + my_off;
+      ci.len = L.len;
+      ci.padded = pl;
+      items[my_e] = ci;
     }
     e += __popc(L.mask);
     off += __shfl_sync(0xffffffffu, incl, 31);
@@ -1122,23 +888,6 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(
   for (int j = 0; j < kScanKeep; ++j)
     if (r0 + j < r1) emit(r0 + j, keep[j]);
   for (uint64_t k = r0 + kScanKeep; k < r1; ++k) emit(k, look(k, false));
-  if (q && last_wave) publish_done(q, q_seq);
-  if (run_src && result_host) {  // the host reads the run lists once it sees seq
-    __syncthreads();  // every run write happens-before thread 0's fence (cumulativity)
-    if (t == 0) {
-      __threadfence_system();
-      result_host[0] = N;
-      result_host[1] = direct ? kPackHeader + kPackEntry * N : payload_off + B;
-      result_host[2] = 0;
-      result_host[3] = N;
-      result_host[4] = base;
-      result_host[6] = B;
-      result_host[7] = s_tot[3];
-      __threadfence_system();
-      result_host[5] = seq;
-      __threadfence_system();
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1480,44 +1229,6 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const CopyItem* items, const u
   }
 }
 
-// SIMT vector copy of 16-B aligned items, split into 4 KiB pieces dealt to
-// warps (a piece per warp-step: 8 x 16-B loads per lane in flight); the
-// POSDUMP_COPY=vec alternative to the TMA bulk path.  Measured beside a
-// copy-engine D2H, both slow ~3x (a 64 MiB gather: 24-26 us alone, 74-80 us
-// beside), so TMA stays the default.
-constexpr uint32_t kVecPiece = 4096;
-
-__global__ void __launch_bounds__(256) k_copy_vec(const CopyItem* items, const uint64_t* n_items_dev,
-                                                  uint64_t n_items_host, uint32_t pieces_per_item) {
-  const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
-  const int lane = threadIdx.x & 31;
-  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
-  const uint64_t units = n * pieces_per_item;
-  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); u < units; u += nw) {
-    const CopyItem c = items[u / pieces_per_item];
-    const uint64_t lo = (u % pieces_per_item) * kVecPiece;
-    if (lo >= c.padded) continue;
-    const uint64_t hi = lo + kVecPiece < c.padded ? lo + kVecPiece : c.padded;
-    const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
-    uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
-    const uint64_t body_hi = (c.len & ~15ull) < hi ? (c.len & ~15ull) : hi;  // full 16-B vectors of payload
-    uint4 v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint64_t o = lo + (uint64_t)(j * 32 + lane) * 16;
-      v[j] = o + 16 <= body_hi ? ldg_stream(s + o) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint64_t o = lo + (uint64_t)(j * 32 + lane) * 16;
-      if (o + 16 <= body_hi) *reinterpret_cast<uint4*>(d + o) = v[j];
-    }
-    // the < 16 B payload remainder and the zero padding up to `padded`
-    const uint64_t t0 = body_hi > lo ? body_hi : lo;
-    for (uint64_t o = t0 + lane; o < hi; o += 32) d[o] = o < c.len ? s[o] : 0;
-  }
-}
-
 // Fallback for items whose src or dst is not 16-B aligned: one warp per item,
 // byte copy + zero padding to `padded`.
 __global__ void k_copy_simt(const CopyItem* items, const uint64_t* n_items_dev, uint64_t n_items_host) {
@@ -1529,135 +1240,6 @@ __global__ void k_copy_simt(const CopyItem* items, const uint64_t* n_items_dev, 
     const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
     uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
     for (uint64_t k = lane; k < c.padded; k += 32) d[k] = k < c.len ? s[k] : 0;
-  }
-}
-
-// Zero-copy drain into the host image (mapped pinned memory): a handful of
-// small CTAs -- no shared memory, few registers -- so they co-reside with the
-// hash kernel's one-CTA-per-SM launch and with application blocks.  Each warp
-// streams one item at a time: kHostUnroll 16-B loads per lane in flight, then
-// the same number of 16-B stores, which leave the SM as posted PCIe writes.
-// <= 32 registers (launch bounds): 4 warps fit beside the hash kernel's
-// 16 x 120-register warps, so the drain runs while later waves hash
-// (the link, ~53 GB/s for SM stores, is the bound; 8 CTAs saturate it).
-// Items whose src/dst are not both 16-B aligned, and item tails, go by byte.
-constexpr int kHostCopyThreads = 128;
-constexpr int kHostCopyCtas = 16;
-constexpr int kHostUnroll = 4;
-
-__global__ void __launch_bounds__(kHostCopyThreads, 16) k_copy_host(const CopyItem* items,
-                                                               const uint64_t* n_items_dev,
-                                                               uint64_t n_items_host) {
-  const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
-  const int lane = threadIdx.x & 31;
-  const uint64_t nw = (uint64_t)gridDim.x * (kHostCopyThreads / 32);
-  for (uint64_t i = (uint64_t)blockIdx.x * (kHostCopyThreads / 32) + (threadIdx.x >> 5); i < n; i += nw) {
-    const CopyItem c = items[i];
-    const uint8_t* s = reinterpret_cast<const uint8_t*>(c.src);
-    uint8_t* d = reinterpret_cast<uint8_t*>(c.dst);
-    const uint64_t body = ((c.src | c.dst) & 15) == 0 ? c.len & ~15ull : 0;
-    constexpr uint32_t kStep = 32 * 16 * kHostUnroll;
-    const uint4* sp = reinterpret_cast<const uint4*>(s) + lane;
-    uint4* dp = reinterpret_cast<uint4*>(d) + lane;
-    const uint4* const se = reinterpret_cast<const uint4*>(s + body / kStep * kStep);
-    for (; sp < se; sp += 32 * kHostUnroll, dp += 32 * kHostUnroll) {
-      uint4 v[kHostUnroll];
-#pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) v[u] = ldg_stream(sp + u * 32);
-#pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) dp[u * 32] = v[u];
-    }
-    for (uint64_t q = body / kStep * kStep + lane * 16; q + 16 <= body; q += 32 * 16)
-      *reinterpret_cast<uint4*>(d + q) = ldg_stream(s + q);
-    for (uint64_t q = body + lane; q < c.padded; q += 32) d[q] = q < c.len ? s[q] : 0;
-  }
-}
-
-// Persistent drain of the ship queue into the host image: launched before
-// the hash on the drain stream, co-resident with it (same footprint as
-// k_copy_host); a warp claims a slot, waits for its producer, stores the
-// chunk at image + chunk * chunk_size, and leaves once the last producer pass
-// (the final wave's scan) has published `done` and every claimed slot is past
-// the final tail.
-constexpr int kDrainThreads = 64;  // 2 warps x 32 registers: two CTAs still fit beside a hash CTA
-constexpr int kDrainCtas = 32;
-
-__global__ void __launch_bounds__(kDrainThreads, 32) k_drain_queue(ShipQueue* q, unsigned long long seq,
-                                                                   const DevBuf* bufs, const uint2* chunk_map,
-                                                                   uint64_t chunk_size, const uint8_t* dag_dirty,
-                                                                   unsigned long long watchdog_ns) {
-  const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) q->dbg[4] = globaltimer_ns();
-  for (;;) {
-    unsigned long long i = 0;
-    if (lane == 0) i = atomicAdd(&q->head, 1ull);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    unsigned long long v = 0;
-    int state = 0;  // 1 got the slot, 2 finished
-    if (lane == 0) {
-      const unsigned long long t0 = globaltimer_ns();
-      for (uint32_t ns = 32;;) {
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(q->slots + i) : "memory");
-        if ((v >> 32) == seq) {
-          state = 1;
-          break;
-        }
-        unsigned long long d, t;
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(d) : "l"(&q->done) : "memory");
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(t) : "l"(&q->tail) : "memory");
-        if (d == seq && i >= t) {
-          state = 2;
-          break;
-        }
-        if (globaltimer_ns() - t0 > watchdog_ns) {  // a producer that never came: do not hang the GPU
-          q->dbg[0] = i;
-          q->dbg[1] = t;
-          q->dbg[2] = d;
-          q->dbg[3] = globaltimer_ns();
-          atomicExch(&q->error, seq);
-          state = 2;
-          break;
-        }
-        __nanosleep(ns);
-        ns = ns < 1024 ? ns * 2 : ns;
-      }
-    }
-    state = __shfl_sync(0xffffffffu, state, 0);
-    if (state == 2) break;
-    const uint64_t g = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)v, 0);
-    const uint2 cm = chunk_map[g];
-    if (dag_dirty && dag_dirty[cm.x]) continue;  // left to the STW delta (cr.hpp:487)
-    const DevBuf& b = bufs[cm.x];
-    const uint64_t start = (uint64_t)cm.y * chunk_size;
-    const uint64_t len = cm.y + 1 == b.nchunks ? b.size - start : chunk_size;
-    const uint8_t* s = reinterpret_cast<const uint8_t*>(b.ptr + start);
-    uint8_t* d = reinterpret_cast<uint8_t*>(b.image + start);
-    const uint64_t body = (((uint64_t)s | (uint64_t)d) & 15) == 0 ? len & ~15ull : 0;
-    constexpr uint32_t kStep = 32 * 16 * kHostUnroll;
-    const uint4* sp = reinterpret_cast<const uint4*>(s) + lane;
-    uint4* dp = reinterpret_cast<uint4*>(d) + lane;
-    const uint4* const se = reinterpret_cast<const uint4*>(s + body / kStep * kStep);
-    for (; sp < se; sp += 32 * kHostUnroll, dp += 32 * kHostUnroll) {
-      uint4 w[kHostUnroll];
-#pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) w[u] = ldg_stream(sp + u * 32);
-#pragma unroll
-      for (int u = 0; u < kHostUnroll; ++u) dp[u * 32] = w[u];
-    }
-    for (uint64_t o = body / kStep * kStep + lane * 16; o + 16 <= body; o += 32 * 16)
-      *reinterpret_cast<uint4*>(d + o) = ldg_stream(s + o);
-    for (uint64_t o = body + lane; o < len; o += 32) d[o] = s[o];
-  }
-  // the last warp out resets the counters for the next pre-copy
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&q->exited, 1ull) == (unsigned long long)gridDim.x - 1) {
-      q->tail = 0;
-      q->head = 0;
-      q->exited = 0;
-      __threadfence();
-    }
   }
 }
 

@@ -115,57 +115,9 @@ struct PinnedArray {
   }
 };
 
-// Hash kernel variants (threads per CTA x warp steps per batch); one CTA per
-// SM either way.  POSDUMP_HASH_CFG selects one for tuning runs.
-enum HashCfg { kCfg512x8 = 0, kCfg256x16, kCfg384x12, kCfg512r12, kCfg512r16, kCfg256r24, kCfg512t6 };
-
-HashCfg hash_cfg() {
-  static const HashCfg c = [] {
-    const char* e = std::getenv("POSDUMP_HASH_CFG");
-    if (!e) return kCfg512x8;
-    if (!std::strcmp(e, "256x16")) return kCfg256x16;
-    if (!std::strcmp(e, "384x12")) return kCfg384x12;
-    if (!std::strcmp(e, "512r12")) return kCfg512r12;
-    if (!std::strcmp(e, "512r16")) return kCfg512r16;
-    if (!std::strcmp(e, "256r24")) return kCfg256r24;
-    if (!std::strcmp(e, "512t6")) return kCfg512t6;
-    return kCfg512x8;
-  }();
-  return c;
-}
-
-int hash_threads() {
-  switch (hash_cfg()) {
-    case kCfg256x16: return 256;
-    case kCfg256r24: return 256;
-    case kCfg384x12: return 384;
-    default: return 512;
-  }
-}
-
-template <int COPY>
+template <int MODE>
 void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
-  switch (hash_cfg()) {
-    case kCfg256x16: k_hash_chunks<COPY, 256, 16><<<grid, 256, kHashSmem, s>>>(p); break;
-    case kCfg384x12: k_hash_chunks<COPY, 384, 12><<<grid, 384, kHashSmem, s>>>(p); break;
-    case kCfg512r12: k_hash_chunks<COPY, 512, 12, true><<<grid, 512, kHashSmem, s>>>(p); break;
-    case kCfg512r16: k_hash_chunks<COPY, 512, 16, true><<<grid, 512, kHashSmem, s>>>(p); break;
-    case kCfg256r24: k_hash_chunks<COPY, 256, 24, true><<<grid, 256, kHashSmem, s>>>(p); break;
-    case kCfg512t6: k_hash_chunks<COPY, 512, 6, false, true><<<grid, 512, kHashSmemTma, s>>>(p); break;
-    default: k_hash_chunks<COPY, 512, 8><<<grid, 512, kHashSmem, s>>>(p); break;
-  }
-}
-
-template <int COPY>
-void set_hash_smem() {
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 384, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 256, 24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem), "smem attr");
-  ck(cudaFuncSetAttribute(k_hash_chunks<COPY, 512, 6, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          kHashSmemTma), "smem attr");
+  k_hash_chunks<MODE><<<grid, kHashThreads, kHashSmem, s>>>(p);
 }
 
 // Tables shared by every launch on a device: Z^512 (replicated in smem by the
@@ -187,31 +139,28 @@ struct CrcTables {
     ck(cudaMemcpy(xinv.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice), "upload xinv");
     ck(cudaStreamSynchronize(cudaStreamLegacy), "upload sync");
     ck(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
-    set_hash_smem<kModeHash>();
-    set_hash_smem<kModeCopy>();
-    set_hash_smem<kModeCached>();
+    ck(cudaFuncSetAttribute(k_hash_chunks<kModeHash>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
+       "smem attr");
+    ck(cudaFuncSetAttribute(k_hash_chunks<kModeCopy>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
+       "smem attr");
+    ck(cudaFuncSetAttribute(k_hash_chunks<kModeCached>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
+       "smem attr");
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
     // Load every kernel now: under lazy module loading (the CUDA 12 default)
-    // a kernel's first launch loads it, and that load waits for the device --
-    // behind a persistent k_drain_queue that waits for this very kernel
-    // (measured: the first direct pre-copy of a process stalled until the
-    // drain's watchdog fired).
-    // The drain CTAs run beside the hash kernel's 193 KiB CTAs: an SM's
-    // L1/shared split can only change while it is idle, so the drains (and
-    // the scan) ask for the hash kernel's maximal-shared carveout -- otherwise
-    // every SM holding a drain CTA is closed to the hash (measured: the hash
-    // ran in two rounds, 2-4x slower, while the ship-queue drain was live).
-    for (const void* f : {(const void*)k_drain_queue, (const void*)k_copy_host, (const void*)k_pack_scan})
-      ck(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
-         "carveout");
+    // a kernel's first launch loads it, and the load waits for the device --
+    // a first launch would serialise behind the copy engine's host leg.  The
+    // scan asks for the hash kernel's maximal-shared carveout: an SM's
+    // L1/shared split only changes while it is idle, and a scan CTA on an SM
+    // with the default split would keep the next wave's hash CTA off it.
+    ck(cudaFuncSetAttribute(k_pack_scan, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+       "carveout");
+    ck(cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+       "carveout");
     cudaFuncAttributes fa;
     ck(cudaFuncGetAttributes(&fa, k_pack_scan), "load k_pack_scan");
     ck(cudaFuncGetAttributes(&fa, k_scan_tiles), "load k_scan_tiles");
-    ck(cudaFuncGetAttributes(&fa, k_drain_queue), "load k_drain_queue");
-    ck(cudaFuncGetAttributes(&fa, k_copy_host), "load k_copy_host");
     ck(cudaFuncGetAttributes(&fa, k_copy_simt), "load k_copy_simt");
-    ck(cudaFuncGetAttributes(&fa, k_copy_vec), "load k_copy_vec");
     ck(cudaFuncGetAttributes(&fa, k_pack_items), "load k_pack_items");
     ck(cudaFuncGetAttributes(&fa, k_buffer_crc), "load k_buffer_crc");
     ck(cudaFuncGetAttributes(&fa, k_note_upstream), "load k_note_upstream");
@@ -338,16 +287,9 @@ struct pos_ctx {
   // the host ranges this context pinned itself (unpinned at destroy)
   bool image_ready = false;
   std::vector<void*> image_pinned;
-  DevArray<CopyItem> d_drain_items;  // STW delta pack payload -> host image
-  uint64_t drain_n = 0;              // items of the last delta copy (pos_delta_drain)
-  bool drain_pending = false;
+  bool drain_pending = false;        // a STW delta awaits pos_delta_drain
   bool direct_pending = false;       // a pos_precopy_direct awaits pos_precopy_direct_result
-  // ship queue (hash -> k_drain_queue) of the direct pre-copy
-  DevArray<ShipQueue> d_q;
-  DevArray<unsigned long long> d_qslots;
-  unsigned long long q_seq = 0;
-  cudaEvent_t ev_drained = nullptr;  // the last k_drain_queue exited (queue reset)
-  // copy-engine drain (default direct mode): run lists written by the scan
+  // copy-engine host leg of the direct mode: run lists written by the scan
   // into mapped pinned memory = the arguments of cudaMemcpyBatchAsync
   PinnedArray<uint64_t> h_run;   // [3][n_chunks]: src, dst, bytes
   PinnedArray<uint64_t> h_drun;  // STW delta drain runs, same layout
@@ -425,28 +367,6 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // deadlocked its look-back while application kernels kept the GPU busy).
 void upload_barrier() { ck(cudaStreamSynchronize(cudaStreamLegacy), "upload sync"); }
 
-// cudaMemcpyBatchAsync flags of the host leg (POSDUMP_CE_OVERLAP=1: prefer
-// overlap with compute).
-unsigned int ce_flags() {
-  static const unsigned int f = [] {
-    const char* e = std::getenv("POSDUMP_CE_OVERLAP");
-    return (e && e[0] == '1') ? (unsigned int)cudaMemcpyFlagPreferOverlapWithCompute : 0u;
-  }();
-  return f;
-}
-
-// Host leg of the direct pre-copy: 0 copy-engine runs, 1 SM ship queue, 2 SM after each scan.
-int direct_drain_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("POSDUMP_DIRECT_DRAIN");
-    if (e && !std::strcmp(e, "queue")) return 1;
-    if (e && !std::strcmp(e, "sm")) return 2;
-    return 0;
-  }();
-  return m;
-}
-
-
 // Per-buffer DAG-dirty flags (dirty_set_) to the device.  With a side
 // stream the copy runs there (concurrently with the first hash) and `s`
 // waits for it only where a consumer is enqueued (upload_dag_flags(c, s)).
@@ -467,22 +387,13 @@ void upload_dag_flags(pos_ctx* c, cudaStream_t s, cudaStream_t side = nullptr) {
   c->dag_uploaded = true;
 }
 
+// TMA bulk copies when every item is 16-B aligned (measured: a SIMT 16-B
+// vector copy was no faster alone and ~3x slower beside a copy-engine D2H),
+// else the SIMT vector/byte copy.
 void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
-                 bool aligned, cudaStream_t s, bool prefer_vec = false) {
+                 bool aligned, cudaStream_t s) {
   int sms = c->crc.sm_count;
-  static const bool force_simt = [] {
-    const char* e = std::getenv("POSDUMP_COPY");
-    return e && !std::strcmp(e, "simt");
-  }();
-  if (force_simt) aligned = false;
-  static const bool force_vec = [] {
-    const char* e = std::getenv("POSDUMP_COPY");
-    return e && !std::strcmp(e, "vec");
-  }();
-  if (aligned && (force_vec || prefer_vec)) {
-    const uint32_t ppi = (uint32_t)std::max<uint64_t>(1, (c->cfg.chunk_size + 15 + kVecPiece - 1) / kVecPiece);
-    k_copy_vec<<<sms * 8, 256, 0, s>>>(items, n_dev, n_host, ppi);
-  } else if (aligned) {
+  if (aligned) {
     // 3 CTAs/SM fit in smem (64 KiB ring each); one elected thread per CTA.
     int grid = sms * 3;
     if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host));
@@ -491,20 +402,6 @@ void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint6
     k_copy_simt<<<sms * 4, 256, 0, s>>>(items, n_dev, n_host);
   }
   check_launch("copy");
-  ++c->launches;
-}
-
-void launch_copy_host(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
-                      cudaStream_t s) {
-  static const int ctas = [] {
-    const char* e = std::getenv("POSDUMP_HOST_CTAS");  // tuning override
-    int v = e ? std::atoi(e) : 0;
-    return v > 0 ? v : kHostCopyCtas;
-  }();
-  int grid = ctas;
-  if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (n_host + 3) / 4));
-  k_copy_host<<<grid, kHostCopyThreads, 0, s>>>(items, n_dev, n_host);
-  check_launch("k_copy_host");
   ++c->launches;
 }
 

@@ -75,7 +75,7 @@ int main() {
   CK(cudaMalloc(&dmap, cmap.size() * sizeof(uint2)));
   CK(cudaMemcpy(dbufs, bufs.data(), bufs.size() * sizeof(DevBuf), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dmap, cmap.data(), cmap.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-  CK(cudaFuncSetAttribute(k_hash_chunks<kModeHash, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem));
+  CK(cudaFuncSetAttribute(k_hash_chunks<kModeHash>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem));
   CK(cudaFuncSetAttribute(k_empty_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem));
 
   HashParams p{};
@@ -133,7 +133,7 @@ int main() {
       std::memset(prof, 0, sizeof prof);
       CK(cudaMemcpyToSymbol(g_hash_prof, prof, sizeof prof));
       cudaMemsetAsync(flush, rep, FL, s);
-      k_hash_chunks<kModeHash, 512, 8><<<148, 512, kHashSmem, s>>>(q);
+      k_hash_chunks<kModeHash><<<148, 512, kHashSmem, s>>>(q);
       CK(cudaStreamSynchronize(s));
     }
     CK(cudaMemcpyFromSymbol(prof, g_hash_prof, sizeof prof));
@@ -163,7 +163,7 @@ int main() {
       std::snprintf(name, sizeof name, "k_hash_chunks n_items=%llu", (unsigned long long)n);
       HashParams q = p;
       q.n_items = n;
-      CK(timed(name, [&] { k_hash_chunks<kModeHash, 512, 8><<<148, 512, kHashSmem, s>>>(q); }, fl));
+      CK(timed(name, [&] { k_hash_chunks<kModeHash><<<148, 512, kHashSmem, s>>>(q); }, fl));
     }
   }
   return 0;

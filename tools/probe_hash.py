@@ -2,7 +2,7 @@
 over chunk counts from 1 to 16 Ki (64 KiB chunks, 4 MiB buffers), L2 flushed
 before every launch (and once with a warm L2).  The intercept of time vs
 bytes is the kernel's fixed cost (launch + table prologue + ramp); the slope
-its streaming rate.  POSDUMP_HASH_CFG / POSDUMP_NSEG pick the variant."""
+its streaming rate."""
 import json
 import os
 import statistics
@@ -17,7 +17,7 @@ flush = pd.DeviceMemory(256 << 20)
 mem = pd.DeviceMemory((16384 + 64) * CH)
 pd.fill_batch([(mem.ptr, mem.nbytes, 7)])
 pd.device_synchronize()
-out = {"cfg": os.environ.get("POSDUMP_HASH_CFG", "default"), "nseg": os.environ.get("POSDUMP_NSEG", "auto")}
+out = {}
 for nch in [int(x) for x in os.environ.get("PROBE_CHUNKS", "1,148,592,1526,3052,6104,16384").split(",")]:
     per = 64  # chunks per buffer
     bufs, h, left, off = [], 1, nch, 0
