@@ -509,13 +509,11 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # as record_dirty's copy cancellation does (cr.hpp:909-918).
         eng.record_dirty(dag_writes)
         def final_stop():  # at_final_stop (cr.hpp:599-621): drain the app, STW gather
+            # (direct mode: the engine itself holds the stop until the
+            # pre-copy's last slice has landed -- check_precopy_done ->
+            # final_stop, cr.hpp:532-597 -- the application never resumes
+            # over chunks still being copied)
             eng.stream_wait_event(2, ckpt)
-            if direct:
-                # The direct pre-copy reads the LIVE buffers: the final stop
-                # comes once it is complete (check_precopy_done -> final_stop,
-                # cr.hpp:532-597), so the application never resumes over
-                # chunks still being copied.
-                eng.stream_wait_event(8, ckpt)
             if args.trace:  # device-clock cross-check of the window (adds two operations to it)
                 eng.event_record(3, ckpt)
                 eng.stamp(3, ckpt)
@@ -531,7 +529,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         else:  # waves: hash/O1/compaction of wave k+1 overlaps the D2H of wave k
             packs = eng.precopy_pipelined(pin.ptr, waves=args.waves, stream=ckpt, copy_stream=copy)
         eng.event_record(1, ckpt)
-        eng.event_record(8, copy)
+        if not direct:
+            eng.event_record(8, copy)
         # Stage the delta's layout now (write sets known at submission), so the
         # stop window holds only the gather; then the final stop: hold the app
         # (its window is fully submitted) and drain it.
@@ -570,7 +569,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                 return 0.0
         hash_ms = kms("hash_waves")
         if args.trace:
-            marks = {"precopy_enqueued": 1, "app_drained": 2, "stop": 3, "stw_end": 4, "precopy_d2h_end": 8, "end": 5}
+            marks = {"precopy_enqueued": 1, "app_drained": 2, "stop": 3, "stw_end": 4, "end": 5}
             tl = {k: round(eng.event_elapsed(0, v), 4) for k, v in marks.items()}
             tl.update(eng.timeline(0))
             tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]

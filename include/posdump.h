@@ -226,17 +226,31 @@ int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* size
  * ckpt_stream the hash (O2), k_buffer_crc (O1) and the tiled scan, which
  * writes maximal runs of shipped chunks into mapped pinned memory and an
  * index-only POSD pack (header + entries, flag 2) into the cache; the host
- * submits each wave's runs to the copy engine on drain_stream the moment the
- * scan lands (runs >= 4 MiB as plain copies, the rest as one
- * cudaMemcpyBatchAsync), so every eligible chunk moves from the live buffer
- * to image + ci*chunk_size with no gather and no host apply.  Returns once
- * every wave's runs are submitted (it waits for the scans, not the copies). */
+ * host leg (a feeder thread) hands each wave's runs to the copy engine on
+ * drain_stream the moment the scan lands, as windowed slices (long runs in
+ * slices, short ones batched with cudaMemcpyBatchAsync), so every eligible
+ * chunk moves from the live buffer to image + ci*chunk_size with no gather
+ * and no host apply.  Returns once the scans are enqueued; work the caller
+ * puts on drain_stream afterwards must follow pos_precopy_direct_result (or
+ * the final stop, which waits for the host leg itself). */
 int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                        void* drain_stream);
 /* Chunks and payload bytes the last pos_precopy_direct shipped, and the end
  * of its index packs in the cache (waits for the scans only). */
 int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_bytes,
                               uint64_t* index_bytes);
+/* An application memcpy during a checkpoint (CopyEngine::submit(App),
+ * engines.hpp:63-78): enqueued on `stream` (after its earlier work) at once;
+ * while a direct pre-copy's host leg is running, the leg submits no further
+ * checkpoint slice until this copy has completed -- app over ckpt at slice
+ * granularity (engines.hpp:153-159): the copy waits behind at most
+ * window x slice bytes of checkpoint traffic.  kind: 1 H2D, 2 D2H, 3 D2D. */
+int pos_app_copy(pos_ctx* ctx, uint64_t dst, uint64_t src, uint64_t bytes, int kind, void* stream);
+/* Host-leg slicing of the direct pre-copy: slices of at most slice_bytes
+ * (>= 64 KiB; default 16 MiB), at most `window` (1..8, default 3) in flight. */
+int pos_set_host_leg(pos_ctx* ctx, uint64_t slice_bytes, uint32_t window);
+/* Slices submitted and application copies yielded to, since creation. */
+int pos_host_leg_stats(pos_ctx* ctx, uint64_t* slices, uint64_t* app_yields);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) moved into the image on
  * `stream` as copy-engine runs, merged where both sides are contiguous. */

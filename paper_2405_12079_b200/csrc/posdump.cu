@@ -217,6 +217,34 @@ struct Loader {
   std::string error;
 };
 
+// Host leg of the direct pre-copy (CopyEngine, engines.hpp:28-167): a feeder
+// thread moves each wave's runs to the copy engine as slices of at most
+// `slice` bytes with at most `window` slices in flight, so an application
+// copy issued meanwhile (pos_app_copy) waits behind at most window x slice
+// bytes of checkpoint traffic and the next slices wait for it -- app over
+// ckpt at slice granularity (engines.hpp:153-159).  Measured without it: an
+// application D2H of 16 MiB issued during a 7.5 GB pre-copy took 117 ms
+// instead of 0.3 ms (tools/probe_app_copy.py).
+struct HostLeg {
+  static constexpr int kMaxWindow = 8;
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool quit = false;
+  bool pending = false;               // a job was handed over and is not finished
+  uint32_t waves = 0;
+  cudaStream_t ds = nullptr;
+  cudaEvent_t ring[kMaxWindow] = {};
+  cudaEvent_t done_ev = nullptr;      // on ds after the job's last slice
+  bool done_ev_valid = false;         // recorded by the last finished job of this epoch
+  std::deque<cudaEvent_t> app;        // application copies in flight (the feeder yields to them)
+  uint64_t slice = 16ull << 20;
+  int window = 3;
+  uint64_t slices = 0, app_yields = 0;
+  int error_code = 0;
+  std::string error;
+};
+
 // NVLink peer-GPU cache (BASELINE config 5): packs of the
 // cache-cycled pre-copy move to slots in a peer GPU's free HBM
 // (cudaMemcpyPeerAsync), which frees the local cache region at NVLink speed
@@ -235,6 +263,7 @@ struct PeerCache {
 struct pos_ctx {
   pos_config cfg{};
   Loader* loader = nullptr;
+  HostLeg* leg = nullptr;
   PeerCache* peer = nullptr;
   CrcTables crc;
   // Buffer set (ascending handle).
@@ -289,6 +318,7 @@ struct pos_ctx {
   std::vector<void*> image_pinned;
   bool drain_pending = false;        // a STW delta awaits pos_delta_drain
   bool direct_pending = false;       // a pos_precopy_direct awaits pos_precopy_direct_result
+  bool direct_epoch = false;         // this epoch ran a direct pre-copy (the final stop follows its host leg)
   // copy-engine host leg of the direct mode: run lists written by the scan
   // into mapped pinned memory = the arguments of cudaMemcpyBatchAsync
   PinnedArray<uint64_t> h_run;   // [3][n_chunks]: src, dst, bytes
@@ -444,6 +474,7 @@ int pos_abi_version(void) { return POSDUMP_ABI_VERSION; }
 // The C ABI, by area (one translation unit).
 #include "context.inc"
 #include "precopy.inc"
+#include "hostleg.inc"
 #include "delta.inc"
 #include "restore.inc"
 #include "util.inc"

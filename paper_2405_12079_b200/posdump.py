@@ -346,6 +346,19 @@ class DumpEngine:
         return {b.handle: bool(v) for b, v in zip(self.buffers, ver) if b.upstream is not None}
 
     # ---- DAG write sets (record_dirty, cr.hpp:901-931)
+    def app_copy(self, dst: int, src: int, nbytes: int, kind: int, stream=None) -> None:
+        """An application memcpy during a checkpoint (CopyEngine::submit(App)):
+        the host leg yields to it (app > ckpt at slice granularity)."""
+        check(lib().pos_app_copy(self.ctx, dst, src, nbytes, kind, _s(stream)))
+
+    def set_host_leg(self, slice_bytes: int = 16 << 20, window: int = 3) -> None:
+        check(lib().pos_set_host_leg(self.ctx, slice_bytes, window))
+
+    def host_leg_stats(self) -> tuple[int, int]:
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_host_leg_stats(self.ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def metrics(self) -> dict:
         """CrMetrics of the session (cr.hpp:69-119): final stop + finalize."""
         m = _lib.pos_metrics()

@@ -1390,3 +1390,44 @@ def test_restore_state_parity(ref, profile, seed, mode):
     assert ours == ref.ref_restore_hash(src, len(img_bytes))
     assert ours == ref.ref_plain_hash(profile.encode(), 0, seed, im["meta"]["cursor"])
     eng.close()
+
+
+def test_app_copy_overtakes_checkpoint_host_leg(orc):
+    """CopyEngine priority (engines.hpp:153-159, test_engines.cpp:62-74): an
+    application D2H issued during a direct pre-copy of 2 GB goes ahead of
+    the checkpoint slices still to come -- it completes in a small fraction
+    of the pre-copy (a plain copy on another stream waited for nearly all of
+    it: tools/probe_app_copy.py) -- and both the application's bytes and
+    the image are exact."""
+    import time
+    n, sz = 16, 125_000_000
+    stride = (sz + 255) // 256 * 256
+    mem = pd.DeviceMemory(n * stride)
+    bufs = [pd.GpuBuffer(handle=i + 1, dev_ptr=mem.ptr + i * stride, size=sz) for i in range(n)]
+    pd.fill_batch([(b.dev_ptr, b.size, 8100 + b.handle) for b in bufs])
+    app_dev = pd.DeviceMemory(16 << 20)
+    pd.fill_bytes(app_dev.ptr, 16 << 20, 8200)
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=256 << 20))
+    eng.register_buffers(bufs)
+    img = pd.PinnedHost(n * stride, image=True)
+    eng.register_image([img.array[i * stride:i * stride + sz] for i in range(n)])
+    app_host = pd.PinnedHost(16 << 20)
+    ckpt, drain, app = pd.Stream(priority=1), pd.Stream(priority=1), pd.Stream()
+    eng.event_record(0, ckpt)
+    eng.precopy_direct(waves=4, stream=ckpt, drain_stream=drain)
+    time.sleep(0.005)
+    eng.event_record(20, app)
+    eng.app_copy(app_host.ptr, app_dev.ptr, 16 << 20, 2, stream=app)
+    eng.event_record(21, app)
+    eng.precopy_direct_result()
+    eng.event_record(1, drain)
+    drain.synchronize()
+    app.synchronize()
+    app_ms, pre_ms = eng.event_elapsed(20, 21), eng.event_elapsed(0, 1)
+    assert pre_ms > 20 and app_ms < 0.25 * pre_ms, (app_ms, pre_ms)
+    assert eng.host_leg_stats()[1] >= 1  # the leg yielded to it
+    assert np.array_equal(app_host.array, mb(orc, 8200, 16 << 20))
+    for i in (0, 7, n - 1):
+        assert np.array_equal(img.array[i * stride:i * stride + sz], mb(orc, 8100 + i + 1, sz))
+    eng.close()

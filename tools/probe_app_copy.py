@@ -1,14 +1,16 @@
 """App copies during a checkpoint's host leg (engines.hpp:153-159: app >
 ckpt at chunk granularity).  While a direct pre-copy moves 7.5 GB of runs
 (60 x 125 MB buffers) to the host image, the application issues a 16 MiB
-H2D and a 16 MiB D2H on its own stream: latency of each vs alone."""
+H2D / D2H on its own stream, either as a plain cudaMemcpyAsync ("raw") or
+through pos_app_copy ("managed": the host leg yields to it): latency vs
+alone, and the pre-copy's duration."""
+import json
 import os
 import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import numpy as np
 import paper_2405_12079_b200 as pd
 from paper_2405_12079_b200.posdump import D2H, H2D
 
@@ -27,12 +29,14 @@ app_host = pd.PinnedHost(16 << 20)
 ckpt, drain, app = pd.Stream(priority=1), pd.Stream(priority=1), pd.Stream()
 
 
-def app_copy(kind):
+def app_copy(kind, managed):
     eng.event_record(20, app)
-    if kind == "h2d":
-        pd.check(pd.lib().pos_memcpy(app_dev.ptr, app_host.ptr, 16 << 20, H2D, int(app)))
+    dst, src = (app_dev.ptr, app_host.ptr) if kind == "h2d" else (app_host.ptr, app_dev.ptr)
+    k = H2D if kind == "h2d" else D2H
+    if managed:
+        eng.app_copy(dst, src, 16 << 20, k, stream=app)
     else:
-        pd.check(pd.lib().pos_memcpy(app_host.ptr, app_dev.ptr, 16 << 20, D2H, int(app)))
+        pd.check(pd.lib().pos_memcpy(dst, src, 16 << 20, k, int(app)))
     eng.event_record(21, app)
     app.synchronize()
     return eng.event_elapsed(20, 21)
@@ -40,17 +44,22 @@ def app_copy(kind):
 
 out = {}
 for kind in ("h2d", "d2h"):
-    out[f"{kind}_alone_ms"] = round(min(app_copy(kind) for _ in range(5)), 3)
-for kind in ("h2d", "d2h"):
-    eng.event_record(0, ckpt)
-    eng.precopy_direct(waves=4, stream=ckpt, drain_stream=drain)
-    time.sleep(0.02)  # the copy engine is busy with the runs now
-    lat = app_copy(kind)
-    eng.event_record(1, drain)
-    drain.synchronize()
-    eng.precopy_direct_result()
-    out[f"{kind}_during_precopy_ms"] = round(lat, 3)
-    out[f"precopy_ms_{kind}"] = round(eng.event_elapsed(0, 1), 1)
-    eng.commit_epoch()
-    eng.set_target_fresh(True)
-print(out)
+    out[f"{kind}_alone_ms"] = round(min(app_copy(kind, False) for _ in range(5)), 3)
+for slice_mb, window in ((16, 3), (8, 2), (64, 4)):
+    eng.set_host_leg(slice_mb << 20, window)
+    for managed in (False, True):
+        for kind in ("h2d", "d2h"):
+            eng.set_target_fresh(True)
+            eng.event_record(0, ckpt)
+            eng.precopy_direct(waves=4, stream=ckpt, drain_stream=drain)
+            time.sleep(0.03)  # the copy engine is busy with the runs now
+            lat = app_copy(kind, managed)
+            eng.precopy_direct_result()
+            eng.event_record(1, drain)
+            drain.synchronize()
+            tag = f"slice{slice_mb}M_w{window}_{'managed' if managed else 'raw'}_{kind}"
+            out[tag] = {"app_ms": round(lat, 3), "precopy_ms": round(eng.event_elapsed(0, 1), 1),
+                        "precopy_GBps": round(N * SZ / eng.event_elapsed(0, 1) / 1e6, 2)}
+            eng.commit_epoch()
+out["slices, app_yields"] = eng.host_leg_stats()
+print(json.dumps(out, indent=1))
