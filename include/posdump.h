@@ -249,8 +249,11 @@ int pos_app_copy(pos_ctx* ctx, uint64_t dst, uint64_t src, uint64_t bytes, int k
 /* Host-leg slicing of the direct pre-copy: slices of at most slice_bytes
  * (>= 64 KiB; default 16 MiB), at most `window` (1..8, default 3) in flight. */
 int pos_set_host_leg(pos_ctx* ctx, uint64_t slice_bytes, uint32_t window);
-/* Slices submitted and application copies yielded to, since creation. */
-int pos_host_leg_stats(pos_ctx* ctx, uint64_t* slices, uint64_t* app_yields);
+/* Since creation: slices submitted, application copies yielded to, and bytes
+ * of runs cancelled because their buffer was recorded dirty (pos_record_dirty)
+ * after the scan -- CopyEngine::cancel (cr.hpp:909-918): the final stop
+ * re-copies those buffers. */
+int pos_host_leg_stats(pos_ctx* ctx, uint64_t* slices, uint64_t* app_yields, uint64_t* cancelled_bytes);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) moved into the image on
  * `stream` as copy-engine runs, merged where both sides are contiguous. */

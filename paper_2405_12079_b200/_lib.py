@@ -170,7 +170,7 @@ SIGNATURES = {
     "pos_image_write": [C.POINTER(pos_image_desc), P, U64, PU64],
     "pos_app_copy": [P, U64, U64, U64, I32, P],
     "pos_set_host_leg": [P, U64, U32],
-    "pos_host_leg_stats": [P, PU64, PU64],
+    "pos_host_leg_stats": [P, PU64, PU64, PU64],
     "pos_finalize_image": [P, C.POINTER(pos_image_desc), P, U32, P, U64, PU64, C.POINTER(pos_metrics)],
     "pos_get_metrics": [P, C.POINTER(pos_metrics)],
     "pos_set_stop_exclusions": [P, P, U32],

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <string>
@@ -240,7 +241,7 @@ struct HostLeg {
   std::deque<cudaEvent_t> app;        // application copies in flight (the feeder yields to them)
   uint64_t slice = 16ull << 20;
   int window = 3;
-  uint64_t slices = 0, app_yields = 0;
+  uint64_t slices = 0, app_yields = 0, cancelled_bytes = 0;
   int error_code = 0;
   std::string error;
 };
@@ -301,6 +302,10 @@ struct pos_ctx {
   int delta_slots[2] = {-1, -1};  // pos_final_stop: the STW window's events (the delta timer)
   DevArray<uint64_t> d_result;  // async pre-copy: [n, total, overflow, n_items]
   std::set<uint64_t> dirty_set;
+  // record_dirty during a direct pre-copy cancels the buffer's copies still
+  // to be submitted (CopyEngine::cancel, cr.hpp:909-918; engines.hpp:80-85):
+  // set by the caller's thread, read by the host leg's feeder.
+  std::unique_ptr<std::atomic<uint8_t>[]> cancelled;
   std::set<uint64_t> stop_excluded;  // at_final_stop's exclusions (pos_set_stop_exclusions)
   pos_metrics metrics{};             // CrMetrics of the session (final stop + finalize)
   bool dag_uploaded = false;

@@ -354,10 +354,11 @@ class DumpEngine:
     def set_host_leg(self, slice_bytes: int = 16 << 20, window: int = 3) -> None:
         check(lib().pos_set_host_leg(self.ctx, slice_bytes, window))
 
-    def host_leg_stats(self) -> tuple[int, int]:
-        a, b = C.c_uint64(0), C.c_uint64(0)
-        check(lib().pos_host_leg_stats(self.ctx, C.byref(a), C.byref(b)))
-        return a.value, b.value
+    def host_leg_stats(self) -> tuple[int, int, int]:
+        """(slices, app copies yielded to, bytes cancelled by record_dirty)."""
+        a, b, c = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        check(lib().pos_host_leg_stats(self.ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     def metrics(self) -> dict:
         """CrMetrics of the session (cr.hpp:69-119): final stop + finalize."""

@@ -1431,3 +1431,39 @@ def test_app_copy_overtakes_checkpoint_host_leg(orc):
     for i in (0, 7, n - 1):
         assert np.array_equal(img.array[i * stride:i * stride + sz], mb(orc, 8100 + i + 1, sz))
     eng.close()
+
+
+def test_record_dirty_cancels_queued_host_leg_copies(orc):
+    """record_dirty during the pre-copy cancels the buffer's copies still to
+    be submitted (cr.hpp:909-918, CopyEngine::cancel): the last of 16 x 125 MB
+    buffers, flagged while the host leg is still on the first ones, is not
+    shipped by the pre-copy; the final stop re-copies it and the image is
+    exact -- including the bytes an application kernel wrote meanwhile."""
+    n, sz = 16, 125_000_000
+    stride = (sz + 255) // 256 * 256
+    mem = pd.DeviceMemory(n * stride)
+    bufs = [pd.GpuBuffer(handle=i + 1, dev_ptr=mem.ptr + i * stride, size=sz) for i in range(n)]
+    pd.fill_batch([(b.dev_ptr, b.size, 8300 + b.handle) for b in bufs])
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=512 << 20))
+    eng.register_buffers(bufs)
+    img = pd.PinnedHost(n * stride, image=True)
+    eng.register_image([img.array[i * stride:i * stride + sz] for i in range(n)])
+    ckpt, drain, app = pd.Stream(priority=1), pd.Stream(priority=1), pd.Stream()
+    eng.precopy_direct(waves=1, stream=ckpt, drain_stream=drain)
+    eng.record_dirty([n])                      # the application's kernel on buffer n is submitted
+    pd.fill_bytes(bufs[-1].dev_ptr, sz, 8400, stream=app)
+    eng.event_record(2, app)
+    eng.stream_wait_event(2, ckpt)             # drain the application
+    eng.at_final_stop(stream=ckpt)             # waits for the pre-copy's last slice by itself
+    drain.wait(ckpt)
+    eng.delta_drain(stream=drain)
+    eng.precopy_direct_result()
+    drain.synchronize()
+    ckpt.synchronize()
+    _, _, cancelled = eng.host_leg_stats()
+    assert cancelled >= sz // 2, cancelled
+    assert np.array_equal(img.array[(n - 1) * stride:(n - 1) * stride + sz], mb(orc, 8400, sz))
+    for i in (0, n - 2):
+        assert np.array_equal(img.array[i * stride:i * stride + sz], mb(orc, 8300 + i + 1, sz))
+    eng.close()
