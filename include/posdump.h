@@ -348,7 +348,15 @@ int pos_restore_want(pos_ctx* ctx, uint64_t handle);
  * `stream` wait (device) for it to land.  No restore running: no-op. */
 int pos_restore_gate(pos_ctx* ctx, uint64_t handle, void* stream);
 int pos_restore_ready(pos_ctx* ctx, uint64_t handle, int* ready);
-/* All buffers loaded (check_all_loaded, cr.hpp:1091-1096); ends the restore. */
+/* hosts[i] == NULL marks buffer i as a Recompute record (cr.hpp:731-735): it
+ * is not loaded but regenerated by delta-restore replay; after its writer is
+ * enqueued, pos_restore_replayed (buffer_ready, cr.hpp:1105-1119) records its
+ * ready event on the writer's stream, and pos_restore_gate on it waits (host:
+ * until replayed; device: until the writer ran). */
+int pos_restore_replayed(pos_ctx* ctx, uint64_t handle, void* stream);
+/* All buffers loaded (check_all_loaded, cr.hpp:1091-1096) and every
+ * Recompute buffer replayed (else POS_E_BAD_STATE, nothing torn down); ends
+ * the restore. */
 int pos_restore_image_wait(pos_ctx* ctx);
 
 /* ---- device crc32 (crc32.hpp:26-34 over device memory) ---------------- */

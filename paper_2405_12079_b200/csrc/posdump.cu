@@ -206,7 +206,9 @@ struct Loader {
   std::condition_variable cv;
   std::deque<uint32_t> queue;         // buffer indices with bytes left to issue; front = next
   std::vector<uint64_t> issued;       // bytes issued per buffer
-  std::vector<uint8_t> state;         // 0 queued, 1 ready event recorded, 2 not part of the image
+  // 0 queued, 1 loaded (ready event recorded), 2 not part of the image,
+  // 3 Recompute: waits for its replayed writer, 4 Recompute replayed (ready event recorded)
+  std::vector<uint8_t> state;
   std::vector<cudaEvent_t> ready;     // per buffer
   std::vector<const uint8_t*> src;    // host image per buffer
   cudaEvent_t ring[kLoadWindow] = {};

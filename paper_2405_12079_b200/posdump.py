@@ -558,17 +558,24 @@ class DumpEngine:
         return nl.value, nr.value
 
     # ---- on-demand restore of a flat host image (restore / gate_restore, cr.hpp:167-204, 1043-1143)
-    def restore_image_begin(self, hosts: Sequence[np.ndarray], order: Sequence[int] = (), slice_bytes: int = 0,
-                            h2d_stream=None) -> None:
-        arrs = [np.ascontiguousarray(h).view(np.uint8).reshape(-1) for h in hosts]
+    def restore_image_begin(self, hosts: Sequence[Optional[np.ndarray]], order: Sequence[int] = (),
+                            slice_bytes: int = 0, h2d_stream=None) -> None:
+        """hosts[i] None: buffer i is a Recompute record (regenerated by the
+        replay; see restore_replayed)."""
+        arrs = [None if h is None else np.ascontiguousarray(h).view(np.uint8).reshape(-1) for h in hosts]
         n = len(arrs)
-        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
-        sizes = np.array([a.size for a in arrs], dtype=np.uint64)
+        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data if a is not None else None for a in arrs])
+        sizes = np.array([a.size if a is not None else 0 for a in arrs], dtype=np.uint64)
         order_a = np.array(list(order), dtype=np.uint64)
         self._restore_keep = arrs
         check(lib().pos_restore_image_begin(self.ctx, ptrs, sizes.ctypes.data, n,
                                             order_a.ctypes.data if order_a.size else None, order_a.size,
                                             slice_bytes, _s(h2d_stream)))
+
+    def restore_replayed(self, handle: int, stream=None) -> None:
+        """buffer_ready for a Recompute buffer (cr.hpp:1105-1119): its writer
+        is enqueued on `stream`."""
+        check(lib().pos_restore_replayed(self.ctx, handle, _s(stream)))
 
     def restore_want(self, handle: int) -> None:
         check(lib().pos_restore_want(self.ctx, handle))

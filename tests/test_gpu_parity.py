@@ -1467,3 +1467,48 @@ def test_record_dirty_cancels_queued_host_leg_copies(orc):
     for i in (0, n - 2):
         assert np.array_equal(img.array[i * stride:i * stride + sz], mb(orc, 8300 + i + 1, sz))
     eng.close()
+
+
+def test_ondemand_restore_recompute_handoff(orc):
+    """The delta-restore hand-off (replay_pending / buffer_ready,
+    cr.hpp:1099-1119) on the on-demand loader: buffer 2 is a Recompute record
+    (not loaded); a reader gated on it waits -- on the host until its writer
+    is enqueued (pos_restore_replayed), on the device until the writer ran --
+    and sees the regenerated bytes; loaded buffers are exact; the restore
+    cannot end while a Recompute buffer awaits its replay."""
+    import threading
+    import time
+    cs = 65536
+    p = Proc(orc, [cs * 40, cs * 30 + 7, cs * 20], seed0=8500)
+    image = [h.copy() for h in p.host]
+    for i in range(3):
+        p.zero(i)
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    h2d, app, replay = pd.Stream(), pd.Stream(), pd.Stream()
+    eng.restore_image_begin([image[0], None, image[2]], order=[3, 1], h2d_stream=h2d)
+    scratch = pd.DeviceMemory(p.bufs[1].size)
+    gated = threading.Event()
+
+    def reader():  # a replayed kernel that reads buffer 2
+        eng.restore_gate(2, stream=app)
+        pd.check(pd.lib().pos_memcpy(scratch.ptr, p.bufs[1].dev_ptr, p.bufs[1].size, 3, int(app)))
+        gated.set()
+
+    t = threading.Thread(target=reader)
+    t.start()
+    time.sleep(0.2)
+    assert not gated.is_set()  # buffer_ready(2) is false until its writer replays
+    with pytest.raises(pd.SimError) as ei:
+        eng.restore_image_wait()
+    assert ei.value.errc == "BadState"
+    pd.fill_bytes(p.bufs[1].dev_ptr, p.bufs[1].size, 8600, stream=replay)  # the writer, replayed
+    eng.restore_replayed(2, stream=replay)
+    t.join(10)
+    assert gated.is_set()
+    app.synchronize()
+    eng.restore_image_wait()
+    assert np.array_equal(scratch.download(), mb(orc, 8600, p.bufs[1].size))
+    assert np.array_equal(p.read(0), image[0]) and np.array_equal(p.read(2), image[2])
+    eng.close()
