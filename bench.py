@@ -268,6 +268,10 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU: (world, rank, device, dist).  NCCL carries only
+    the barriers and the max of the timings.  Fewer GPUs than ranks (a
+    plumbing check on a 1-GPU box) maps ranks onto GPUs round-robin and uses
+    gloo, since NCCL refuses two ranks on one device."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -275,9 +279,14 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        ngpu = torch.cuda.device_count()
+        backend = "nccl" if ngpu >= world else "gloo"
+        if ngpu:
+            local = local % ngpu
         if backend == "nccl":
             torch.cuda.set_device(local)
+        else:
+            log(f"rank {rank}: {ngpu} GPU(s) for {world} ranks -> GPU {local}, gloo (plumbing check only)")
         dist.init_process_group(backend)
     return world, rank, local, dist
 
@@ -409,7 +418,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # produced on the device
     pd.fill_batch([(b.dev_ptr, b.size, 5000 + b.handle) for b in bufs])
     pd.device_synchronize()
-    eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0))
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0), device=local)
     eng.register_buffers(bufs)
     if wl.params:  # note_h2d_provenance (process.hpp:505-522): Upstream.crc on device
         eng.hash_chunks()
@@ -463,9 +472,11 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             threading.Thread(target=self.run, daemon=True).start()
 
         def run(self):
+            pd.check(pd.lib().pos_set_device(local))  # the CUDA device is per host thread
             while True:
                 self.go.wait()
                 self.go.clear()
+                eng.event_record(9, app)  # the application's window: 9 -> 2
                 for a in self.q:
                     self.fill(a.ctypes.data, a.shape[0], self.h)
                 eng.event_record(2, app)
@@ -575,6 +586,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]
             print(json.dumps(tl), file=sys.stderr)
         r = {"ms": ms, "stw_ms": stw, "stw_dev_ms": stw_dev, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
+             "app_ms": eng.event_elapsed(9, 2) if window else 0.0,
              "precopy_bytes": pre_payload if direct else sum(z for _, z in packs),
              "delta_bytes": dpay if direct else dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
@@ -592,6 +604,22 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         log(f"warm-up epoch {e}")
         checkpoint(e, False)
         e += 1
+    # the application's window alone (no dump running): its slowdown beside the dump
+    app_alone = []
+    for k in range(3):
+        win = wl.window(e + 100 + k)
+        if not win:
+            break
+        args_list = [np.array([[by_handle[h].dev_ptr, by_handle[h].size, s & 0xFFFFFFFFFFFFFFFF] for h, s in kk],
+                              dtype=np.uint64) for kk in win]
+        pd.check(pd.lib().pos_memset(flush.ptr, k, flush.nbytes, None))
+        pd.device_synchronize()
+        eng.event_record(9, app)
+        for a in args_list:
+            pd.lib().pos_fill_batch(a.ctypes.data, a.shape[0], int(app))
+        eng.event_record(2, app)
+        app.synchronize()
+        app_alone.append(eng.event_elapsed(9, 2))
     log("timed steps")
     barrier(dist, local)
     res = []
@@ -718,6 +746,12 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                            "achieved": round(stw_gbps, 1), "peak": peak, "unit": "GB/s",
                            "frac": round(stw_gbps / peak, 4) if peak else None,
                            "note": "read + write of the DAG-dirty buffers over the whole STW window (launch incl.)"},
+            **({"app_interference": {
+                "window_ms_alone": round(statistics.median(app_alone), 4),
+                "window_ms_during_dump": round(statistics.median(r["app_ms"] for r in res), 4),
+                "slowdown": round(statistics.median(r["app_ms"] for r in res) / statistics.median(app_alone), 3),
+                "window": "the application kernels of the pre-copy window (k_fill of the DAG-dirty buffers), "
+                          "event-timed on the application stream"}} if app_alone else {}),
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
                           for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "delta_hash_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
@@ -871,7 +905,7 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
         off += (n + 255) // 256 * 256
     pd.fill_batch([(b.dev_ptr, b.size, 5000 + b.handle) for b in bufs])
     pd.device_synchronize()
-    eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0))
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0), device=local)
     eng.register_buffers(bufs)
     peer = None
     if args.peer_cache_gb > 0:  # NVLink peer-GPU cache (config 5): the next GPU, or this one on a 1-GPU box
