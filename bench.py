@@ -420,6 +420,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     pd.device_synchronize()
     eng = pd.DumpEngine(pd.SimConfig(chunk_size=CHUNK, cache_capacity=0), device=local)
     eng.register_buffers(bufs)
+    if args.hash_sms:
+        eng.set_hash_sms(args.hash_sms)
     if wl.params:  # note_h2d_provenance (process.hpp:505-522): Upstream.crc on device
         eng.hash_chunks()
         eng.scan_dedup()
@@ -442,7 +444,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             o += (b.size + 255) // 256 * 256
         log(f"allocating the pinned host image ({o} B)")
         img_pin = pd.PinnedHost(max(o, 1), image=True)  # zero-filled huge pages, pinned + mapped
-        log("host image ready")
+        huge_gb = anon_huge_gb()
+        log(f"host image ready ({huge_gb} GB of anonymous huge pages in the process)")
         host_image = [img_pin.array[a:a + b.size] for a, b in zip(img_offs, bufs)]
         eng.register_image(host_image)
         pins = []
@@ -721,6 +724,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             "run": {
                 "d2h_bytes_per_step": int(d2h_bytes), "stw_delta_bytes": int(delta_bytes),
                 "l2": "flushed between steps (256 MiB memset)", "host_cpus": numa,
+                **({"image_huge_pages_gb": huge_gb} if direct else {}),
+                "hash_sms": args.hash_sms or "all",
                 "mode": ("direct: hash -> O1 -> scan per wave, copy-engine runs from the live buffers into the "
                          "pinned host image" if direct else "pack: POSD packs in the cache, D2H + host apply")},
             "gpu_launches": int(statistics.mean(r["launches"] for r in res)),
@@ -856,6 +861,17 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
 
 def pack_entries(writes) -> int:
     return sum((n + CHUNK - 1) // CHUNK + 1 for _, _, n, _ in writes)
+
+
+def anon_huge_gb():
+    """Transparent huge pages backing this process (the image's IOMMU/TLB reach)."""
+    try:
+        for line in open("/proc/self/smaps_rollup"):
+            if line.startswith("AnonHugePages:"):
+                return round(int(line.split()[1]) * 1024 / 1e9, 1)
+    except OSError:
+        pass
+    return None
 
 
 def cpu_model() -> str:
@@ -1112,6 +1128,8 @@ def main():
     ap.add_argument("--ref-sample-bytes", type=int, default=1 << 30,
                     help="CPU reference: bounded sample (a prefix of the buffer set) of at least this many bytes")
     ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")
+    ap.add_argument("--hash-sms", type=int, default=0,
+                    help="SMs the hash may occupy (0 = all); the application's kernels get the rest")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
     ap.add_argument("--peer-cache-gb", type=float, default=0.0,
                     help="--mode stream: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")

@@ -169,6 +169,7 @@ SIGNATURES = {
     "pos_last_kernel_ms": [P, C.c_char_p, C.POINTER(C.c_float)],
     "pos_image_write": [C.POINTER(pos_image_desc), P, U64, PU64],
     "pos_app_copy": [P, U64, U64, U64, I32, P],
+    "pos_set_hash_sms": [P, U32],
     "pos_restore_replayed": [P, U64, P],
     "pos_set_host_leg": [P, U64, U32],
     "pos_host_leg_stats": [P, PU64, PU64, PU64],

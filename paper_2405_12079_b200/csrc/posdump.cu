@@ -381,7 +381,14 @@ struct pos_ctx {
   // One CTA per SM (152 KiB of smem tables); items are dealt round-robin over
   // CTAs first, so even a short list occupies every SM.
   int hash_grid(uint64_t items) const {
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>(items, (uint64_t)crc.sm_count));
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(items, (uint64_t)hash_sm_budget()));
+  }
+  // SMs the dump's hash may occupy (pos_set_hash_sms; 0 = all): the
+  // ChecksumEngine's budget (checksum_bw, config.hpp:20-23) -- every hash CTA
+  // holds a whole SM for its wave, so the application's kernels get the rest.
+  uint32_t hash_sms = 0;
+  int hash_sm_budget() const {
+    return hash_sms && (int)hash_sms < crc.sm_count ? (int)hash_sms : crc.sm_count;
   }
 };
 

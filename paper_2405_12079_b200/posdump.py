@@ -351,6 +351,10 @@ class DumpEngine:
         the host leg yields to it (app > ckpt at slice granularity)."""
         check(lib().pos_app_copy(self.ctx, dst, src, nbytes, kind, _s(stream)))
 
+    def set_hash_sms(self, sms: int) -> None:
+        """SMs the hash may occupy (0 = all): the rest stay with the application."""
+        check(lib().pos_set_hash_sms(self.ctx, sms))
+
     def set_host_leg(self, slice_bytes: int = 16 << 20, window: int = 3) -> None:
         check(lib().pos_set_host_leg(self.ctx, slice_bytes, window))
 
