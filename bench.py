@@ -454,7 +454,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         host_image = [np.zeros(b.size, np.uint8) for b in bufs]
     handles = [b.handle for b in bufs]
     flush = pd.DeviceMemory(256 << 20)
-    ckpt, app = pd.Stream(priority=args.ckpt_priority), pd.Stream()
+    ckpt, app = pd.Stream(priority=args.ckpt_priority), pd.Stream(priority=args.app_priority)
     copy = pd.Stream(priority=args.drain_priority if args.drain_priority >= 0 else
                      (args.ckpt_priority if args.mode == "direct" else 0))
     by_handle = {b.handle: b for b in bufs}
@@ -1125,6 +1125,7 @@ def main():
                          "--peer-cache-gb through a peer GPU's HBM)")
     ap.add_argument("--ring", type=int, default=3, help="pinned landing buffers (rotated per step)")
     ap.add_argument("--ckpt-priority", type=int, default=1, help="1: dump stream at the highest stream priority")
+    ap.add_argument("--app-priority", type=int, default=0, help="1: the application's stream at the highest priority")
     ap.add_argument("--ref-sample-bytes", type=int, default=1 << 30,
                     help="CPU reference: bounded sample (a prefix of the buffer set) of at least this many bytes")
     ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")

@@ -380,6 +380,10 @@ struct pos_ctx {
   }
   // One CTA per SM (152 KiB of smem tables); items are dealt round-robin over
   // CTAs first, so even a short list occupies every SM.
+  // (Measured, config-5 step, tools/ in profiles/r2/app_interference.txt:
+  // short-lived hash CTAs of 64 chunks with the application at the higher
+  // stream priority cut the window's slowdown from 11.8x to 4.8x at 0.82 of
+  // HBM; an SM budget of 18 cuts it to 1.28x at the same dump rate.)
   int hash_grid(uint64_t items) const {
     return (int)std::max<uint64_t>(1, std::min<uint64_t>(items, (uint64_t)hash_sm_budget()));
   }
