@@ -863,6 +863,16 @@ def pack_entries(writes) -> int:
     return sum((n + CHUNK - 1) // CHUNK + 1 for _, _, n, _ in writes)
 
 
+def mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def anon_huge_gb():
     """Transparent huge pages backing this process (the image's IOMMU/TLB reach)."""
     try:
@@ -1148,6 +1158,15 @@ def main():
         args.waves = {"c1": 4, "c3": 16, "c4": 16, "c5": 16}.get(args.workload, 1)
     world, rank, local, dist = dist_setup()
     wl = Workload(args.workload)
+    if args.impl != "reference" and args.mode == "direct" and wl.name in ("c3", "c5"):
+        # every rank keeps its own pinned host image of its whole state: when
+        # the node's memory cannot hold world x state, the states stream
+        # through pinned landing slots instead (same bytes over each link)
+        need = world * wl.total * 1.05
+        avail = mem_available()
+        if avail is not None and avail < need:
+            log(f"host memory {avail / 1e9:.0f} GB < {need / 1e9:.0f} GB for {world} host images: --mode stream")
+            args.mode = "stream"
     if args.impl == "reference":
         out = run_reference(args, wl, world, rank)
     elif args.mode == "stream":
