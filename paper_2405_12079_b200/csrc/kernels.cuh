@@ -1161,8 +1161,12 @@ struct PieceIter {  // walks (item, offset) pieces of this CTA's grid-stride ite
   uint64_t item, off;
 };
 
+// ppi == 0: CTA b copies items b, b + grid, ... piece by piece.  ppi > 0
+// (every item <= ppi pieces): the grid strides over the n * ppi PIECES
+// instead, so a short list of long items (the STW delta: ~200 chunks of
+// 64 KiB at config 2) still puts every CTA's ring to work at once.
 __global__ void __launch_bounds__(32) k_copy_bulk(const CopyItem* items, const uint64_t* n_items_dev,
-                                                  uint64_t n_items_host) {
+                                                  uint64_t n_items_host, uint32_t ppi) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kCopyStages * kCopyPiece);
   const uint64_t n = n_items_dev ? *n_items_dev : n_items_host;
@@ -1172,7 +1176,17 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const CopyItem* items, const u
 
   // Piece = up to kCopyPiece bytes of the 16-B-aligned body of an item.
   auto body = [&](uint64_t i) { return items[i].len & ~15ull; };
+  uint64_t gp = blockIdx.x;  // ppi > 0: this CTA's next global piece
   auto advance = [&](PieceIter& it) {
+    if (ppi) {  // next non-empty piece of the grid-stride over pieces
+      for (gp += gridDim.x; gp < n * ppi; gp += gridDim.x) {
+        it.item = gp / ppi;
+        it.off = (gp % ppi) * kCopyPiece;
+        if (it.off < body(it.item)) return;
+      }
+      it.item = n;
+      return;
+    }
     it.off += kCopyPiece;
     while (it.item < n && it.off >= body(it.item)) {
       it.item += gridDim.x;
@@ -1180,6 +1194,16 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const CopyItem* items, const u
     }
   };
   auto first = [&]() {
+    if (ppi) {
+      PieceIter it{n, 0};
+      for (; gp < n * ppi; gp += gridDim.x) {
+        it.item = gp / ppi;
+        it.off = (gp % ppi) * kCopyPiece;
+        if (it.off < body(it.item)) return it;
+      }
+      it.item = n;
+      return it;
+    }
     PieceIter it{blockIdx.x, 0};
     while (it.item < n && body(it.item) == 0) it.item += gridDim.x;
     return it;

@@ -439,13 +439,21 @@ void upload_dag_flags(pos_ctx* c, cudaStream_t s, cudaStream_t side = nullptr) {
 // vector copy was no faster alone and ~3x slower beside a copy-engine D2H),
 // else the SIMT vector/byte copy.
 void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint64_t n_host,
-                 bool aligned, cudaStream_t s) {
+                 bool aligned, cudaStream_t s, uint64_t max_item_bytes = 0) {
   int sms = c->crc.sm_count;
   if (aligned) {
     // 3 CTAs/SM fit in smem (64 KiB ring each); one elected thread per CTA.
+    // A host-known list of items no longer than max_item_bytes is spread
+    // over the grid piece by piece (more CTAs than items).
     int grid = sms * 3;
-    if (!n_dev) grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host));
-    k_copy_bulk<<<grid, 32, kCopySmem, s>>>(items, n_dev, n_host);
+    uint32_t ppi = 0;
+    if (!n_dev && max_item_bytes) {
+      ppi = (uint32_t)std::max<uint64_t>(1, (max_item_bytes + kCopyPiece - 1) / kCopyPiece);
+      grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host * ppi));
+    } else if (!n_dev) {
+      grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, n_host));
+    }
+    k_copy_bulk<<<grid, 32, kCopySmem, s>>>(items, n_dev, n_host, ppi);
   } else {
     k_copy_simt<<<sms * 4, 256, 0, s>>>(items, n_dev, n_host);
   }
