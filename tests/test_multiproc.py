@@ -77,3 +77,19 @@ def test_reference_arm_under_torchrun(tmp_path):
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["cpu_baseline"]["kind"] == "reference"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
+
+
+def test_gpus_flag_relaunches_one_process_per_gpu(tmp_path):
+    """`bench.py --gpus 2` outside torchrun re-executes itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1) instead of silently running one."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "libgpucrsim_ref.so")
+    if not os.path.exists(ref):
+        pytest.skip("oracle/_ref not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["OMP_NUM_THREADS"] = "1"
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+           "--warmup", "3", "--ref-sample-bytes", "8000000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
