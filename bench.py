@@ -301,6 +301,29 @@ def all_max(dist, vals, device):
     return t.cpu().tolist()
 
 
+def gather_rows(dist, row, device):
+    """Every rank's row of floats, on every rank (all_gather; NCCL or gloo)."""
+    if dist is None:
+        return [list(row)]
+    import torch
+    dev = f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(row, dtype=torch.float64, device=dev)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.cpu().tolist() for o in out]
+
+
+def rank_summary(dist, device, step_ms, stw_ms, e2e_ms, link_gbps):
+    """Max over ranks of the timings (the job's step) and each rank's own row:
+    step, STW window and host-link GB/s of every GPU (each rank
+    checkpoints its own state over its own link)."""
+    rows = gather_rows(dist, [step_ms, stw_ms, e2e_ms, link_gbps], device)
+    mx = [max(r[k] for r in rows) for k in range(3)]
+    per_rank = [{"rank": i, "ms_per_step": round(r[0], 4), "stw_ms": round(r[1], 4), "e2e_ms": round(r[2], 3),
+                 "host_link_gbps": round(r[3], 2)} for i, r in enumerate(rows)]
+    return mx[0], mx[1], mx[2], per_rank
+
+
 def aggregate_value(world: int, state_bytes: int, step_ms: float) -> float:
     """Whole-job GB/s: every rank checkpoints state_bytes; time = max over ranks."""
     return world * state_bytes / (step_ms * 1e-3) / 1e9
@@ -657,7 +680,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     e2e_ms = statistics.median(r["wall_ms"] for r in e2e_res)
     d2h_bytes = statistics.mean(r["precopy_bytes"] + r["delta_bytes"] for r in res)
     delta_bytes = statistics.mean(r["delta_bytes"] for r in res)
-    step_ms, stw_ms, e2e_ms = all_max(dist, [step_ms, stw_ms, e2e_ms], local)
+    step_ms, stw_ms, e2e_ms, per_rank = rank_summary(dist, local, step_ms, stw_ms, e2e_ms,
+                                                     d2h_bytes / (step_ms * 1e-3) / 1e9)
 
     link_peak = pinned_d2h_peak(pd, eng, flush, copy, pins[0] if pins else None)
     d2h_precopy = statistics.mean(r["precopy_bytes"] / (r["d2h_ms"] * 1e-3) / 1e9 for r in res)
@@ -739,6 +763,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                           "achieved_over": "whole step: every byte that crossed PCIe / step time",
                           "precopy_leg_gbps": round(d2h_precopy, 2),
                           "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run"},
+            "per_rank": per_rank,
+            "host_link_aggregate_gbps": round(sum(r["host_link_gbps"] for r in per_rank), 2),
             "stw_gather": {"bound": "hbm", "bytes": int(delta_bytes), "alg_bytes": int(2 * delta_bytes),
                            "achieved": round(stw_gbps, 1), "peak": peak, "unit": "GB/s",
                            "frac": round(stw_gbps / peak, 4) if peak else None,
@@ -989,9 +1015,10 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
     step_ms = sum(r["ms"] for r in res) / len(res)
     stw_ms = statistics.median(r["stw_ms"] for r in res)
     wall_ms = statistics.median(r["wall_ms"] for r in res)
-    step_ms, stw_ms, wall_ms = all_max(dist, [step_ms, stw_ms, wall_ms], local)
     link_peak = pinned_d2h_peak(pd, eng, flush, copy)
     d2h = statistics.mean(r["precopy_bytes"] + r["delta_bytes"] for r in res)
+    step_ms, stw_ms, wall_ms, per_rank = rank_summary(dist, local, step_ms, stw_ms, wall_ms,
+                                                      d2h / (step_ms * 1e-3) / 1e9)
     out = None
     if rank == 0:
         out = {
@@ -1003,6 +1030,8 @@ def run_gpu_stream(args, wl: Workload, world, rank, local, dist):
             "run": {"d2h_bytes_per_step": int(d2h), "packs_per_step": res[-1]["packs"], "host_cpus": numa,
                     "mode": "cache-cycled pre-copy (pos_precopy_stream), app idle at the checkpoint"},
             "stages_ms": {"hash_waves_ms": round(statistics.mean(r["hash_ms"] for r in res), 3)},
+            "per_rank": per_rank,
+            "host_link_aggregate_gbps": round(sum(r["host_link_gbps"] for r in per_rank), 2),
             **({"peer_cache": {"device": peer, "bytes": int(args.peer_cache_gb * 1e9),
                                "capture_ms": round(statistics.mean(r["capture_ms"] for r in res), 3),
                                "note": ("capture = every pack in the peer's HBM (the application may resume); "

@@ -38,6 +38,43 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _summary_worker(rank, world, port, q):
+    """The GPU arm's rank logic with the engine stubbed out: each rank brings
+    its own step / STW / e2e timings and host-link rate, rank_summary gives
+    the job's max and every rank's row, aggregate_value the weak-scaling sum."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    step, stw, e2e, link = 2000.0 + 100 * rank, 0.4 - 0.1 * rank, 2100.0 + rank, 56.0 - rank
+    m_step, m_stw, m_e2e, per_rank = bench.rank_summary(dist, rank, step, stw, e2e, link)
+    q.put((rank, m_step, m_stw, m_e2e, per_rank, bench.aggregate_value(world, 120_000_000_000, m_step)))
+    dist.destroy_process_group()
+
+
+def test_rank_summary_over_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_summary_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {o[0]: o[1:] for o in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0] == out[1]
+    m_step, m_stw, m_e2e, per_rank, value = out[0]
+    assert (m_step, m_stw, m_e2e) == (2100.0, 0.4, 2101.0)
+    assert [r["rank"] for r in per_rank] == [0, 1]
+    assert per_rank[1]["ms_per_step"] == 2100.0 and per_rank[1]["stw_ms"] == pytest.approx(0.3)
+    assert per_rank[0]["host_link_gbps"] == 56.0 and per_rank[1]["host_link_gbps"] == 55.0
+    assert value == pytest.approx(2 * 120.0 / 2.1)
+
+
 def test_all_max_and_barrier_over_gloo():
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
