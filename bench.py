@@ -577,10 +577,11 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         if app_thread.error is not None:
             raise app_thread.error
         doff, dbytes = app_thread.stw_result
-        copy.wait(ckpt)
         if direct:
-            eng.delta_drain(stream=copy)
+            eng.delta_drain(stream=copy)  # waits for the gather (not the post-stop hash) by itself
+            copy.wait(ckpt)  # the step ends when the post-stop hash is done too
         else:
+            copy.wait(ckpt)
             eng.d2h_async(pin.ptr + doff, doff, dbytes, stream=copy)
         eng.event_record(5, copy)
         copy.synchronize()

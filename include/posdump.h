@@ -256,7 +256,9 @@ int pos_set_host_leg(pos_ctx* ctx, uint64_t slice_bytes, uint32_t window);
 int pos_host_leg_stats(pos_ctx* ctx, uint64_t* slices, uint64_t* app_yields, uint64_t* cancelled_bytes);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) moved into the image on
- * `stream` as copy-engine runs, merged where both sides are contiguous. */
+ * `stream` as copy-engine runs, merged where both sides are contiguous.
+ * `stream` waits for the STW gather itself (not for the post-stop hash that
+ * follows it on the dump stream). */
 int pos_delta_drain(pos_ctx* ctx, void* stream);
 
 /* ---- CoW staging (gate_cow / stage_buffers, cr.hpp:806-888) ------------- */

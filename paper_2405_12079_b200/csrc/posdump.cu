@@ -351,6 +351,7 @@ struct pos_ctx {
   PinnedArray<uint8_t> h_stage;  // delta header + work list upload
   PinnedArray<uint8_t> h_dag;
   cudaEvent_t stage_free = nullptr;
+  cudaEvent_t gathered = nullptr;  // the STW gather landed (the delta drain waits on it, not on the post-stop hash)
   cudaEvent_t ev_dag = nullptr;  // DAG flags uploaded on a side stream
   bool dag_side = false;
   // Pre-copy packs: one per wave, chained at a device-side cache cursor.

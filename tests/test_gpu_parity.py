@@ -741,8 +741,7 @@ def test_direct_precopy_into_image(orc, cs, waves, offsets, pageable):
     p.write(3, 100, 50, 80)  # written during the pre-copy window
     pd.device_synchronize()
     off, n = eng.at_final_stop(stream=ckpt)
-    drain.wait(ckpt)
-    eng.delta_drain(stream=drain)
+    eng.delta_drain(stream=drain)  # no host-side ordering: the drain waits for the gather itself
     drain.synchronize()
     ckpt.synchronize()
     nch, pay = eng.precopy_direct_result()
@@ -1324,6 +1323,54 @@ def test_buffer_level_o2_skip(orc, trust):
     eng.commit_epoch()
     eng.hash_chunks()  # nothing written since: with trust, nothing hashed at all
     assert not eng.flags().any() or not trust
+    eng.close()
+
+
+@pytest.mark.parametrize("waves", [1, 2])
+def test_direct_precopy_trust_written_bit(orc, waves):
+    """The direct pre-copy (hash -> O1 -> tiled scan -> copy-engine runs) with
+    the buffer-level O2 skip (cr.hpp:396-401): a clean
+    buffer is neither hashed nor shipped even though its bytes changed, a
+    written buffer ships exactly its changed chunks (short tails included)."""
+    cs = 4096
+    sizes = [cs * 40 + 100, cs * 33, cs * 5, cs * 70 + 7, cs]
+    p = Proc(orc, sizes, seed0=7300)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20, trust_written_bit=True))
+    eng.register_buffers(p.bufs)
+    pin = pd.PinnedHost(sum((n + 255) // 256 * 256 for n in sizes) + 256)
+    pin.array[:] = 0
+    image, o = [], 0
+    for n in sizes:
+        image.append(pin.array[o:o + n])
+        o += (n + 255) // 256 * 256
+    eng.register_image(image)
+    ckpt, drain = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=waves, stream=ckpt, drain_stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    eng.precopy_direct_result()
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i])
+    eng.commit_epoch()
+    before = [im.copy() for im in image]
+    p.write(0, cs * 2, cs * 3, 7400)      # buffer 0: chunks 2-4, reported
+    p.write(0, cs * 40 - 50, 100, 7401)   # ... and its last two chunks (tail)
+    p.bufs[0].written_since_ckpt = True
+    eng.update_buffer(p.bufs[0])
+    p.write(1, cs * 5, 10, 7402)          # buffer 1: changed, NOT reported
+    p.write(3, cs * 69, cs + 7, 7403)     # buffer 3: reported, last two chunks
+    p.bufs[3].written_since_ckpt = True
+    eng.update_buffer(p.bufs[3])
+    pd.device_synchronize()
+    eng.precopy_direct(waves=waves, stream=ckpt, drain_stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    nch, pay = eng.precopy_direct_result()
+    assert nch == 3 + 2 + 2
+    assert pay == 3 * cs + cs + 112 + cs + 16  # padded to 16 B in the index pack
+    assert np.array_equal(image[0], p.host[0]) and np.array_equal(image[3], p.host[3])
+    assert np.array_equal(image[1], before[1]) and not np.array_equal(image[1], p.host[1])
+    assert np.array_equal(image[2], p.host[2]) and np.array_equal(image[4], p.host[4])
     eng.close()
 
 
