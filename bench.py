@@ -12,7 +12,7 @@ stop-the-world ms"), default mode `direct`:
                 drained AND the pre-copy complete] -> event, TMA bulk gather of
                 the DAG-dirty buffers into the cache (STW delta-copy), event
                 -> hash of the gathered copy
-  copy stream : cudaMemcpyBatchAsync of each wave's runs, live buffers ->
+  copy stream : copy-engine copies of each wave's runs, live buffers ->
                 pinned host image (the checkpoint target's captured_), then the
                 delta's runs, cache -> image
   app stream  : the application's kernels of the pre-copy window (their
@@ -653,6 +653,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             res.append(checkpoint(e, False))
+            log(f"step {e}: {res[-1]['ms']:.2f} ms (stw {res[-1]['stw_ms']:.4f} ms, d2h {res[-1]['d2h_ms']:.2f} ms)")
             e += 1
     barrier(dist, local)
     log("e2e steps")

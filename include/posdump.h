@@ -228,7 +228,7 @@ int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* size
  * index-only POSD pack (header + entries, flag 2) into the cache; the host
  * host leg (a feeder thread) hands each wave's runs to the copy engine on
  * drain_stream the moment the scan lands, as windowed slices (long runs in
- * slices, short ones batched with cudaMemcpyBatchAsync), so every eligible
+ * slices, short ones one copy each), so every eligible
  * chunk moves from the live buffer to image + ci*chunk_size with no gather
  * and no host apply.  Returns once the scans are enqueued; work the caller
  * puts on drain_stream afterwards must follow pos_precopy_direct_result (or

@@ -1297,6 +1297,75 @@ __global__ void k_stage_in(const __grid_constant__ StageList L) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Host leg for SHORT runs (chunk_copied into captured_, cr.hpp:499-501): SM
+// stores straight into the mapped pinned host image.  The copy engine pays
+// ~4 us per copy (64 KiB runs: 13.8 GB/s, 448 KiB: 38, one copy at a time
+// however many streams), while 4 CTAs of plain 16-B stores hold the link at
+// 52.7 GB/s for any run length and cost a concurrent HBM kernel ~1.25x (16
+// CTAs: 3.3x) -- tools/runs_micro.cu, profiles/r2/runs_micro.txt.  A batch
+// is one slot of the host leg's window: SoA {src, dst, bytes, exclusive
+// prefix} in mapped pinned memory, read once into shared memory; CTA g
+// copies bytes [g*T/G, (g+1)*T/G) of the batch's concatenation.
+constexpr int kShipThreads = 512;
+constexpr int kShipCtas = 4;
+constexpr uint32_t kShipMaxRuns = 2048;
+constexpr uint32_t kShipSmem = 4 * kShipMaxRuns * 8;
+
+__device__ __forceinline__ void cta_copy_to_host(const uint8_t* s, uint8_t* d, uint64_t m) {
+  if ((((uintptr_t)s ^ (uintptr_t)d) & 15) == 0) {
+    const uint64_t head = umin64(m, (16 - ((uintptr_t)s & 15)) & 15);
+    if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+    s += head;
+    d += head;
+    m -= head;
+    const uint64_t n16 = m >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "l"(s4 + i));
+      d4[i] = v;
+    }
+    if (threadIdx.x < (m & 15)) d[16 * n16 + threadIdx.x] = s[16 * n16 + threadIdx.x];
+  } else {  // different alignments mod 16 (odd chunk sizes): bytes
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+__global__ void __launch_bounds__(kShipThreads) k_ship_runs(const uint64_t* runs, uint32_t n, uint64_t total) {
+  extern __shared__ __align__(16) uint64_t ship_sm[];
+  uint64_t* src = ship_sm;
+  uint64_t* dst = ship_sm + n;
+  uint64_t* len = ship_sm + 2 * n;
+  uint64_t* pre = ship_sm + 3 * n;
+  // the host rewrites a slot between launches: uncached loads, all in flight at once
+  for (uint32_t i = threadIdx.x; i < 4 * n; i += blockDim.x) {
+    uint64_t v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(runs + i));
+    ship_sm[i] = v;
+  }
+  __syncthreads();
+  const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+  uint64_t lo = per * blockIdx.x;
+  const uint64_t hi = umin64(total, lo + per);
+  if (lo >= hi) return;
+  uint32_t a = 0, b = n;  // last run with pre <= lo
+  while (b - a > 1) {
+    const uint32_t mid = (a + b) / 2;
+    if (pre[mid] <= lo) a = mid; else b = mid;
+  }
+  for (uint32_t r = a; lo < hi && r < n; ++r) {
+    const uint64_t from = lo - pre[r], to = umin64(len[r], hi - pre[r]);
+    if (to > from)
+      cta_copy_to_host(reinterpret_cast<const uint8_t*>(src[r]) + from, reinterpret_cast<uint8_t*>(dst[r]) + from,
+                       to - from);
+    lo = pre[r] + len[r];
+  }
+}
+
 // A globaltimer stamp in stream order, written by a one-thread kernel: a
 // clock that does not ride the channel's event machinery (timing events on a
 // stream queued next to a long copy-engine batch were seen landing ~40 us

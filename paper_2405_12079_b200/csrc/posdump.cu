@@ -148,6 +148,7 @@ struct CrcTables {
        "smem attr");
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
+    ck(cudaFuncSetAttribute(k_ship_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, kShipSmem), "smem attr");
     // Load every kernel now: under lazy module loading (the CUDA 12 default)
     // a kernel's first launch loads it, and the load waits for the device --
     // a first launch would serialise behind the copy engine's host leg.  The
@@ -244,6 +245,8 @@ struct HostLeg {
   uint64_t slice = 16ull << 20;
   int window = 3;
   uint64_t slices = 0, app_yields = 0, cancelled_bytes = 0;
+  PinnedArray<uint64_t> ship;                 // [kMaxWindow][4][kShipMaxRuns]: a slot's short-run batch
+  std::atomic<uint64_t> ship_launches{0};     // k_ship_runs launched by the feeder
   int error_code = 0;
   std::string error;
 };
@@ -327,9 +330,11 @@ struct pos_ctx {
   bool direct_pending = false;       // a pos_precopy_direct awaits pos_precopy_direct_result
   bool direct_epoch = false;         // this epoch ran a direct pre-copy (the final stop follows its host leg)
   // copy-engine host leg of the direct mode: run lists written by the scan
-  // into mapped pinned memory = the arguments of cudaMemcpyBatchAsync
+  // into mapped pinned memory = the host leg's copy list
   PinnedArray<uint64_t> h_run;   // [3][n_chunks]: src, dst, bytes
   PinnedArray<uint64_t> h_drun;  // STW delta drain runs, same layout
+  PinnedArray<uint64_t> h_dship; // the drain's short-run batches (k_ship_runs)
+  cudaEvent_t dship_done = nullptr;
   DevArray<TileStatus> d_tiles;  // tiled scan: decoupled look-back status
   DevArray<TileCtl> d_tile_ctl;  // [kMaxWaves]: ticket + finished counters
   uint64_t drun_n = 0, drun_cap = 0;
@@ -460,6 +465,17 @@ void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint6
   }
   check_launch("copy");
   ++c->launches;
+}
+
+// Runs of at least kCeRun bytes go to the copy engine (>= 4 MiB: 54 GB/s,
+// no cost to concurrent kernels); shorter ones are shipped by k_ship_runs.
+constexpr uint64_t kCeRun = 4ull << 20;
+
+// One batch of short runs, SoA [4][n] {src, dst, bytes, exclusive prefix} in
+// mapped pinned memory, stored into the host image by kShipCtas CTAs.
+void launch_ship(const uint64_t* runs, uint32_t n, uint64_t total, cudaStream_t s) {
+  k_ship_runs<<<kShipCtas, kShipThreads, 32 * n, s>>>(runs, n, total);
+  check_launch("k_ship_runs");
 }
 
 // Global per-device CRC engine for pos_crc32 (no context).

@@ -1,5 +1,5 @@
 """STW gather (TMA bulk copy into the cache) alone vs beside a copy-engine
-direct drain (cudaMemcpyBatchAsync of ~16K 64 KiB runs) and beside a plain
+direct drain (copy-engine runs, ~16K of 64 KiB) and beside a plain
 CE D2H of 1 GiB."""
 import os
 import sys
