@@ -247,6 +247,7 @@ struct HostLeg {
   uint64_t slices = 0, app_yields = 0, cancelled_bytes = 0;
   PinnedArray<uint64_t> ship;                 // [kMaxWindow][4][kShipMaxRuns]: a slot's short-run batch
   std::atomic<uint64_t> ship_launches{0};     // k_ship_runs launched by the feeder
+  std::atomic<bool> shipped_last{false};      // the last job launched k_ship_runs
   int error_code = 0;
   std::string error;
 };
@@ -321,6 +322,7 @@ struct pos_ctx {
            delta_payload_off = 0;
   bool delta_aligned = true;
   bool delta_drain = false;  // drain items staged with the delta
+  bool drain_short = false;  // ... some of them shorter than kCeRun (k_ship_runs)
   DevArray<CopyItem> d_delta_items;
   // host image (pos_register_image): device-visible address per buffer, and
   // the host ranges this context pinned itself (unpinned at destroy)

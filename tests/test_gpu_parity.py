@@ -1559,3 +1559,54 @@ def test_ondemand_restore_recompute_handoff(orc):
     assert np.array_equal(scratch.download(), mb(orc, 8600, p.bufs[1].size))
     assert np.array_equal(p.read(0), image[0]) and np.array_equal(p.read(2), image[2])
     eng.close()
+
+
+@pytest.mark.parametrize("offsets", [None, [0, 3, 0, 5, 0]])
+def test_direct_host_leg_short_and_long_runs(orc, offsets):
+    """The host leg's two engines in one pre-copy: runs of >= 4 MiB as
+    copy-engine slices, shorter runs as k_ship_runs batches (more than
+    kShipMaxRuns = 2048 runs per wave, so several batches; runs split between
+    CTAs mid-run; unaligned buffers take the byte path).  Every shipped chunk
+    lands in the image (chunk_copied, cr.hpp:499-501), clean chunks are never
+    written."""
+    cs = 4096
+    sizes = [6 << 20, 24 << 20, 4 << 20, 9 << 20, 4097]
+    p = Proc(orc, sizes, seed0=6100, offsets=offsets)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=64 << 20))
+    eng.register_buffers(p.bufs)
+    pin = pd.PinnedHost(sum((n + 255) // 256 * 256 for n in sizes))
+    pin.array[:] = 0
+    image, o = [], 0
+    for n in sizes:
+        image.append(pin.array[o:o + n])
+        o += (n + 255) // 256 * 256
+    eng.register_image(image)
+    ckpt, drain = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=1, stream=ckpt, drain_stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    eng.precopy_direct_result()
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i]), f"epoch 0 buffer {i}"
+    eng.commit_epoch()
+    # epoch 1: buffer 0 wholly rewritten (one long run), buffer 1 every
+    # other chunk (3072 one-chunk runs), buffer 3 random chunks, the tail
+    # buffer's last byte
+    p.write(0, 0, sizes[0], 91)
+    for c in range(0, sizes[1] // cs, 2):
+        p.write(1, c * cs + 17, 40, 1000 + c)
+    rng = np.random.default_rng(5)
+    for c in rng.choice(sizes[3] // cs, 300, replace=False):
+        p.write(3, int(c) * cs, 8, 5000 + int(c))
+    p.write(4, 4096, 1, 92)
+    pd.device_synchronize()
+    marker = [im.copy() for im in image]
+    eng.precopy_direct(waves=1, stream=ckpt, drain_stream=drain)
+    drain.synchronize()
+    ckpt.synchronize()
+    nch, pay = eng.precopy_direct_result()
+    assert nch == sizes[0] // cs + sizes[1] // cs // 2 + 300 + 1
+    for i in range(len(sizes)):
+        assert np.array_equal(image[i], p.host[i]), f"epoch 1 buffer {i}"
+    assert np.array_equal(image[2], marker[2])
+    eng.close()
