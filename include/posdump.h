@@ -226,11 +226,11 @@ int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* size
  * ckpt_stream the hash (O2), k_buffer_crc (O1) and the tiled scan, which
  * writes maximal runs of shipped chunks into mapped pinned memory and an
  * index-only POSD pack (header + entries, flag 2) into the cache; the host
- * host leg (a feeder thread) hands each wave's runs to the copy engine on
- * drain_stream the moment the scan lands, as windowed slices (long runs in
- * slices, short ones one copy each), so every eligible
- * chunk moves from the live buffer to image + ci*chunk_size with no gather
- * and no host apply.  Returns once the scans are enqueued; work the caller
+ * host leg (a feeder thread) moves each wave's runs on drain_stream the
+ * moment the scan lands, as windowed slices: runs of >= 4 MiB as copy-engine
+ * copies, shorter ones as k_ship_runs batches (SM stores into the mapped
+ * image), so every eligible chunk moves from the live buffer to
+ * image + ci*chunk_size with no gather and no host apply.  Returns once the scans are enqueued; work the caller
  * puts on drain_stream afterwards must follow pos_precopy_direct_result (or
  * the final stop, which waits for the host leg itself). */
 int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
@@ -256,7 +256,8 @@ int pos_set_host_leg(pos_ctx* ctx, uint64_t slice_bytes, uint32_t window);
 int pos_host_leg_stats(pos_ctx* ctx, uint64_t* slices, uint64_t* app_yields, uint64_t* cancelled_bytes);
 /* After pos_delta_copy with an image registered: the delta pack's payload
  * (already in the cache -- the stop is over) moved into the image on
- * `stream` as copy-engine runs, merged where both sides are contiguous.
+ * `stream` as runs merged where both sides are contiguous (>= 4 MiB by the
+ * copy engine, shorter ones by k_ship_runs).
  * `stream` waits for the STW gather itself (not for the post-stop hash that
  * follows it on the dump stream). */
 int pos_delta_drain(pos_ctx* ctx, void* stream);

@@ -136,8 +136,8 @@ uint64_t ref_read_image_check(const uint8_t* p, uint64_t n) {
 // map of CrEngine (cr.hpp:1300).  ref_state_dump runs, per chunk, the
 // reference's digest crc32 (crc32.hpp:26-34) and, for dirty chunks, the
 // chunk_copied() capture: read_content + std::copy into captured_[h]
-// (cr.hpp:488-501).  Buffers are split across `threads` std::threads
-// (parallel-for over buffers; the reference itself is single-threaded).
+// (cr.hpp:488-501).  Chunks are split across `threads` std::threads
+// (parallel-for over chunks; the reference itself is single-threaded).
 struct RefState {
   DeviceMemory dev;
   std::vector<BufferHandle> handles;
@@ -174,21 +174,27 @@ uint64_t ref_state_dump(void* p, const uint32_t* prev, int prev_valid, uint32_t*
   std::vector<std::vector<uint8_t>*> dst;
   for (BufferHandle h : s->handles) dst.push_back(&s->captured[h]);
   std::vector<uint64_t> dirty(threads ? threads : 1, 0);
+  // Thread t takes the contiguous global chunk range [N*t/nt, N*(t+1)/nt):
+  // every chunk is independent (its own crc32, its own bytes of captured_),
+  // so a state of a few huge buffers still keeps every core busy.
+  const uint64_t N = first.back();
   auto work = [&](uint32_t t, uint32_t nt) {
-    for (size_t i = t; i < s->handles.size(); i += nt) {
+    const uint64_t lo = N * t / nt, hi = N * (t + 1) / nt;
+    size_t i = std::upper_bound(first.begin(), first.end(), lo) - first.begin() - 1;
+    for (uint64_t g = lo; g < hi; ++g) {
+      while (g >= first[i + 1]) ++i;
       const GpuBuffer& b = s->dev.at(s->handles[i]);
-      for (uint32_t ci = 0; ci < b.chunk_count(); ++ci) {
-        uint64_t g = first[i] + ci, off = static_cast<uint64_t>(ci) * b.chunk_size;
-        uint64_t len = b.chunk_bytes(ci);
-        uint32_t d = crc32(b.content().data() + off, len);
-        cur[g] = d;
-        bool is_dirty = !prev_valid || prev[g] != d;
-        flags[g] = is_dirty;
-        if (!is_dirty) continue;
-        ++dirty[t];
-        std::vector<uint8_t> bytes = b.read_content(off, len);
-        std::copy(bytes.begin(), bytes.end(), dst[i]->begin() + static_cast<ptrdiff_t>(off));
-      }
+      const uint32_t ci = static_cast<uint32_t>(g - first[i]);
+      const uint64_t off = static_cast<uint64_t>(ci) * b.chunk_size;
+      const uint64_t len = b.chunk_bytes(ci);
+      uint32_t d = crc32(b.content().data() + off, len);
+      cur[g] = d;
+      bool is_dirty = !prev_valid || prev[g] != d;
+      flags[g] = is_dirty;
+      if (!is_dirty) continue;
+      ++dirty[t];
+      std::vector<uint8_t> bytes = b.read_content(off, len);
+      std::copy(bytes.begin(), bytes.end(), dst[i]->begin() + static_cast<ptrdiff_t>(off));
     }
   };
   uint32_t nt = threads ? threads : 1;

@@ -106,12 +106,13 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const uint64_t L = 65536;
   uint8_t *src, *dst, *flush;
-  cudaMalloc(&src, 2048 * L);
-  cudaMalloc(&dst, 2048 * L);
+  const uint32_t NMAX = 17200;  // config 5's STW delta: 1.125 GB = 17166 x 64 KiB
+  cudaMalloc(&src, NMAX * L);
+  cudaMalloc(&dst, NMAX * L);
   cudaMalloc(&flush, 256 << 20);
-  cudaMemset(src, 5, 2048 * L);
+  cudaMemset(src, 5, NMAX * L);
   Item* d_items;
-  cudaMalloc(&d_items, 2048 * sizeof(Item));
+  cudaMalloc(&d_items, NMAX * sizeof(Item));
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -119,10 +120,13 @@ int main() {
   cudaFuncSetAttribute(k_bulk<4096, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096 + 256);
   cudaFuncSetAttribute(k_bulk<8192, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192 + 128);
   cudaFuncSetAttribute(k_bulk<4096, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 128);
-  for (uint32_t n : {50u, 200u, 800u, 2048u}) {
+  cudaFuncSetAttribute(k_bulk<32768, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768 + 64);
+  cudaFuncSetAttribute(k_bulk<16384, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 16384 + 64);
+  cudaFuncSetAttribute(k_bulk<16384, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16384 + 64);
+  for (uint32_t n : {50u, 200u, 800u, 2048u, 17166u}) {
     std::vector<Item> h(n);
     for (uint32_t i = 0; i < n; ++i)  // scattered sources (every other chunk of 2n), dense destination
-      h[i] = Item{(uint64_t)(src + (uint64_t)((i * 7919u) % 2048u) * L), (uint64_t)(dst + (uint64_t)i * L), L};
+      h[i] = Item{(uint64_t)(src + (uint64_t)((i * 7919ull) % n) * L), (uint64_t)(dst + (uint64_t)i * L), L};
     cudaMemcpy(d_items, h.data(), n * sizeof(Item), cudaMemcpyHostToDevice);
     auto timeit = [&](const char* name, auto fn) {
       std::vector<float> t;
@@ -145,10 +149,13 @@ int main() {
     timeit("bulk 8K x8, 3/SM", [&] { k_bulk<8192, 8><<<nsm * 3, 32, 8 * 8192 + 128>>>(d_items, n, L / 8192); });
     timeit("bulk 4K x16, 3/SM", [&] { k_bulk<4096, 16><<<nsm * 3, 32, 16 * 4096 + 256>>>(d_items, n, L / 4096); });
     timeit("bulk 4K x8, 6/SM", [&] { k_bulk<4096, 8><<<nsm * 6, 32, 8 * 4096 + 128>>>(d_items, n, L / 4096); });
+    timeit("bulk 32K x3, 2/SM", [&] { k_bulk<32768, 3><<<nsm * 2, 32, 3 * 32768 + 64>>>(d_items, n, L / 32768); });
+    timeit("bulk 16K x6, 2/SM", [&] { k_bulk<16384, 6><<<nsm * 2, 32, 6 * 16384 + 64>>>(d_items, n, L / 16384); });
+    timeit("bulk 16K x3, 4/SM", [&] { k_bulk<16384, 3><<<nsm * 4, 32, 3 * 16384 + 64>>>(d_items, n, L / 16384); });
     timeit("simt U=4, 4x148", [&] { k_simt<4><<<nsm * 4, 512>>>(d_items, n, L); });
     timeit("simt U=8, 4x148", [&] { k_simt<8><<<nsm * 4, 512>>>(d_items, n, L); });
     timeit("simt U=2, 4x148", [&] { k_simt<2><<<nsm * 4, 512>>>(d_items, n, L); });
-    timeit("cudaMemcpyAsync D2D x n", [&] {
+    if (n <= 2048) timeit("cudaMemcpyAsync D2D x n", [&] {
       for (uint32_t i = 0; i < n; ++i) cudaMemcpyAsync((void*)h[i].dst, (const void*)h[i].src, L, cudaMemcpyDeviceToDevice);
     });
   }

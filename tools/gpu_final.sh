@@ -2,8 +2,8 @@
 # (BASELINE config 5) and its reference arm, the other workloads' lines, and
 # the ncu launch list of the default bench command.
 P=gpurun_out/final; mkdir -p $P
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 | tee $P/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1 | tee $P/smoke.log
 timeout 900 python bench.py > $P/bench_c5.jsonl 2> $P/bench_c5.err; cut -c1-300 $P/bench_c5.jsonl
 timeout 900 python bench.py --impl reference > $P/bench_ref.jsonl 2> $P/bench_ref.err; cut -c1-300 $P/bench_ref.jsonl
 timeout 600 python bench.py --workload c2 --steps 20 > $P/bench_c2.jsonl 2>/dev/null; cut -c1-300 $P/bench_c2.jsonl
