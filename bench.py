@@ -425,6 +425,7 @@ def bind_numa_local(device: int) -> str:
 
 
 def run_gpu(args, wl: Workload, world, rank, local, dist):
+    import ctypes as C
     import paper_2405_12079_b200 as pd
     from paper_2405_12079_b200.posdump import D2H
     numa = bind_numa_local(local)
@@ -445,6 +446,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     eng.register_buffers(bufs)
     if args.hash_sms:
         eng.set_hash_sms(args.hash_sms)
+    if args.slice_mib or args.window:
+        eng.set_host_leg(slice_bytes=(args.slice_mib or 16) << 20, window=args.window or 3)
     if wl.params:  # note_h2d_provenance (process.hpp:505-522): Upstream.crc on device
         eng.hash_chunks()
         eng.scan_dedup()
@@ -482,6 +485,33 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                      (args.ckpt_priority if args.mode == "direct" else 0))
     by_handle = {b.handle: b for b in bufs}
 
+    class app_window:
+        """The application's window as a callable: one pos_fill_batch launch
+        per kernel, or (graph=True) all of them captured once into a CUDA
+        graph launched as one stream operation."""
+
+        def __init__(self, args_list, graph):
+            self.args, self.exec = args_list, None
+            if graph and args_list:
+                pd.check(pd.lib().pos_stream_begin_capture(int(app)))
+                for a in args_list:
+                    pd.check(pd.lib().pos_fill_batch(a.ctypes.data, a.shape[0], int(app)))
+                ge = C.c_void_p()
+                pd.check(pd.lib().pos_stream_end_capture(int(app), C.byref(ge)))
+                self.exec = ge.value
+
+        def __call__(self):
+            if self.exec:
+                pd.check(pd.lib().pos_graph_launch(self.exec, int(app)))
+            else:
+                for a in self.args:
+                    pd.lib().pos_fill_batch(a.ctypes.data, a.shape[0], int(app))
+
+        def close(self):
+            if self.exec:
+                pd.check(pd.lib().pos_graph_destroy(self.exec))
+                self.exec = None
+
     class AppThread:
         """Long-lived application host thread: submits a window of kernels
         (pos_fill_batch) on the app stream, records event 2, and -- like an
@@ -495,6 +525,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             self.go, self.staged = threading.Event(), threading.Event()
             self.fill, self.h = pd.lib().pos_fill_batch, int(app)
             self.stw = None
+            self.loop, self.graph, self.stop_loop, self.iters = False, False, threading.Event(), 0
             threading.Thread(target=self.run, daemon=True).start()
 
         def run(self):
@@ -502,10 +533,21 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             while True:
                 self.go.wait()
                 self.go.clear()
+                window = app_window(self.q, self.graph)
                 eng.event_record(9, app)  # the application's window: 9 -> 2
-                for a in self.q:
-                    self.fill(a.ctypes.data, a.shape[0], self.h)
+                window()
+                self.iters = 1
+                # app-load pass: the application keeps iterating its window for
+                # the whole pre-copy, at most two iterations queued ahead
+                if self.loop:
+                    eng.event_record(20, app)  # end of iteration 1
+                while self.loop and not self.stop_loop.is_set():
+                    window()
+                    self.iters += 1
+                    eng.event_record(20 + (self.iters - 1) % 2, app)
+                    eng.event_elapsed(9, 20 + (self.iters - 2) % 2)  # host waits for the iteration before
                 eng.event_record(2, app)
+                window.close()
                 self.staged.wait()  # the engine is not re-entrant: after prepare_final_stop
                 self.staged.clear()
                 try:
@@ -514,8 +556,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                     self.stw_result, self.error = None, ex
                 self.done.set()
 
-        def submit(self, args_list, stw):
-            self.q, self.stw = args_list, stw
+        def submit(self, args_list, stw, loop=False, graph=False):
+            self.q, self.stw, self.loop, self.graph = args_list, stw, loop, graph
+            self.stop_loop.clear()
             self.done.clear()
             self.go.set()
 
@@ -525,7 +568,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     app_thread = AppThread()
     apply_threads = max(1, min(32, len(os.sched_getaffinity(0))))
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
-    def checkpoint(e: int, e2e: bool):
+    def checkpoint(e: int, e2e: bool, app_load: bool = False, app_graph: bool = False):
         pin = pins[e % len(pins)] if pins else None
         # untimed application iteration
         pd.fill_batch([(by_handle[h].dev_ptr + o, n, seed) for h, o, n, seed in wl.epoch_writes(e)])
@@ -558,7 +601,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             # the window is [event 3, gather, event 4] and nothing else
             return eng.at_final_stop(stream=ckpt, stw_begin_slot=3, stw_end_slot=4)
 
-        app_thread.submit(app_args, final_stop)  # the application's own host thread
+        app_thread.submit(app_args, final_stop, loop=app_load and bool(app_args),
+                          graph=app_graph)  # the application's own host thread
         eng.event_record(0, ckpt)  # device clock starts with the dump's first operation
         if direct:  # hash -> O1 -> scan per wave; chunks stored into the image on `copy`
             eng.precopy_direct(waves=args.waves, stream=ckpt, drain_stream=copy)
@@ -572,6 +616,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # stop window holds only the gather; then the final stop: hold the app
         # (its window is fully submitted) and drain it.
         eng.prepare_final_stop(stream=ckpt)
+        if app_load and direct:  # the application iterates until the host leg submitted its last slice
+            eng.host_leg_stats()
+            app_thread.stop_loop.set()
         app_thread.staged.set()
         app_thread.wait()
         if app_thread.error is not None:
@@ -613,7 +660,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             tl["packs_MB"] = [round(z / 1e6, 2) for _, z in packs] + [round(dbytes / 1e6, 2)]
             print(json.dumps(tl), file=sys.stderr)
         r = {"ms": ms, "stw_ms": stw, "stw_dev_ms": stw_dev, "hash_ms": hash_ms, "wall_ms": (t1 - t0) * 1e3,
-             "app_ms": eng.event_elapsed(9, 2) if window else 0.0,
+             "app_ms": eng.event_elapsed(9, 2) if window else 0.0, "app_iters": app_thread.iters if window else 0,
              "precopy_bytes": pre_payload if direct else sum(z for _, z in packs),
              "delta_bytes": dpay if direct else dbytes, "launches": eng.launches - launches0 + len(window),
              "d2h_ms": kms("d2h"), "compact_ms": kms("copy"),
@@ -647,6 +694,24 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         eng.event_record(2, app)
         app.synchronize()
         app_alone.append(eng.event_elapsed(9, 2))
+    # ... and iterated back to back with the app-load pass's own loop (host
+    # throttle included): the baseline of its throughput ratio
+    app_loop_alone = {}
+    if app_alone and direct and not args.no_window:
+        for graph in (False, True):
+            window, n_it = app_window(args_list, graph), 2000
+            window()  # warm
+            app.synchronize()
+            eng.event_record(9, app)
+            window()
+            eng.event_record(20, app)
+            for it in range(2, n_it + 1):
+                window()
+                eng.event_record(20 + (it - 1) % 2, app)
+                eng.event_elapsed(9, 20 + (it - 2) % 2)
+            eng.event_record(2, app)
+            app_loop_alone[graph] = eng.event_elapsed(9, 2) / n_it
+            window.close()
     log("timed steps")
     barrier(dist, local)
     res = []
@@ -656,6 +721,15 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             log(f"step {e}: {res[-1]['ms']:.2f} ms (stw {res[-1]['stw_ms']:.4f} ms, d2h {res[-1]['d2h_ms']:.2f} ms)")
             e += 1
     barrier(dist, local)
+    # Application under a continuous load: its window iterated through the
+    # whole pre-copy (every write DAG-tracked), untimed for the headline.
+    app_load = []
+    if direct and app_alone and not args.no_window:
+        log("application-load steps")
+        for graph in (False, False, True, True):
+            app_load.append(checkpoint(e, False, app_load=True, app_graph=graph))
+            app_load[-1]["graph"] = graph
+            e += 1
     log("e2e steps")
     e2e_res = []
     for _ in range(max(3, min(args.steps, 10))):
@@ -776,7 +850,26 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                 "window_ms_during_dump": round(statistics.median(r["app_ms"] for r in res), 4),
                 "slowdown": round(statistics.median(r["app_ms"] for r in res) / statistics.median(app_alone), 3),
                 "window": "the application kernels of the pre-copy window (k_fill of the DAG-dirty buffers), "
-                          "event-timed on the application stream"}} if app_alone else {}),
+                          "event-timed on the application stream",
+                **({"under_load": {
+                    "app_throughput_vs_alone": round(statistics.median(
+                        r["app_iters"] * app_loop_alone[False] / r["app_ms"] for r in app_load if not r["graph"]), 4),
+                    "app_throughput_vs_alone_graph": round(statistics.median(
+                        r["app_iters"] * app_loop_alone[True] / r["app_ms"] for r in app_load if r["graph"]), 4),
+                    "app_iteration_ms_alone": round(app_loop_alone[False], 4),
+                    "app_iteration_ms_alone_graph": round(app_loop_alone[True], 4),
+                    "app_iterations_per_step": int(statistics.median(r["app_iters"] for r in app_load)),
+                    "dump_gbps": round(total / (statistics.median(r["ms"] for r in app_load) * 1e-3) / 1e9, 3),
+                    "stw_ms": round(statistics.median(r["stw_ms"] for r in app_load), 4),
+                    "why": ("the window is launch-bound (9 kernels of ~25 us): while the host link is saturated "
+                            "every stream operation's command fetch waits behind the posted D2H writes; one CUDA "
+                            "graph launch per window instead of 9 launches (graph) cuts that cost: "
+                            "tools/frontend_micro.cu"),
+                    "how": ("4 extra checkpoints (not in value; 2 per variant): the application iterates its window back to back "
+                            "until the host leg has submitted its last slice; throughput = iterations x the "
+                            "iteration time of the same loop with no dump / event-timed application time")}}
+                   if app_load and len(app_loop_alone) == 2
+                   and statistics.median(r["app_iters"] for r in app_load) >= 10 else {})}} if app_alone else {}),
             "stages_ms": {k: round(statistics.mean(r[k] for r in res), 4)
                           for k in ("hash_ms", "scan_ms", "compact_ms", "delta_ms", "delta_hash_ms", "d2h_ms")},
             "e2e": {"value": round(world * total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
@@ -1182,6 +1275,8 @@ def main():
     ap.add_argument("--hash-sms", type=int, default=0,
                     help="SMs the hash may occupy (0 = all); the application's kernels get the rest")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
+    ap.add_argument("--slice-mib", type=int, default=0, help="host-leg slice size (default: the engine's 16 MiB)")
+    ap.add_argument("--window", type=int, default=0, help="host-leg slices in flight (default: the engine's 3)")
     ap.add_argument("--peer-cache-gb", type=float, default=0.0,
                     help="--mode stream: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")
     args = ap.parse_args()

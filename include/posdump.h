@@ -236,7 +236,9 @@ int pos_register_image(pos_ctx* ctx, uint8_t* const* hosts, const uint64_t* size
 int pos_precopy_direct(pos_ctx* ctx, int exclude_dag_dirty, uint32_t waves, void* ckpt_stream,
                        void* drain_stream);
 /* Chunks and payload bytes the last pos_precopy_direct shipped, and the end
- * of its index packs in the cache (waits for the scans only). */
+ * of its index packs in the cache.  Blocks until every byte of that
+ * pre-copy is in the image (the host leg submitted its last slice and the
+ * slice landed). */
 int pos_precopy_direct_result(pos_ctx* ctx, uint64_t* chunks, uint64_t* payload_bytes,
                               uint64_t* index_bytes);
 /* An application memcpy during a checkpoint (CopyEngine::submit(App),
@@ -372,6 +374,13 @@ int pos_crc32_update(uint32_t crc, uint64_t dev_ptr, uint64_t n, uint32_t* out, 
 int pos_fill(uint64_t dev_ptr, uint64_t n, uint64_t seed, void* stream);
 /* Batched form: ranges[i] = {dev_ptr, n, seed}. */
 int pos_fill_batch(const uint64_t* ranges, uint32_t count, void* stream);
+/* CUDA graphs for launch-bound callers (the bench's application window):
+ * capture what this thread enqueues on `stream` (thread-local mode), then
+ * launch the instantiated graph as ONE stream operation. */
+int pos_stream_begin_capture(void* stream);
+int pos_stream_end_capture(void* stream, void** graph_exec);
+int pos_graph_launch(void* graph_exec, void* stream);
+int pos_graph_destroy(void* graph_exec);
 
 /* ---- timing ----------------------------------------------------------- */
 int pos_event_record(pos_ctx* ctx, uint32_t slot, void* stream);

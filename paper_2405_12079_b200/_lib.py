@@ -159,6 +159,10 @@ SIGNATURES = {
     "pos_crc32_update": [U32, U64, U64, PU32, P],
     "pos_fill": [U64, U64, U64, P],
     "pos_fill_batch": [P, U32, P],
+    "pos_stream_begin_capture": [P],
+    "pos_stream_end_capture": [P, C.POINTER(C.c_void_p)],
+    "pos_graph_launch": [P, P],
+    "pos_graph_destroy": [P],
     "pos_event_record": [P, U32, P],
     "pos_event_elapsed": [P, U32, U32, C.POINTER(C.c_float)],
     "pos_stream_wait_event": [P, U32, P],

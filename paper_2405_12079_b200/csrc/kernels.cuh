@@ -1150,8 +1150,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
 // thread drives the pipeline.  Requires 16-B aligned src/dst (checked by the
 // host; otherwise k_copy_simt runs).  The <16-B remainder of an item and its
 // zero padding go through one vector store.
-constexpr int kCopyStages = 4;
-constexpr uint32_t kCopyPiece = 16384;
+constexpr int kCopyStages = 8;
+constexpr uint32_t kCopyPiece = 8192;
 constexpr uint32_t kCopySmem = kCopyStages * kCopyPiece + 64;
 
 

@@ -47,4 +47,16 @@ for gb in (4, G):
         for o in range(0, n // S2 * S2, S2):
             pd.check(mc(img.ptr + o, src.ptr + (o % (1 << 30)), S2, D2H, int(s1)))
     res[f"image_sweep_{gb}GB_64M_1stream"] = timed(sweep64, n // S2 * S2)
+    res[f"image_sweep_{gb}GB_16M_1stream_again"] = timed(lambda: sweep((s1,)), n)
     print(json.dumps(res), flush=True)
+del img
+# cudaHostAlloc'd destination at scale (the image is mmap + cudaHostRegister)
+H = int(os.environ.get("HOSTALLOC_GB", "16"))
+big = pd.PinnedHost(H * 10**9)
+n = H * 10**9 // S * S
+def sweep_h():
+    for o in range(0, n, S):
+        pd.check(mc(big.ptr + o, src.ptr + (o % (1 << 30)), S, D2H, int(s1)))
+res[f"hostalloc_sweep_{H}GB_16M_1stream"] = timed(sweep_h, n)
+res[f"hostalloc_sweep_{H}GB_16M_1stream_again"] = timed(sweep_h, n)
+print(json.dumps(res), flush=True)
