@@ -1322,7 +1322,21 @@ __device__ __forceinline__ void cta_copy_to_host(const uint8_t* s, uint8_t* d, u
     const uint64_t n16 = m >> 4;
     const uint4* s4 = reinterpret_cast<const uint4*>(s);
     uint4* d4 = reinterpret_cast<uint4*>(d);
-    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) {
+    // 4 loads in flight per thread before the stores: the HBM reads stay
+    // ahead of the link even when a hash wave saturates HBM beside them
+    constexpr int U = 4;
+    uint64_t i = threadIdx.x;
+    for (; i + (U - 1) * blockDim.x < n16; i += U * blockDim.x) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(s4 + i + u * blockDim.x));
+#pragma unroll
+      for (int u = 0; u < U; ++u) d4[i + u * blockDim.x] = v[u];
+    }
+    for (; i < n16; i += blockDim.x) {
       uint4 v;
       asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)

@@ -248,6 +248,9 @@ struct HostLeg {
   PinnedArray<uint64_t> ship;                 // [kMaxWindow][4][kShipMaxRuns]: a slot's short-run batch
   std::atomic<uint64_t> ship_launches{0};     // k_ship_runs launched by the feeder
   std::atomic<bool> shipped_last{false};      // the last job launched k_ship_runs
+  cudaStream_t s2 = nullptr;                  // second stream for k_ship_runs batches
+  int s2_prio = 0;
+  cudaEvent_t join_ev = nullptr;              // ds -> s2 at the start, s2 -> ds at the end
   int error_code = 0;
   std::string error;
 };
