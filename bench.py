@@ -724,7 +724,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # Application under a continuous load: its window iterated through the
     # whole pre-copy (every write DAG-tracked), untimed for the headline.
     app_load = []
-    if direct and app_alone and not args.no_window:
+    if direct and app_alone and not args.no_window and not args.no_app_load:
         log("application-load steps")
         for graph in (False, False, True, True):
             app_load.append(checkpoint(e, False, app_load=True, app_graph=graph))
@@ -1272,6 +1272,8 @@ def main():
     ap.add_argument("--ref-sample-bytes", type=int, default=1 << 30,
                     help="CPU reference: bounded sample (a prefix of the buffer set) of at least this many bytes")
     ap.add_argument("--no-window", action="store_true", help="diagnostic: no application kernels during the dump")
+    ap.add_argument("--no-app-load", action="store_true",
+                    help="skip the application-load checkpoints (after the timed steps; e.g. under ncu)")
     ap.add_argument("--hash-sms", type=int, default=0,
                     help="SMs the hash may occupy (0 = all); the application's kernels get the rest")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")

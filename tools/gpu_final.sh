@@ -11,5 +11,5 @@ timeout 600 python bench.py --workload c1 --steps 20 > $P/bench_c1.jsonl 2>/dev/
 timeout 900 python bench.py --workload c4 --steps 5 > $P/bench_c4.jsonl 2>/dev/null; cut -c1-300 $P/bench_c4.jsonl
 timeout 900 python bench.py --workload c3 --steps 3 > $P/bench_c3.jsonl 2>/dev/null; cut -c1-300 $P/bench_c3.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $P/launches_c5.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-app-load > /dev/null 2>&1
 ls -la $P

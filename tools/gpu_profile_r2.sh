@@ -3,7 +3,7 @@
 # STW gather (standalone: tools/profile_c5_wave.py).
 P=gpurun_out/r2prof; mkdir -p $P
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $P/launches_c5.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $P/launches_c5.out 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-app-load > $P/launches_c5.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_hash_chunks -s 2 -c 1 -o $P/hash_c5wave \
   python tools/profile_c5_wave.py > $P/hash_c5wave.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_copy_bulk -s 1 -c 1 -o $P/gather_c5 \
