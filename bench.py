@@ -526,6 +526,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             self.fill, self.h = pd.lib().pos_fill_batch, int(app)
             self.stw = None
             self.loop, self.graph, self.stop_loop, self.iters = False, False, threading.Event(), 0
+            self.submitted = threading.Event()
             threading.Thread(target=self.run, daemon=True).start()
 
         def run(self):
@@ -536,6 +537,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                 window = app_window(self.q, self.graph)
                 eng.event_record(9, app)  # the application's window: 9 -> 2
                 window()
+                self.submitted.set()
                 self.iters = 1
                 # app-load pass: the application keeps iterating its window for
                 # the whole pre-copy, at most two iterations queued ahead
@@ -559,6 +561,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         def submit(self, args_list, stw, loop=False, graph=False):
             self.q, self.stw, self.loop, self.graph = args_list, stw, loop, graph
             self.stop_loop.clear()
+            self.submitted.clear()
             self.done.clear()
             self.go.set()
 
@@ -568,7 +571,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     app_thread = AppThread()
     apply_threads = max(1, min(32, len(os.sched_getaffinity(0))))
     # slots: 0 start, 1 compact done, 2 app drained, 3 stop, 4 stw end, 5 end
-    def checkpoint(e: int, e2e: bool, app_load: bool = False, app_graph: bool = False):
+    def checkpoint(e: int, e2e: bool, app_load: bool = False, app_graph: bool = False, pregather: bool = False):
         pin = pins[e % len(pins)] if pins else None
         # untimed application iteration
         pd.fill_batch([(by_handle[h].dev_ptr + o, n, seed) for h, o, n, seed in wl.epoch_writes(e)])
@@ -616,6 +619,9 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # stop window holds only the gather; then the final stop: hold the app
         # (its window is fully submitted) and drain it.
         eng.prepare_final_stop(stream=ckpt)
+        if pregather and dag_writes:  # eager delta capture behind the window's writers (not with app_load:
+            app_thread.submitted.wait()  # its repeated writes are not re-recorded)
+            eng.pregather(dag_writes, after_stream=app, stream=ckpt)
         if app_load and direct:  # the application iterates until the host leg submitted its last slice
             eng.host_leg_stats()
             app_thread.stop_loop.set()
@@ -735,6 +741,15 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     for _ in range(max(3, min(args.steps, 10))):
         e2e_res.append(checkpoint(e, True))
         e += 1
+    # Eager delta capture: the window's buffers gathered behind their writers
+    # (pos_delta_pregather), so the stop gathers only what was written since;
+    # the last of them is the checkpoint the image-parity check restores
+    eager = []
+    if direct and not args.no_window:
+        log("eager-capture steps")
+        for _ in range(3):
+            eager.append(checkpoint(e, False, pregather=True))
+            e += 1
     # Image parity.  (1) 512 random chunks: host image bytes == device bytes;
     # (2) small states: every buffer byte for byte; large states (c3/c4/c5):
     # the device state is thrown away and restored from the host image, and
@@ -841,6 +856,14 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                           "peak_source": "best of 5 pinned cudaMemcpyAsync D2H of 256 MiB, measured in this run"},
             "per_rank": per_rank,
             "host_link_aggregate_gbps": round(sum(r["host_link_gbps"] for r in per_rank), 2),
+            **({"stw_eager_capture": {
+                "stw_ms": round(statistics.median(r["stw_ms"] for r in eager), 4),
+                "ms_per_step": round(statistics.median(r["ms"] for r in eager), 4),
+                "how": ("3 extra checkpoints (not in value): pos_delta_pregather gathers the window's DAG-dirty "
+                        "buffers into the delta pack behind their last writers, before the stop; the stop "
+                        "gathers only buffers written since (none here), the image bytes are the same; the "
+                        "last of them is the checkpoint image_parity restores")}}
+               if eager else {}),
             "stw_gather": {"bound": "hbm", "bytes": int(delta_bytes), "alg_bytes": int(2 * delta_bytes),
                            "achieved": round(stw_gbps, 1), "peak": peak, "unit": "GB/s",
                            "frac": round(stw_gbps / peak, 4) if peak else None,

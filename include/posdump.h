@@ -302,6 +302,14 @@ int pos_final_stop(pos_ctx* ctx, void* stream, int stw_begin_slot, int stw_end_s
  * holds only the kernel.  pos_delta_copy re-stages if dirty_set_ or the
  * pre-copy pack changed since. */
 int pos_delta_prepare(pos_ctx* ctx, void* stream, uint64_t* pack_offset, uint64_t* pack_bytes);
+/* Eager delta capture: gather the listed DAG-dirty buffers into their slots
+ * of the prepared delta pack now, on `stream` behind everything
+ * `after_stream` has enqueued so far (their last writers), so the final stop
+ * gathers only the rest.  A buffer recorded dirty again afterwards
+ * (pos_record_dirty: a later writer) is re-gathered at the stop.  The image
+ * equals at_final_stop's re-copy (cr.hpp:599-621) either way.  Needs a
+ * current pos_delta_prepare (else POS_E_BAD_STATE). */
+int pos_delta_pregather(pos_ctx* ctx, const uint64_t* handles, uint32_t n, void* after_stream, void* stream);
 
 /* ---- host leg ------------------------------------------------------------- */
 /* Pinned D2H of cache[offset, offset+bytes) into host_dst, on `stream`, in

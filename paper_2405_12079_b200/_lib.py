@@ -159,6 +159,7 @@ SIGNATURES = {
     "pos_crc32_update": [U32, U64, U64, PU32, P],
     "pos_fill": [U64, U64, U64, P],
     "pos_fill_batch": [P, U32, P],
+    "pos_delta_pregather": [P, P, U32, P, P],
     "pos_stream_begin_capture": [P],
     "pos_stream_end_capture": [P, C.POINTER(C.c_void_p)],
     "pos_graph_launch": [P, P],

@@ -327,6 +327,12 @@ struct pos_ctx {
   bool delta_drain = false;  // drain items staged with the delta
   bool drain_short = false;  // ... some of them shorter than kCeRun (k_ship_runs)
   DevArray<CopyItem> d_delta_items;
+  // eager delta capture (pos_delta_pregather): per buffer index, the delta
+  // pack's items [first, first + count) and whether they were gathered
+  // after the buffer's last writer, ahead of the stop
+  std::vector<uint2> delta_items_of;
+  std::vector<uint8_t> pregathered;
+  cudaEvent_t ev_pregather = nullptr;
   // host image (pos_register_image): device-visible address per buffer, and
   // the host ranges this context pinned itself (unpinned at destroy)
   bool image_ready = false;

@@ -524,6 +524,13 @@ class DumpEngine:
         check(lib().pos_delta_prepare(self.ctx, _s(stream), C.byref(off), C.byref(n)))
         return off.value, n.value
 
+    def pregather(self, handles: Iterable[int], after_stream=None, stream=None) -> None:
+        """Eager delta capture (pos_delta_pregather): gather these DAG-dirty
+        buffers into the prepared delta pack behind after_stream's writers."""
+        hs = np.array(sorted(handles), dtype=np.uint64)
+        check(lib().pos_delta_pregather(self.ctx, hs.ctypes.data if hs.size else None, int(hs.size),
+                                        _s(after_stream), _s(stream)))
+
     # ---- host leg
     def d2h_async(self, host_ptr: int, offset: int, nbytes: int, stream=None, slice_bytes: int = 0) -> None:
         check(lib().pos_d2h_async(self.ctx, host_ptr, offset, nbytes, slice_bytes, _s(stream)))

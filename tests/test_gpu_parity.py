@@ -1610,3 +1610,45 @@ def test_direct_host_leg_short_and_long_runs(orc, offsets):
         assert np.array_equal(image[i], p.host[i]), f"epoch 1 buffer {i}"
     assert np.array_equal(image[2], marker[2])
     eng.close()
+
+
+@pytest.mark.parametrize("cs,offsets", [(4096, None), (65536, [0, 3, 0, 9, 0])])
+def test_delta_pregather_equals_stop_gather(orc, cs, offsets):
+    """Eager delta capture (pos_delta_pregather): buffers gathered behind
+    their last writer before the stop, one of them written again and
+    re-recorded dirty (a later writer), the rest gathered at the stop -- the
+    delta pack is byte-identical to the reference's at_final_stop re-copy of
+    the final contents (cr.hpp:599-621), and the post-stop digests match."""
+    sizes = [3 * cs, 5000, 100, 2 * cs + 33, 4 * cs]
+    p = Proc(orc, sizes, seed0=7700, handles=[2, 4, 6, 8, 10], offsets=offsets)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=4 << 20))
+    eng.register_buffers(p.bufs)
+    n0 = eng.plan_precopy()
+    dirty = [4, 8, 10]
+    eng.record_dirty(dirty)
+    eng.prepare_final_stop()
+    ckpt = pd.Stream()
+    # the window's writers on the application stream, each buffer captured behind its writer
+    p.write(1, 10, 4000, 31)
+    p.write(3, 0, 2 * cs, 32)
+    eng.pregather([4, 8], after_stream=None, stream=ckpt)
+    p.write(4, 7, 3 * cs, 33)
+    eng.pregather([10], after_stream=None, stream=ckpt)
+    # a later writer of buffer 8: re-recorded dirty -> gathered again at the stop
+    p.write(3, 5, 100, 34)
+    eng.record_dirty([8])
+    eng.pregather([4], after_stream=None, stream=ckpt)  # already captured: no-op
+    pd.device_synchronize()
+    off, n1 = eng.at_final_stop(stream=ckpt, stw_begin_slot=3, stw_end_slot=4)
+    ckpt.synchronize()
+    assert off == (n0 + 255) // 256 * 256
+    got = download_cache(eng, off, n1)
+    g_flags = np.concatenate([np.full(b.chunk_count(cs), b.handle in dirty, np.uint8) for b in p.bufs])
+    want = opack(orc, list(zip(p.handles, p.host)), cs, g_flags, epoch=0, pflags=1)
+    assert np.array_equal(got, want)
+    cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests()[g_flags == 1], cur[g_flags == 1])
+    # the stop consumed the preparation: a new pregather needs a new one
+    with pytest.raises(pd.SimError):
+        eng.pregather([4], stream=ckpt)
+    eng.close()
