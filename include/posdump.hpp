@@ -234,6 +234,15 @@ class DumpEngine {
   }
   const std::set<BufferHandle>& dirty_set() const { return dirty_; }
 
+  // Eager delta capture: DAG-dirty buffers whose last writer is already on
+  // after_stream are gathered into the prepared delta pack now; the stop
+  // gathers only the rest (pos_delta_pregather).
+  void prepare_final_stop(void* stream = nullptr) { check(pos_delta_prepare(ctx_, stream, nullptr, nullptr)); }
+  void pregather(const std::vector<BufferHandle>& done_writing, void* after_stream, void* stream = nullptr) {
+    check(pos_delta_pregather(ctx_, done_writing.data(), static_cast<uint32_t>(done_writing.size()), after_stream,
+                              stream));
+  }
+
   // at_final_stop (cr.hpp:599-621): the STW delta pack.
   PackRef at_final_stop(void* stream = nullptr) {
     PackRef r;

@@ -295,6 +295,36 @@ TEST_CASE("[gpu] staging exhaustion surfaces as StagingExhausted") {
   }
 }
 
+TEST_CASE("[gpu] eager delta capture: pregathered buffers land as the stop gather would") {  // cr.hpp:599-621
+  SimConfig cfg;
+  cfg.chunk_size = 4096;
+  cfg.cache_capacity = 4 << 20;
+  DumpEngine e(cfg);
+  DevBuf a(5 * 4096 + 9, 81), b(6000, 82), c(4096 * 2, 83);
+  e.snapshot({GpuBuffer{1, a.ptr, a.size}, GpuBuffer{2, b.ptr, b.size}, GpuBuffer{3, c.ptr, c.size}});
+  std::map<BufferHandle, std::vector<uint8_t>> captured{
+      {1, std::vector<uint8_t>(a.size)}, {2, std::vector<uint8_t>(b.size)}, {3, std::vector<uint8_t>(c.size)}};
+  auto ship = [&](const PackRef& p) {
+    std::vector<uint8_t> pk = pinned_d2h(e, p);
+    apply_pack(pk.data(), pk.size(), captured, 2);
+  };
+  ship(e.plan_precopy());
+  e.record_dirty({1, 2, 3});
+  e.prepare_final_stop();
+  a.write(7, 5000, 84);
+  b.write(0, b.size, 85);
+  e.pregather({1, 2}, nullptr);  // behind their writers on the legacy stream
+  c.write(100, 300, 86);
+  b.write(10, 20, 87);           // a later writer of buffer 2: recorded, so the stop re-gathers it
+  e.record_dirty({2});
+  check(pos_device_sync());
+  PackRef fin = e.at_final_stop(nullptr, 3, 4);
+  ship(fin);
+  REQUIRE(captured[1] == a.host);
+  REQUIRE(captured[2] == b.host);
+  REQUIRE(captured[3] == c.host);
+}
+
 int main(int argc, char** argv) { return minicatch::run(argc, argv); }
 
 TEST_CASE("[gpu] direct pre-copy writes chunk_copied's bytes straight into captured_") {
