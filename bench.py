@@ -1203,17 +1203,20 @@ def cpu_breakdown(wl: Workload, threads: int, sample_bytes: int) -> dict:
             t.append(time.perf_counter() - t0)
         return round(acc / min(t) / 1e9, 3)
 
-    def crc_buf(a):
-        for o in range(0, a.size, CHUNK):
-            ref.ref_crc32(a.ctypes.data + o, min(CHUNK, a.size - o))
+    # the chunks of the sample, dealt in contiguous ranges over the threads
+    # (ctypes drops the GIL inside ref_crc32)
+    chunks = [(a.ctypes.data + o, min(CHUNK, a.size - o)) for a in bufs for o in range(0, a.size, CHUNK)]
+
+    def crc_range(t, nt):
+        for p, n in chunks[len(chunks) * t // nt:len(chunks) * (t + 1) // nt]:
+            ref.ref_crc32(p, n)
 
     def crc_all(nt):
         if nt == 1:
-            for a in bufs:
-                crc_buf(a)
+            crc_range(0, 1)
         else:
             with ThreadPoolExecutor(nt) as ex:
-                list(ex.map(crc_buf, bufs))
+                list(ex.map(lambda t: crc_range(t, nt), range(nt)))
 
     sizes = np.array([a.size for a in bufs], np.uint64)
     ptrs = (C.c_void_p * len(bufs))(*[a.ctypes.data for a in bufs])
