@@ -534,22 +534,28 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
             while True:
                 self.go.wait()
                 self.go.clear()
-                window = app_window(self.q, self.graph)
-                eng.event_record(9, app)  # the application's window: 9 -> 2
-                window()
-                self.submitted.set()
-                self.iters = 1
-                # app-load pass: the application keeps iterating its window for
-                # the whole pre-copy, at most two iterations queued ahead
-                if self.loop:
-                    eng.event_record(20, app)  # end of iteration 1
-                while self.loop and not self.stop_loop.is_set():
+                try:
+                    window = app_window(self.q, self.graph)
+                    eng.event_record(9, app)  # the application's window: 9 -> 2
                     window()
-                    self.iters += 1
-                    eng.event_record(20 + (self.iters - 1) % 2, app)
-                    eng.event_elapsed(9, 20 + (self.iters - 2) % 2)  # host waits for the iteration before
-                eng.event_record(2, app)
-                window.close()
+                    self.submitted.set()
+                    self.iters = 1
+                    # app-load pass: the application keeps iterating its window for
+                    # the whole pre-copy, at most two iterations queued ahead
+                    if self.loop:
+                        eng.event_record(20, app)  # end of iteration 1
+                    while self.loop and not self.stop_loop.is_set():
+                        window()
+                        self.iters += 1
+                        eng.event_record(20 + (self.iters - 1) % 2, app)
+                        eng.event_elapsed(9, 20 + (self.iters - 2) % 2)  # host waits for the iteration before
+                    eng.event_record(2, app)
+                    window.close()
+                except Exception as ex:  # never leave the main thread waiting: surfaced by wait()
+                    self.stw_result, self.error = None, ex
+                    self.submitted.set()
+                    self.done.set()
+                    continue
                 self.staged.wait()  # the engine is not re-entrant: after prepare_final_stop
                 self.staged.clear()
                 try:
@@ -621,6 +627,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         eng.prepare_final_stop(stream=ckpt)
         if pregather and dag_writes:  # eager delta capture behind the window's writers (not with app_load:
             app_thread.submitted.wait()  # its repeated writes are not re-recorded)
+            if app_thread.done.is_set() and app_thread.error is not None:
+                raise app_thread.error
             eng.pregather(dag_writes, after_stream=app, stream=ckpt)
         if app_load and direct:  # the application iterates until the host leg submitted its last slice
             eng.host_leg_stats()
