@@ -525,14 +525,16 @@ def test_pipelined_precopy_matches_single_pack(orc, waves):
     eng.close()
 
 
-@pytest.mark.parametrize("profile,seed,mode", [
-    ("gpt2-infer-desk", 1, 3),    # inference: parameters H2D-loaded -> DedupRef records
-    ("resnet-train-desk", 1, 3),  # training under DAG retention
-    ("fuzz", 7, 3),
-    ("fuzz", 8, 1),               # stop-the-world image
-    ("ppo-train-desk", 2, 3),     # a Recompute record
+@pytest.mark.parametrize("profile,seed,mode,eager", [
+    ("gpt2-infer-desk", 1, 3, False),    # inference: parameters H2D-loaded -> DedupRef records
+    ("resnet-train-desk", 1, 3, False),  # training under DAG retention
+    ("fuzz", 7, 3, False),
+    ("fuzz", 8, 1, False),               # stop-the-world image
+    ("ppo-train-desk", 2, 3, False),     # a Recompute record
+    ("resnet-train-desk", 1, 3, True),   # eager delta capture: the same image
+    ("ppo-train-desk", 2, 3, True),
 ])
-def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode):
+def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode, eager):
     """Drop-in parity at engine level (P3 + P4): the reference CrEngine
     checkpoints a trace (checkpoint_at's flow, scenario.hpp:63-78); the
     device state at its cut is loaded onto the GPU with the session's
@@ -573,6 +575,9 @@ def test_reference_engine_image_is_reproduced(orc, ref, profile, seed, mode):
     eng.precopy_direct(waves=2, stream=s, drain_stream=d)
     eng.precopy_direct_result()
     d.synchronize()
+    if eager:  # every re-copied buffer already holds its bytes at the cut: captured before the stop
+        eng.prepare_final_stop(stream=s)
+        eng.pregather(recopy, stream=s)
     eng.at_final_stop(stream=s)
     d.wait(s)
     eng.delta_drain(stream=d)
