@@ -405,8 +405,8 @@ int pos_timeline(pos_ctx* ctx, uint32_t slot, float* out14);
 int pos_stamp(pos_ctx* ctx, uint32_t slot, void* stream);
 int pos_stamp_elapsed(pos_ctx* ctx, uint32_t a, uint32_t b, float* ms);
 /* SMs the hash kernel may occupy (0 = all, the default).  Each hash CTA
- * holds a whole SM for its wave (192 KiB of tables), so the application's
- * kernels run on the rest -- the ChecksumEngine's rate budget (checksum_bw,
+ * holds an SM's shared memory for its wave (192 KiB of tables) and 3/4 of
+ * its registers, so the application's kernels run beside it and on the rest -- the ChecksumEngine's rate budget (checksum_bw,
  * config.hpp:20-23) on a real GPU.  A host-link-bound dump needs ~1/8 of
  * the SMs to keep its hash ahead of the copy engine. */
 int pos_set_hash_sms(pos_ctx* ctx, uint32_t sms);

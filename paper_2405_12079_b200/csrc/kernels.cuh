@@ -107,7 +107,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // Hash kernel geometry.
 constexpr int kHashThreads = 512;            // 16 warps, 1 CTA per SM
 constexpr int kStepBytes = 512;              // one warp step: 32 lanes x 16 B
-constexpr int kUnroll = 8;                   // warp steps per batch (4 KiB per warp)
+constexpr int kUnroll = 6;                   // warp steps per batch (3 KiB per warp)
 constexpr uint32_t kRepTableBytes = 131072;  // lane-replicated Z^512: 4 x 256 x 32 lanes x 4 B
 constexpr uint32_t kSmallTablesBytes = 6 * 4096;
 // The replicated table sits at ABSOLUTE shared address 0x10000, so the PRMT
@@ -400,10 +400,14 @@ __device__ unsigned long long g_hash_prof[1024][16][5];
 // kModeCopy: every work item -> digest + pack entry + payload (hash while copying).
 // kModeCached: every work item's payload, already in the pack -> digest + entry.
 // One CTA of kHashThreads per SM (the replicated table takes 192 KiB of
-// shared memory); <= 120 registers leave room for the small scan / copy
-// CTAs of the other streams on the same SM.
+// shared memory).  <= 96 registers (batches of 6 steps) leave a quarter of
+// the register file to other CTAs on the same SM -- the application's and
+// the dump's own scan / ship / copy kernels.  Measured on a config-5 wave
+// (7.5 GB): 8 steps / 120 registers 1.203 ms, 6 / 96 1.22 ms; the
+// application's optimizer-tail window launched beside the dump's first
+// waves: 17x -> 1.8x slower than alone (profiles/r2/hash_regs.txt).
 template <int MODE>
-__global__ void __maxnreg__(120) k_hash_chunks(HashParams p) {
+__global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
   constexpr int kThreads = kHashThreads;
   constexpr bool COPY = MODE == kModeCopy;
   constexpr bool WORK = MODE != kModeHash;

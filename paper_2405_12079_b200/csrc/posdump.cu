@@ -406,7 +406,8 @@ struct pos_ctx {
   }
   // SMs the dump's hash may occupy (pos_set_hash_sms; 0 = all): the
   // ChecksumEngine's budget (checksum_bw, config.hpp:20-23) -- every hash CTA
-  // holds a whole SM for its wave, so the application's kernels get the rest.
+  // holds its SM's shared memory for its wave (the application's CTAs
+  // co-reside in the registers it leaves), the rest of the SMs are theirs.
   uint32_t hash_sms = 0;
   int hash_sm_budget() const {
     return hash_sms && (int)hash_sms < crc.sm_count ? (int)hash_sms : crc.sm_count;
