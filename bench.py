@@ -711,7 +711,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     # ... and iterated back to back with the app-load pass's own loop (host
     # throttle included): the baseline of its throughput ratio
     app_loop_alone = {}
-    if app_alone and direct and not args.no_window:
+    if app_alone and direct and not args.no_window and not args.no_app_load:
         for graph in (False, True):
             window, n_it = app_window(args_list, graph), 2000
             window()  # warm
