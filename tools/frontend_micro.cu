@@ -1,10 +1,13 @@
 // Why a launch-bound application slows down while the copy engine saturates
 // the host link: an iteration of 9 short HBM kernels (125 MB fills, ~25 us
 // each) timed alone and beside a continuous D2H into pinned memory, issued
-// as 9 stream launches or as one CUDA graph launch.
+// as 9 stream launches or as one CUDA graph launch; and beside a duty-cycled
+// D2H (an idle gap after every slice).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/frontend_micro tools/frontend_micro.cu -lpthread
 #include <cuda_runtime.h>
 #include <atomic>
+#include <chrono>
+#include <utility>
 #include <cstdint>
 #include <cstdio>
 #include <thread>
@@ -54,15 +57,24 @@ int main() {
     return ms / iters;
   };
   std::atomic<bool> stop{false};
-  auto ce_loop = [&]() {  // windowed 16 MiB slices, 3 in flight, until stopped
+  std::atomic<uint64_t> moved{0};
+  int gap_us = 0;  // idle time after every slice (a duty cycle below the link)
+  size_t slice = S;
+  auto ce_loop = [&]() {  // windowed slices, 3 in flight (1 with a gap), until stopped
     cudaEvent_t ring[3];
     for (auto& e : ring) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     uint64_t k = 0;
+    const int W = gap_us ? 1 : 3;
     while (!stop.load()) {
-      if (k >= 3) cudaEventSynchronize(ring[k % 3]);
-      const size_t o = (k * S) % ce_bytes;
-      cudaMemcpyAsync(ce_dst + o, ce_src + o, S, cudaMemcpyDeviceToHost, ce);
-      cudaEventRecord(ring[k % 3], ce);
+      if (k >= (uint64_t)W) cudaEventSynchronize(ring[k % W]);
+      if (gap_us && k) {
+        auto t0 = std::chrono::steady_clock::now();
+        while (std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(gap_us)) {}
+      }
+      const size_t o = (k * slice) % (ce_bytes - slice);
+      cudaMemcpyAsync(ce_dst + o, ce_src + o, slice, cudaMemcpyDeviceToHost, ce);
+      cudaEventRecord(ring[k % W], ce);
+      moved += slice;
       ++k;
     }
     cudaStreamSynchronize(ce);
@@ -71,14 +83,23 @@ int main() {
   run_app(false, 20);
   run_app(true, 20);
   const float alone_s = run_app(false, 400), alone_g = run_app(true, 400);
-  std::thread t(ce_loop);
-  run_app(false, 20);
-  const float ce_s = run_app(false, 400), ce_g = run_app(true, 400);
-  stop = true;
-  t.join();
-  printf("app iteration (9 x 125 MB fill kernels), ms per iteration\n");
-  printf("  stream launches : alone %.4f  beside CE D2H %.4f  (%.2fx)\n", alone_s, ce_s, ce_s / alone_s);
-  printf("  one graph launch: alone %.4f  beside CE D2H %.4f  (%.2fx)\n", alone_g, ce_g, ce_g / alone_g);
+  printf("app iteration (9 x 125 MB fill kernels), ms per iteration: alone %.4f (stream launches), %.4f (graph)\n",
+         alone_s, alone_g);
+  for (auto [g, sl] : {std::pair<int, size_t>{0, S}, {20, S}, {60, S}, {10, 4 << 20}, {30, 4 << 20}}) {
+    gap_us = g;
+    slice = sl;
+    stop = false;
+    moved = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    std::thread t(ce_loop);
+    run_app(false, 20);
+    const float ce_s = run_app(false, 400), ce_g = run_app(true, 400);
+    stop = true;
+    t.join();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    printf("  D2H %2d MiB slices, gap %2d us: link %5.1f GB/s | stream launches %.4f (%.2fx)  graph %.4f (%.2fx)\n",
+           (int)(sl >> 20), g, moved.load() / sec / 1e9, ce_s, ce_s / alone_s, ce_g, ce_g / alone_g);
+  }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
