@@ -1657,3 +1657,27 @@ def test_delta_pregather_equals_stop_gather(orc, cs, offsets):
     with pytest.raises(pd.SimError):
         eng.pregather([4], stream=ckpt)
     eng.close()
+
+
+def test_empty_buffer_set_checkpoint(orc, ref):
+    """A process with no live allocation (test_image.cpp:86-95's empty image):
+    the pre-copy pack and the STW delta are header-only, the scatter of an
+    empty pack is a no-op, and finalize writes the reference's 64-byte
+    image."""
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=1 << 20))
+    eng.register_buffers([])
+    n = eng.plan_precopy()
+    pack = download_cache(eng, 0, n)
+    assert pack[:4].tobytes() == b"POSD" and int(pack[16:20].view(np.uint32)[0]) == 0
+    eng.record_dirty([1, 2])  # handles outside the (empty) snapshot are ignored (cr.hpp:904)
+    off, m = eng.at_final_stop()
+    delta = download_cache(eng, off, m)
+    assert int(delta[16:20].view(np.uint32)[0]) == 0
+    dev = pd.DeviceMemory(max(n, 256))
+    dev.upload(pack)
+    eng.materialize(dev.ptr, n)
+    pd.device_synchronize()
+    out, metrics = pd.finalize_image(pd.CheckpointImage(page_size=4096), [], engine=eng)
+    assert len(out) == 64 and out == pd.write_image(pd.CheckpointImage(page_size=4096))
+    assert metrics["bytes_precopy"] == metrics["bytes_dirty"] == 0
+    eng.close()

@@ -119,3 +119,71 @@ def test_full_size_parity(orc, name):
     eng.close()
     mem.close()
     del d0
+
+
+def test_buffers_beyond_4gib(orc):
+    """64-bit offsets everywhere (buffer.hpp sizes are uint64_t): two buffers
+    larger than 4 GiB and a tiny one.  Chunk digests past the 4 GiB mark ==
+    crc32 of the oracle's bytes, the digest table folds into each buffer's
+    device CRC, a sparse epoch's direct pre-copy lands every written chunk
+    at image + ci * chunk_size beyond 4 GiB, and the STW gather of a 5 GiB
+    DAG-dirty buffer (a > 4 GiB delta pack) drains into the image intact."""
+    G = 1 << 30
+    sizes = [5 * G + 12345, 3, 4 * G + 2 * CS + 7]
+    stride = [(n + 255) // 256 * 256 for n in sizes]
+    offs = [0, stride[0], stride[0] + stride[1]]
+    mem = pd.DeviceMemory(sum(stride))
+    bufs = [pd.GpuBuffer(handle=i + 1, dev_ptr=mem.ptr + o, size=n) for i, (o, n) in enumerate(zip(offs, sizes))]
+    seeds = {1: 61, 2: 62, 3: 63}
+    pd.fill_batch([(b.dev_ptr, b.size, seeds[b.handle]) for b in bufs])
+    pd.device_synchronize()
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=CS, cache_capacity=6 * G))
+    eng.register_buffers(bufs)
+    img = pd.PinnedHost(sum(stride), image=True)
+    image = [img.array[o:o + n] for o, n in zip(offs, sizes)]
+    eng.register_image(image)
+    nch = [(n + CS - 1) // CS for n in sizes]
+    base = [0, nch[0], nch[0] + nch[1]]
+    s, d = pd.Stream(), pd.Stream()
+    eng.precopy_direct(waves=2, stream=s, drain_stream=d)
+    eng.precopy_direct_result()
+    d.synchronize()
+    dig = eng.digests()
+    eng.scan_dedup()
+    crcs, _ = eng.buffer_crcs()
+    rng = np.random.default_rng(7)
+    for i in (0, 2):
+        hi = np.arange((4 * G) // CS - 2, nch[i])  # the chunks around and past 4 GiB, all of them
+        for c in np.concatenate([hi, rng.choice(nch[i], 256, replace=False)]):
+            want = chunk_bytes(orc, sizes[i], seeds[i + 1], [], int(c))
+            assert dig[base[i] + c] == orc.or_crc32(want.ctypes.data, want.size), (i, c)
+            if c % 64 == 0 or c == nch[i] - 1:
+                assert np.array_equal(image[i][c * CS:c * CS + want.size], want), (i, c)
+        dd = np.ascontiguousarray(dig[base[i]:base[i] + nch[i]])
+        assert orc.or_fold_digests(dd.ctypes.data, sizes[i], CS) == crcs[i], i
+    eng.commit_epoch()
+    # epoch 1: sparse writes past 4 GiB in buffer 3; buffer 1 rewritten whole by the "window" (DAG-dirty)
+    writes3 = [(4 * G + 100, 5000, 71), (4 * G + CS + 3, 2 * CS, 72), (17 * CS, 9, 73)]
+    pd.fill_batch([(bufs[2].dev_ptr + o, n, sd) for o, n, sd in writes3])
+    eng.record_dirty([1])
+    pd.fill_batch([(bufs[0].dev_ptr, sizes[0], 81)])
+    pd.device_synchronize()
+    eng.precopy_direct(waves=2, stream=s, drain_stream=d)
+    nship, _ = eng.precopy_direct_result()
+    touched = sorted({c for o, n, _ in writes3 for c in range(o // CS, (o + n - 1) // CS + 1)})
+    assert nship == len(touched)
+    off, m = eng.at_final_stop(stream=s)
+    assert m > 5 * G
+    d.wait(s)
+    eng.delta_drain(stream=d)
+    d.synchronize()
+    s.synchronize()
+    for c in touched:
+        want = chunk_bytes(orc, sizes[2], seeds[3], writes3, c)
+        assert np.array_equal(image[2][c * CS:c * CS + want.size], want), c
+    for c in list(range(0, nch[0], 997)) + [(4 * G) // CS, nch[0] - 1]:
+        want = chunk_bytes(orc, sizes[0], 81, [], c)
+        assert np.array_equal(image[0][c * CS:c * CS + want.size], want), c
+    eng.close()
+    img.close()
+    mem.close()
