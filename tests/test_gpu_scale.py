@@ -163,7 +163,7 @@ def test_buffers_beyond_4gib(orc):
         assert orc.or_fold_digests(dd.ctypes.data, sizes[i], CS) == crcs[i], i
     eng.commit_epoch()
     # epoch 1: sparse writes past 4 GiB in buffer 3; buffer 1 rewritten whole by the "window" (DAG-dirty)
-    writes3 = [(4 * G + 100, 5000, 71), (4 * G + CS + 3, 2 * CS, 72), (17 * CS, 9, 73)]
+    writes3 = [(4 * G + 100, 5000, 71), (4 * G + CS + 3, CS + 4, 72), (17 * CS, 9, 73)]  # the 2nd ends at the buffer end
     pd.fill_batch([(bufs[2].dev_ptr + o, n, sd) for o, n, sd in writes3])
     eng.record_dirty([1])
     pd.fill_batch([(bufs[0].dev_ptr, sizes[0], 81)])
