@@ -1066,7 +1066,9 @@ def cpu_model() -> str:
 def bench_config(wl: Workload, world: int) -> dict:
     """The config dict both arms print (the driver compares them)."""
     cfg = {"workload": wl.desc, "workload_id": wl.name, "chunk_size": CHUNK, "state_bytes_per_gpu": wl.total,
-           "buffers": len(wl.sizes), "parallelism": f"replicas{world}"}
+           "buffers": len(wl.sizes), "parallelism": f"replicas{world}",
+           "l2": "flushed between timed steps (256 MiB memset)" +
+                 ("; the state is also larger than L2" if wl.total > 126 << 20 else "")}
     return cfg
 
 
