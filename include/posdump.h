@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define POSDUMP_ABI_VERSION 2
+#define POSDUMP_ABI_VERSION 3  /* 3: pos_delta_pregather, graph capture, precopy_direct_result waits for the landing */
 
 enum {
   POS_OK = 0,

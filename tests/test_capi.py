@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
-    assert lib.pos_abi_version() == 2
+    assert lib.pos_abi_version() == 3
 
 
 def test_error_codes_mirror_errc():
