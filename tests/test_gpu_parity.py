@@ -1681,3 +1681,67 @@ def test_empty_buffer_set_checkpoint(orc, ref):
     assert len(out) == 64 and out == pd.write_image(pd.CheckpointImage(page_size=4096))
     assert metrics["bytes_precopy"] == metrics["bytes_dirty"] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_direct_checkpoint_random_sessions(orc, trial):
+    """Randomised direct-mode sessions against the host mirror: chunk sizes
+    (incl. not a multiple of 16), buffer sizes from 1 B to 12 MB at odd
+    offsets, 1-4 waves, random sparse and whole-buffer writes, a random DAG
+    dirty set (some written during the pre-copy, some pregathered), three
+    epochs.  After every final stop + drain the image equals the device
+    state, and image bytes between the buffers' ranges are never written
+    (chunk_copied / at_final_stop, cr.hpp:447-621)."""
+    rng = np.random.default_rng(1000 + trial)
+    cs = int(rng.choice([1000, 4096, 16384, 65536]))
+    nb = int(rng.integers(3, 12))
+    sizes = [int(rng.choice([1, 17, cs - 1, cs, cs + 1, 3 * cs + 5])) if rng.random() < 0.4
+             else int(rng.integers(1, 12 << 20)) for _ in range(nb)]
+    offsets = [int(rng.integers(0, 16)) for _ in range(nb)]
+    p = Proc(orc, sizes, seed0=20000 + 100 * trial, offsets=offsets)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=sum(sizes) + (64 << 20)))
+    eng.register_buffers(p.bufs)
+    gap = 64
+    pin = pd.PinnedHost(sum(n + gap for n in sizes))
+    pin.array[:] = 0xAB
+    image, o = [], 0
+    for n in sizes:
+        image.append(pin.array[o:o + n])
+        o += n + gap
+    eng.register_image(image)
+    ckpt, drain = pd.Stream(), pd.Stream()
+    for epoch in range(3):
+        if epoch:
+            for _ in range(int(rng.integers(1, 3 * nb))):
+                i = int(rng.integers(nb))
+                off = int(rng.integers(sizes[i]))
+                n = int(rng.integers(1, sizes[i] - off + 1))
+                p.write(i, off, n, int(rng.integers(1 << 30)))
+        pd.device_synchronize()
+        dag = sorted({int(h) for h in rng.choice(p.handles, int(rng.integers(0, nb)), replace=False)})
+        eng.record_dirty(dag)
+        eng.precopy_direct(waves=int(rng.integers(1, 5)), stream=ckpt, drain_stream=drain)
+        late = [h for h in dag if rng.random() < 0.5]  # written during the pre-copy window
+        for h in late:
+            i = p.handles.index(h)
+            off = int(rng.integers(sizes[i]))
+            p.write(i, off, int(rng.integers(1, sizes[i] - off + 1)), int(rng.integers(1 << 30)))
+        pd.device_synchronize()
+        eng.prepare_final_stop(stream=ckpt)
+        early = [h for h in dag if h not in late and rng.random() < 0.5]
+        if early:
+            eng.pregather(early, stream=ckpt)
+        eng.at_final_stop(stream=ckpt)
+        eng.delta_drain(stream=drain)
+        drain.synchronize()
+        ckpt.synchronize()
+        eng.precopy_direct_result()
+        for i in range(nb):
+            assert np.array_equal(image[i], p.host[i]), (trial, epoch, i, sizes[i], cs)
+        o = 0
+        for n in sizes:  # the gaps between image ranges: untouched
+            assert np.all(pin.array[o + n:o + n + gap] == 0xAB), (trial, epoch)
+            o += n + gap
+        eng.commit_epoch()
+        eng.clear_dirty()
+    eng.close()
