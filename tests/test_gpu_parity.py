@@ -1683,7 +1683,7 @@ def test_empty_buffer_set_checkpoint(orc, ref):
     eng.close()
 
 
-@pytest.mark.parametrize("trial", range(6))
+@pytest.mark.parametrize("trial", range(24))
 def test_direct_checkpoint_random_sessions(orc, trial):
     """Randomised direct-mode sessions against the host mirror: chunk sizes
     (incl. not a multiple of 16), buffer sizes from 1 B to 12 MB at odd
