@@ -1745,3 +1745,70 @@ def test_direct_checkpoint_random_sessions(orc, trial):
         eng.commit_epoch()
         eng.clear_dirty()
     eng.close()
+
+
+@pytest.mark.parametrize("trial", range(16))
+def test_pack_and_delta_random_vs_oracle(orc, trial):
+    """Randomised O2 + O3 + STW delta against the C oracle (P2 + P4): random
+    chunk size, buffer sizes and offsets, sparse writes, a random DAG dirty
+    set.  The pre-copy pack == the oracle's pack of the chunks whose digest
+    changed outside the dirty set (bytes, entries, crcs); the dirty flags ==
+    the oracle's digest compare; the delta pack == the oracle's pack of the
+    dirty set's every chunk (at_final_stop)."""
+    rng = np.random.default_rng(5000 + trial)
+    cs = int(rng.choice([512, 1000, 4096, 65536]))
+    nb = int(rng.integers(2, 10))
+    sizes = [int(rng.integers(1, 2 << 20)) if rng.random() < 0.7 else int(rng.choice([1, cs, cs + 1, 7 * cs - 3]))
+             for _ in range(nb)]
+    handles = sorted(int(h) for h in rng.choice(np.arange(1, 1000), nb, replace=False))
+    p = Proc(orc, sizes, seed0=30000 + 100 * trial, handles=handles,
+             offsets=[int(rng.integers(0, 32)) * 16 for _ in range(nb)])
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=2 * sum(sizes) + (32 << 20)))
+    eng.register_buffers(p.bufs)
+    eng.hash_chunks()
+    prev = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    assert np.array_equal(eng.digests(), prev)
+    eng.commit_epoch()
+    for _ in range(int(rng.integers(1, 4 * nb))):
+        i = int(rng.integers(nb))
+        off = int(rng.integers(sizes[i]))
+        p.write(i, off, int(rng.integers(1, min(sizes[i] - off, 3 * cs) + 1)), int(rng.integers(1 << 40)))
+    pd.device_synchronize()
+    dag = sorted(int(h) for h in rng.choice(handles, int(rng.integers(0, nb)), replace=False))
+    eng.record_dirty(dag)
+    n = eng.plan_precopy(exclude_dag_dirty=True)
+    cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+    oflags = np.zeros(cur.size, np.uint8)
+    orc.or_dirty_flags(prev.ctypes.data, cur.ctypes.data, cur.size, 1, oflags.ctypes.data)
+    assert np.array_equal(eng.flags(), oflags)
+    elig, g = oflags.copy(), 0
+    for b in p.bufs:
+        nc = b.chunk_count(cs)
+        if b.handle in dag:
+            elig[g:g + nc] = 0
+        g += nc
+    want = opack(orc, list(zip(p.handles, p.host)), cs, elig, epoch=1)
+    assert n == want.size and np.array_equal(download_cache(eng, 0, n), want)
+    off, m = eng.at_final_stop()
+    dflags = np.concatenate([np.full(b.chunk_count(cs), b.handle in dag, np.uint8) for b in p.bufs])
+    wantd = opack(orc, list(zip(p.handles, p.host)), cs, dflags, epoch=1, pflags=1)
+    assert m == wantd.size and np.array_equal(download_cache(eng, off, m), wantd)
+    # restore scatter (materialize, cr.hpp:1026-1084) of both packs onto zeroed
+    # buffers: exactly the packed chunks come back, nothing else is written
+    packs = [download_cache(eng, 0, n), download_cache(eng, off, m)]
+    for i in range(nb):
+        p.zero(i)
+    dev = pd.DeviceMemory(max(n, m))
+    for pk in packs:
+        dev.upload(pk)
+        eng.materialize(dev.ptr, pk.size)
+        pd.device_synchronize()
+    g = 0
+    for i, b in enumerate(p.bufs):
+        got, nc = p.read(i), b.chunk_count(cs)
+        for c in range(nc):
+            lo, hi = c * cs, min(sizes[i], (c + 1) * cs)
+            shipped = elig[g + c] or dflags[g + c]
+            assert np.array_equal(got[lo:hi], p.host[i][lo:hi] if shipped else np.zeros(hi - lo, np.uint8)), (i, c)
+        g += nc
+    eng.close()
