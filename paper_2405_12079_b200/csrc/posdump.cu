@@ -482,6 +482,9 @@ void launch_copy(pos_ctx* c, const CopyItem* items, const uint64_t* n_dev, uint6
 // Runs of at least kCeRun bytes go to the copy engine (>= 4 MiB: 54 GB/s,
 // no cost to concurrent kernels); shorter ones are shipped by k_ship_runs.
 constexpr uint64_t kCeRun = 4ull << 20;
+// Pack D2H (pack / stream modes): copies of up to 64 MiB -- the copy engine
+// pays ~4 us per copy (8 MiB slices: ~2.7 % of the link; 64 MiB: 0.35 %).
+constexpr uint64_t kD2HSlice = 64ull << 20;
 
 // One batch of short runs, SoA [4][n] {src, dst, bytes, exclusive prefix} in
 // mapped pinned memory, stored into the host image by kShipCtas CTAs.
