@@ -1253,6 +1253,17 @@ def cpu_breakdown(wl: Workload, threads: int, sample_bytes: int) -> dict:
                "1": best(lambda: ref.ref_state_dump(st, prev.ctypes.data, 0, cur.ctypes.data, fl.ctypes.data, 1)),
                str(threads): best(lambda: ref.ref_state_dump(st, prev.ctypes.data, 0, cur.ctypes.data,
                                                              fl.ctypes.data, threads))}}
+    # materialize's write_content of Inline records (cr.hpp:1062-1070, buffer.hpp:80-83): the
+    # restore-side byte move, one buffer per thread
+    def write_all(nt):
+        if nt == 1:
+            for k, a in enumerate(bufs):
+                ref.ref_state_write(st, k, 0, a.ctypes.data, a.size)
+        else:
+            with ThreadPoolExecutor(nt) as ex:
+                list(ex.map(lambda k: ref.ref_state_write(st, k, 0, bufs[k].ctypes.data, bufs[k].size),
+                            range(len(bufs))))
+    out["materialize_write_content"] = {"1": best(lambda: write_all(1)), str(threads): best(lambda: write_all(threads))}
     ref.ref_state_destroy(st)
     recs = (Rec * len(bufs))()
     for k, a in enumerate(bufs):
