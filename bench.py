@@ -446,6 +446,8 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
     eng.register_buffers(bufs)
     if args.hash_sms:
         eng.set_hash_sms(args.hash_sms)
+    if args.o2_digest2:
+        eng.set_o2_digest2(True)
     if args.slice_mib or args.window:
         eng.set_host_leg(slice_bytes=(args.slice_mib or 16) << 20, window=args.window or 3)
     if wl.params:  # note_h2d_provenance (process.hpp:505-522): Upstream.crc on device
@@ -1339,6 +1341,8 @@ def main():
                     help="SMs the hash may occupy (0 = all); the application's kernels get the rest")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
     ap.add_argument("--slice-mib", type=int, default=0, help="host-leg slice size (default: the engine's 16 MiB)")
+    ap.add_argument("--o2-digest2", action="store_true",
+                    help="a second, non-linear chunk digest beside CRC-32 in the O2 compare")
     ap.add_argument("--window", type=int, default=0, help="host-leg slices in flight (default: the engine's 3)")
     ap.add_argument("--peer-cache-gb", type=float, default=0.0,
                     help="--mode stream: NVLink peer-GPU cache of this many GB on the next GPU (config 5)")

@@ -410,6 +410,13 @@ int pos_stamp_elapsed(pos_ctx* ctx, uint32_t a, uint32_t b, float* ms);
  * config.hpp:20-23) on a real GPU.  A host-link-bound dump needs ~1/8 of
  * the SMs to keep its hash ahead of the copy engine. */
 int pos_set_hash_sms(pos_ctx* ctx, uint32_t sms);
+/* A second, non-linear 32-bit chunk digest beside CRC-32 in the O2 compare
+ * (on = 1): a chunk counts as unchanged only if both digests are.  CRC-32 is
+ * GF(2)-linear, so a change by a multiple of its polynomial keeps it; the
+ * second digest (a position-keyed multiply-xorshift sum) catches that.  The
+ * reported digests stay the reference's CRC-32 (crc32.hpp:26-34).  Off by
+ * default; the first epoch after switching it on compares CRC-32s only. */
+int pos_set_o2_digest2(pos_ctx* ctx, int on);
 /* Kernels this context has launched (monotone counter). */
 int pos_launch_count(pos_ctx* ctx, uint64_t* out);
 /* Device time of the most recent hash kernel launch (ms). */

@@ -175,6 +175,7 @@ SIGNATURES = {
     "pos_image_write": [C.POINTER(pos_image_desc), P, U64, PU64],
     "pos_app_copy": [P, U64, U64, U64, I32, P],
     "pos_set_hash_sms": [P, U32],
+    "pos_set_o2_digest2": [P, I32],
     "pos_restore_replayed": [P, U64, P],
     "pos_set_host_leg": [P, U64, U32],
     "pos_host_leg_stats": [P, PU64, PU64, PU64],

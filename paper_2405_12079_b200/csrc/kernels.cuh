@@ -96,7 +96,24 @@ struct HashParams {
   uint64_t item_base;        // hash mode: first global chunk of this launch
   const uint32_t* xseg;      // [32]: x^(8 k seg_bytes) mod P
   const uint32_t* lastseg;   // [nbufs]: x^(8 * length of the tail chunk's last segment)
+  // Second, non-linear chunk digest for the O2 compare (kModeHash, opt-in):
+  // a chunk counts as clean only if its CRC-32 AND this digest are unchanged
+  uint32_t* digest2_cur;
+  const uint32_t* digest2_prev;
+  int d2_prev_valid;
 };
+
+// The second digest: a sum over the chunk's 16-B vectors of a multiply-xorshift
+// mix of the vector and its position (its 16-B index from the chunk's aligned
+// base).  Not GF(2)-linear, so a change that leaves the CRC-32 alone (a
+// multiple of its polynomial) changes it with probability 1 - 2^-32.
+__device__ __forceinline__ uint32_t d2_mix(uint4 v, uint32_t q) {
+  uint32_t a = (v.x ^ (q * 0x9E3779B1u)) * 0x85EBCA77u;
+  uint32_t b = (v.y + (a ^ (a >> 16))) * 0xC2B2AE3Du;
+  uint32_t c = (v.z ^ __funnelshift_l(b, b, 13)) * 0x27D4EB2Fu;
+  uint32_t d = (v.w + __funnelshift_l(c, c, 17)) * 0x165667B1u;
+  return d ^ (d >> 15);
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -236,9 +253,10 @@ __device__ __forceinline__ uint32_t adv_small(const uint32_t* t, uint32_t x) {
 // with x^(-8 pad).  Leading bytes below the 16-B aligned base read as zero,
 // which leaves a register that starts at 0 unchanged.  COPY: every loaded
 // vector is also stored at dst (only when src is 16-B aligned).
-template <bool COPY>
+template <bool COPY, bool D2 = false>
 __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint32_t* xinv, uint32_t lsel, int lane,
-                                               uint64_t src, uint64_t len, uint32_t k_len, uint8_t* dst) {
+                                               uint64_t src, uint64_t len, uint32_t k_len, uint8_t* dst,
+                                               uint32_t q0 = 0, uint32_t* h2 = nullptr) {
   const uint64_t a0 = src & ~15ull;
   const uint64_t lead = src - a0;
   const uint64_t end = lead + len;
@@ -248,9 +266,12 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint
   uint4* dbase = reinterpret_cast<uint4*>(dst) + lane;
 
   uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  uint32_t hs = 0;  // D2: this lane's share of the second digest
+  const uint32_t qlane = q0 + (uint32_t)lane;
   uint64_t blk = 0;
   if (lead != 0 && nblk > 1) {  // first step straddles the aligned base
     uint4 v = load_masked(a0, 0, lane, lead, end);
+    if (D2) hs += d2_mix(v, qlane);
     c0 = adv512(lsel, c0 ^ v.x);
     c1 = adv512(lsel, c1 ^ v.y);
     c2 = adv512(lsel, c2 ^ v.z);
@@ -271,6 +292,7 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (vec_copy) stg_stream(dbase + (at + u) * 32, buf[u]);
+      if (D2) hs += d2_mix(buf[u], qlane + (uint32_t)(at + u) * 32u);
       c0 = adv512(lsel, c0 ^ buf[u].x);
       c1 = adv512(lsel, c1 ^ buf[u].y);
       c2 = adv512(lsel, c2 ^ buf[u].z);
@@ -296,6 +318,7 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint
   for (; blk < full_end; ++blk) {
     uint4 v = ldg_stream(base + blk * 32);
     if (vec_copy) stg_stream(dbase + blk * 32, v);
+    if (D2) hs += d2_mix(v, qlane + (uint32_t)blk * 32u);
     c0 = adv512(lsel, c0 ^ v.x);
     c1 = adv512(lsel, c1 ^ v.y);
     c2 = adv512(lsel, c2 ^ v.z);
@@ -303,6 +326,12 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint32_t* small, const uint
   }
   // Last (partial) step: bytes past `end` read as zero.
   uint4 v = load_masked(a0, full_end, lane, lead, end);
+  if (D2) {
+    hs += d2_mix(v, qlane + (uint32_t)full_end * 32u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    *h2 = hs;
+  }
   if (vec_copy) {
     uint64_t off = full_end * kStepBytes + (uint64_t)lane * 16;
     if (off < end) stg_stream(dbase + full_end * 32, v);  // zero tail == POSD padding
@@ -406,7 +435,7 @@ __device__ unsigned long long g_hash_prof[1024][16][5];
 // (7.5 GB): 8 steps / 120 registers 1.203 ms, 6 / 96 1.22 ms; the
 // application's optimizer-tail window launched beside the dump's first
 // waves: 17x -> 1.8x slower than alone (profiles/r2/hash_regs.txt).
-template <int MODE>
+template <int MODE, bool D2 = false>
 __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
   constexpr int kThreads = kHashThreads;
   constexpr bool COPY = MODE == kModeCopy;
@@ -450,6 +479,7 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
   // are dealt round-robin over CTAs.
   constexpr int W = kThreads / 32;
   __shared__ uint32_t s_seg[2][W];
+  __shared__ uint32_t s_seg2[D2 ? 2 : 1][D2 ? W : 1];  // D2: the segments' second-digest sums
   const int warp = threadIdx.x >> 5;
   const uint32_t nseg = p.nseg;
   const uint32_t G = W / nseg;                       // groups per CTA
@@ -494,6 +524,7 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
         !(b.flags & (kBufWrittenSinceCkpt | kBufFresh | kBufStaged))) {
       if (lane == 31 && (nseg == 1 || my_seg == 0)) {
         p.digest_cur[g] = p.digest_prev[g];
+        if (D2) p.digest2_cur[g] = p.digest2_prev[g];
         if (p.flags) p.flags[g] = 0;
       }
       continue;
@@ -511,8 +542,10 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
     const uint64_t lo = (uint64_t)seg * p.seg_bytes;
     const uint64_t n = p.nseg == 1 ? len : (lo >= len ? 0 : (len - lo < p.seg_bytes ? len - lo : p.seg_bytes));
     POS_PROF(2, round == 0);
-    const uint32_t r = n ? warp_crc32<COPY>(small, p.xinv, lsel, lane, src + lo, n, p.nseg == 1 ? k_len : 0u,
-                                            COPY ? dst + lo : nullptr)
+    uint32_t h2 = 0;  // D2: the second digest of this warp's bytes
+    const uint32_t q0 = D2 ? (uint32_t)((((src + lo) & ~15ull) - (src & ~15ull)) >> 4) : 0u;
+    const uint32_t r = n ? warp_crc32<COPY, D2>(small, p.xinv, lsel, lane, src + lo, n, p.nseg == 1 ? k_len : 0u,
+                                                COPY ? dst + lo : nullptr, q0, &h2)
                          : 0u;
     POS_PROF(3, round == 0);
     if (nseg == 1) {
@@ -520,9 +553,17 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
     } else {
       // raw(chunk) = XOR_s Z^(len - end_s)(raw_s); segments past the tail are empty.
       uint32_t* slot = s_seg[round & 1] + my_group * nseg;
-      if (lane == 31) slot[seg] = r;
+      uint32_t* slot2 = D2 ? s_seg2[round & 1] + my_group * nseg : nullptr;
+      if (lane == 31) {
+        slot[seg] = r;
+        if (D2) slot2[seg] = h2;
+      }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + my_group), "r"(nseg * 32) : "memory");
       if (seg != 0) continue;  // the group's first warp folds and publishes
+      if (D2) {  // segments past the tail are empty: their sums are 0
+        h2 = 0;
+        for (uint32_t k = 0; k < nseg; ++k) h2 += slot2[k];
+      }
       const uint32_t m = (uint32_t)((len - 1) / p.seg_bytes);  // last non-empty segment
       const uint32_t xl = len == p.chunk_size ? p.xseg[1] : p.lastseg[cm.x];
       uint32_t v = 0;
@@ -537,7 +578,10 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
     if (lane == 31) {
       // a CoW-staged buffer keeps the digest of its staged snapshot (pre-copy hash only)
       const bool staged = !WORK && p.flags && (b.flags & kBufStaged);
-      if (!staged) p.digest_cur[g] = crc;
+      if (!staged) {
+        p.digest_cur[g] = crc;
+        if (D2) p.digest2_cur[g] = h2;
+      }
       if (WORK) {
         uint4* e = reinterpret_cast<uint4*>(p.pack + kPackHeader + (uint64_t)entry * kPackEntry);
         e[0] = make_uint4((uint32_t)b.handle, (uint32_t)(b.handle >> 32), (uint32_t)dst_off,
@@ -546,7 +590,8 @@ __global__ void __maxnreg__(96) k_hash_chunks(HashParams p) {
       } else if (staged) {
         p.flags[g] = 0;  // its snapshot is in the staging pack: nothing to ship
       } else if (p.flags) {
-        const bool dirty = !p.prev_valid || (b.flags & kBufFresh) || p.digest_prev[g] != crc;
+        const bool dirty = !p.prev_valid || (b.flags & kBufFresh) || p.digest_prev[g] != crc ||
+                           (D2 && p.d2_prev_valid && p.digest2_prev[g] != h2);
         p.flags[g] = dirty;
         if (dirty && p.bitmap) atomicOr(p.bitmap + (g >> 5), 1u << (g & 31));
       }

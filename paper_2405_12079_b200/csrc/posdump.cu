@@ -118,7 +118,10 @@ struct PinnedArray {
 
 template <int MODE>
 void launch_hash(int grid, cudaStream_t s, const HashParams& p) {
-  k_hash_chunks<MODE><<<grid, kHashThreads, kHashSmem, s>>>(p);
+  if (MODE == kModeHash && p.digest2_cur)
+    k_hash_chunks<kModeHash, true><<<grid, kHashThreads, kHashSmem, s>>>(p);
+  else
+    k_hash_chunks<MODE><<<grid, kHashThreads, kHashSmem, s>>>(p);
 }
 
 // Tables shared by every launch on a device: Z^512 (replicated in smem by the
@@ -145,6 +148,8 @@ struct CrcTables {
     ck(cudaFuncSetAttribute(k_hash_chunks<kModeCopy>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
        "smem attr");
     ck(cudaFuncSetAttribute(k_hash_chunks<kModeCached>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
+       "smem attr");
+    ck(cudaFuncSetAttribute(k_hash_chunks<kModeHash, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem),
        "smem attr");
     ck(cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem),
        "smem attr");
@@ -292,6 +297,10 @@ struct pos_ctx {
   DevArray<DevBuf> d_bufs;
   DevArray<uint2> d_chunk_map;
   DevArray<uint32_t> d_digest[2];
+  // the optional second digest of the O2 compare (pos_set_o2_digest2), same
+  // double buffering as d_digest; d2_valid: the previous table is complete
+  DevArray<uint32_t> d_digest2[2];
+  bool digest2 = false, d2_valid = false, d2_ran = false;
   int cur = 0;
   bool prev_valid = false;
   bool fresh_target = false;  // CheckpointTarget::fresh (cr.hpp:35): this round ships every chunk

@@ -355,6 +355,10 @@ class DumpEngine:
         """SMs the hash may occupy (0 = all): the rest stay with the application."""
         check(lib().pos_set_hash_sms(self.ctx, sms))
 
+    def set_o2_digest2(self, on: bool = True) -> None:
+        """A second, non-linear chunk digest in the O2 compare (pos_set_o2_digest2)."""
+        check(lib().pos_set_o2_digest2(self.ctx, 1 if on else 0))
+
     def set_host_leg(self, slice_bytes: int = 16 << 20, window: int = 3) -> None:
         check(lib().pos_set_host_leg(self.ctx, slice_bytes, window))
 

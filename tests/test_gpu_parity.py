@@ -1812,3 +1812,111 @@ def test_pack_and_delta_random_vs_oracle(orc, trial):
             assert np.array_equal(got[lo:hi], p.host[i][lo:hi] if shipped else np.zeros(hi - lo, np.uint8)), (i, c)
         g += nc
     eng.close()
+
+
+def crc_null_change(orc, n, start):
+    """A nonzero byte pattern E of length n (bits in bytes [start, start+8))
+    with crc32(A ^ E) == crc32(A) for every A of length n: CRC-32 is affine
+    in its input, so a GF(2) dependency among the CRC effects of 64 single
+    bits is a change it cannot see."""
+    zeros = np.zeros(n, np.uint8)
+    z = orc.or_crc32(zeros.ctypes.data, n)
+    basis = {}
+    for i in range(64):
+        e = zeros.copy()
+        e[start + i // 8] ^= 1 << (i % 8)
+        v, m = orc.or_crc32(e.ctypes.data, n) ^ z, 1 << i
+        while v:
+            h = v.bit_length() - 1
+            if h not in basis:
+                basis[h] = (v, m)
+                break
+            v, m = v ^ basis[h][0], m ^ basis[h][1]
+        if v == 0:
+            out = zeros.copy()
+            for k in range(64):
+                if m >> k & 1:
+                    out[start + k // 8] ^= 1 << (k % 8)
+            return out
+    raise AssertionError("no dependency among 64 bits")
+
+
+@pytest.mark.parametrize("d2", [False, True])
+def test_o2_second_digest_catches_crc_preserving_change(orc, d2):
+    """The chunk-level O2 compare's blind spot, and its guard: a change that
+    leaves a chunk's CRC-32 unchanged (XOR of a multiple of the polynomial)
+    is invisible to a CRC-32-only compare (the documented residual risk) and
+    caught by the second digest (pos_set_o2_digest2).  The reported digest
+    stays the reference's CRC-32 either way."""
+    cs = 65536
+    p = Proc(orc, [4 * cs, 3 * cs + 100], seed0=8800)
+    E = crc_null_change(orc, cs, 1000)
+    a = p.host[0][cs:2 * cs]
+    assert E.any() and orc.or_crc32(a.ctypes.data, cs) == orc.or_crc32((a ^ E).ctypes.data, cs)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=1 << 20))
+    eng.register_buffers(p.bufs)
+    eng.set_o2_digest2(d2)
+    eng.hash_chunks()
+    d0 = eng.digests().copy()
+    eng.commit_epoch()
+    changed = a ^ E
+    p.mem[0].upload(changed, offset=cs)
+    p.host[0][cs:2 * cs] = changed
+    pd.device_synchronize()
+    eng.hash_chunks()
+    assert np.array_equal(eng.digests(), d0)  # the CRC-32s did not move
+    flags = eng.flags()
+    want = np.zeros(d0.size, np.uint8)
+    if d2:
+        want[1] = 1
+    assert np.array_equal(flags, want)
+    eng.close()
+
+
+@pytest.mark.parametrize("cs,offsets", [(65536, None), (4096, [0, 3, 0, 9, 5]), (1000, [0, 1, 2, 3, 4])])
+def test_o2_second_digest_is_exact_on_ordinary_writes(orc, cs, offsets):
+    """With the second digest on, the dirty flags of ordinary writes equal
+    the CRC-32 compare's (the oracle's) across three epochs and varying wave
+    counts, through the direct pre-copy into an image, at unaligned buffer
+    starts and a chunk size that is not a multiple of 16, and a buffer-set
+    change carries the second digests along."""
+    sizes = [3 * cs + 7, 17, cs, 9 * cs, 5 * cs + 1]
+    p = Proc(orc, sizes, seed0=8900, offsets=offsets)
+    eng = pd.DumpEngine(pd.SimConfig(chunk_size=cs, cache_capacity=16 << 20))
+    eng.register_buffers(p.bufs)
+    eng.set_o2_digest2(True)
+    pin = pd.PinnedHost(sum(sizes))
+    image, o = [], 0
+    for n in sizes:
+        image.append(pin.array[o:o + n])
+        o += n
+    eng.register_image(image)
+    s, d = pd.Stream(), pd.Stream()
+    rng = np.random.default_rng(cs)
+    prev = None
+    for epoch in range(3):
+        if epoch:
+            for _ in range(6):
+                i = int(rng.integers(len(sizes)))
+                off = int(rng.integers(sizes[i]))
+                p.write(i, off, int(rng.integers(1, min(sizes[i] - off, 300) + 1)), int(rng.integers(1 << 30)))
+            pd.device_synchronize()
+        eng.precopy_direct(waves=int(rng.integers(1, 3)), stream=s, drain_stream=d)
+        eng.precopy_direct_result()
+        d.synchronize()
+        cur = np.concatenate([odigests(orc, h, cs) for h in p.host])
+        if prev is not None:
+            oflags = np.zeros(cur.size, np.uint8)
+            orc.or_dirty_flags(prev.ctypes.data, cur.ctypes.data, cur.size, 1, oflags.ctypes.data)
+            assert np.array_equal(eng.flags(), oflags), epoch
+        for i in range(len(sizes)):
+            assert np.array_equal(image[i], p.host[i]), (epoch, i)
+        prev = cur
+        eng.commit_epoch()
+    # a buffer-set change keeps the surviving buffers' digests (both kinds): nothing ships
+    eng.update_buffer_set(p.bufs)
+    eng.register_image(image)
+    eng.precopy_direct(waves=1, stream=s, drain_stream=d)
+    nch, _ = eng.precopy_direct_result()
+    assert nch == 0
+    eng.close()

@@ -20,6 +20,8 @@ pd.fill_batch([(b.dev_ptr, b.size, 5000 + b.handle) for b in bufs])
 pd.device_synchronize()
 eng = pd.DumpEngine(pd.SimConfig(chunk_size=65536, cache_capacity=2 << 30))
 eng.register_buffers(bufs)
+if "--digest2" in sys.argv:  # the O2 compare's second digest on
+    eng.set_o2_digest2(True)
 for i in range(4):
     pd.check(pd.lib().pos_memset(flush.ptr, i, flush.nbytes, None))
     pd.device_synchronize()
