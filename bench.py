@@ -773,6 +773,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         np.array_equal(img, mem.download(b.size, offset=b.dev_ptr - mem.ptr)) for b, img in zip(bufs, host_image)))
     restore = (restore_measure(eng, pd, wl, bufs, host_image, mem, e)
                if (wl.name in ("c3", "c4", "c5") and direct) else None)
+    writer = image_writer_measure(pd, bufs, host_image) if (direct and wl.total > (4 << 30)) else None
     if restore is not None:
         ok = ok and restore["digests_match_checkpoint"] and restore["delta_replay"]["bit_exact"]
 
@@ -918,6 +919,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
                                   "; whole image: device state lost, restored from the image, every chunk "
                                   "digest == the checkpoint's")),
             **({"restore": restore} if restore else {}),
+            **({"image_writer": writer} if writer else {}),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -1031,6 +1033,34 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
                              "alg_bytes": "2 x payload (read pack, write buffers)", "bit_exact": bool(delta_ok),
                              "no_stray_writes": bool(
                                  int(np.count_nonzero(replay_dig != digests_ckpt)) <= pack_entries(writes))}}
+
+
+def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> dict:
+    """The streaming POSI writer (write_image, image.hpp:136-207; SURVEY 8(f)
+    rank 1) on a prefix of the checkpoint image: Inline records straight from
+    the pinned host image into a pre-touched output buffer, one host thread."""
+    recs, allocs, acc = [], [], 0
+    for b, img in zip(bufs, host_image):
+        if acc >= sample_bytes:
+            break
+        recs.append(pd.GpuBufferRec(handle=b.handle, kind=0, inline_bytes=img))
+        allocs.append((b.handle, 0x7000_0000_0000 + acc, b.size))
+        acc += b.size
+    ci = pd.CheckpointImage(page_size=4096, gpu_records=recs, allocs=allocs, next_handle=len(recs) + 1)
+    out = np.zeros(acc + (1 << 20) + 64 * len(recs), np.uint8)
+    out[::4096] = 1  # first touch outside the timed call
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        n = pd.write_image(ci, out=out)
+        times.append(time.perf_counter() - t0)
+    ms = min(times) * 1e3
+    del out
+    return {"bytes": int(n), "records": len(recs), "ms": round(ms, 2), "gbps": round(n / (ms * 1e-3) / 1e9, 2),
+            "threads": 1,
+            "how": "pos_image_write of a POSI image of the first buffers' Inline records (from the pinned host "
+                   "image) into a pre-touched buffer; byte-identity with the reference's write_image is "
+                   "tests/test_capi.py; the reference's own write_image: cpu_breakdown.write_image"}
 
 
 def pack_entries(writes) -> int:

@@ -764,7 +764,10 @@ def finalize_image(host_side: CheckpointImage, bufs: Sequence[FinalizeBuf], engi
     return out.tobytes(), {k: int(getattr(m, k)) for k in METRIC_KEYS}
 
 
-def write_image(img: CheckpointImage) -> bytes:
+def write_image(img: CheckpointImage, out: Optional[np.ndarray] = None):
+    """write_image (image.hpp:136-207) through pos_image_write: the POSI bytes,
+    or -- with `out` (a uint8 array at least that large) -- written into
+    `out` without a copy, returning the image size."""
     keep = []
     pages = (_lib.pos_image_page * max(len(img.host_pages), 1))()
     for i, (idx, data) in enumerate(img.host_pages):
@@ -800,7 +803,10 @@ def write_image(img: CheckpointImage) -> bytes:
     d.cursor, d.next_handle, d.next_base = img.cursor, img.next_handle, img.next_base
     d.dag_bytes, d.dag_len = (dag.ctypes.data if dag.size else None), dag.size
     size = C.c_uint64(0)
+    if out is not None:
+        check(lib().pos_image_write(C.byref(d), out.ctypes.data, out.nbytes, C.byref(size)))
+        return size.value
     check(lib().pos_image_write(C.byref(d), None, 0, C.byref(size)))
-    out = np.empty(size.value, dtype=np.uint8)
-    check(lib().pos_image_write(C.byref(d), out.ctypes.data, out.nbytes, C.byref(size)))
-    return out.tobytes()
+    buf = np.empty(size.value, dtype=np.uint8)
+    check(lib().pos_image_write(C.byref(d), buf.ctypes.data, buf.nbytes, C.byref(size)))
+    return buf.tobytes()
