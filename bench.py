@@ -1038,7 +1038,8 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
 def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> dict:
     """The streaming POSI writer (write_image, image.hpp:136-207; SURVEY 8(f)
     rank 1) on a prefix of the checkpoint image: Inline records straight from
-    the pinned host image into a pre-touched output buffer, one host thread."""
+    the pinned host image into a pre-touched output buffer (the payload
+    copies on up to 16 host threads)."""
     recs, allocs, acc = [], [], 0
     for b, img in zip(bufs, host_image):
         if acc >= sample_bytes:
@@ -1057,7 +1058,7 @@ def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> d
     ms = min(times) * 1e3
     del out
     return {"bytes": int(n), "records": len(recs), "ms": round(ms, 2), "gbps": round(n / (ms * 1e-3) / 1e9, 2),
-            "threads": 1,
+            "threads": min(16, os.cpu_count() or 1),
             "how": "pos_image_write of a POSI image of the first buffers' Inline records (from the pinned host "
                    "image) into a pre-touched buffer; byte-identity with the reference's write_image is "
                    "tests/test_capi.py; the reference's own write_image: cpu_breakdown.write_image"}

@@ -9,10 +9,12 @@
 // Inline payloads stream straight from wherever the dump landed them.
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/posdump.h"
@@ -35,10 +37,23 @@ inline bool posi_meta_default(const pos_image_desc& d) {  // image.hpp:68-71
          d.next_base == kDeviceAddrBase;
 }
 
+// Large payloads (Inline bytes, host pages) are not copied in the cursor's
+// pass: their places are known there, so the copies run afterwards on
+// several host threads (one thread moves ~14 GB/s; the writer streams tens
+// of GB per checkpoint).
+struct PosiCopy {
+  uint8_t* dst;
+  const uint8_t* src;
+  uint64_t n;
+};
+
 struct PosiCursor {
   uint8_t* p;
+  std::vector<PosiCopy>* deferred = nullptr;
+  static constexpr uint64_t kDeferMin = 1ull << 20;
   void raw(const void* s, uint64_t n) {
-    if (n) std::memcpy(p, s, n);
+    if (n >= kDeferMin && deferred) deferred->push_back(PosiCopy{p, static_cast<const uint8_t*>(s), n});
+    else if (n) std::memcpy(p, s, n);
     p += n;
   }
   void u8(uint8_t v) { raw(&v, 1); }
@@ -46,6 +61,32 @@ struct PosiCursor {
   void u32(uint32_t v) { raw(&v, 4); }
   void u64(uint64_t v) { raw(&v, 8); }
 };
+
+// The deferred copies in 64 MiB pieces over up to 16 threads.
+inline void run_posi_copies(const std::vector<PosiCopy>& cps) {
+  constexpr uint64_t kPiece = 64ull << 20;
+  std::vector<PosiCopy> pieces;
+  uint64_t total = 0;
+  for (const PosiCopy& c : cps)
+    for (uint64_t o = 0; o < c.n; o += kPiece) {
+      pieces.push_back(PosiCopy{c.dst + o, c.src + o, std::min(kPiece, c.n - o)});
+      total += pieces.back().n;
+    }
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nt = (unsigned)std::min<uint64_t>({(uint64_t)std::min(hw, 16u), pieces.size(), total / kPiece + 1});
+  if (nt <= 1) {
+    for (const PosiCopy& c : pieces) std::memcpy(c.dst, c.src, c.n);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i = next++; i < pieces.size(); i = next++) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
 
 inline int write_posi_image(const pos_image_desc& d, uint8_t* out, uint64_t cap, uint64_t* size,
                             std::string* err) {
@@ -91,7 +132,8 @@ inline int write_posi_image(const pos_image_desc& d, uint8_t* out, uint64_t cap,
   *size = total;
   if (!out || cap < total) return POS_OK;
 
-  PosiCursor w{out};
+  std::vector<PosiCopy> deferred;
+  PosiCursor w{out, &deferred};
   w.raw("POSI", 4);
   w.u16(1);
   w.u16(d.dag_len ? 1 : 0);
@@ -138,6 +180,7 @@ inline int write_posi_image(const pos_image_desc& d, uint8_t* out, uint64_t cap,
     w.u64(d.next_handle);
     w.u64(d.next_base);
   }
+  run_posi_copies(deferred);
   return POS_OK;
 }
 

@@ -273,3 +273,20 @@ def test_read_image_check_matches_reference(orc, ref):
             n_valid += want == 0
             n_checked += 1
     assert n_valid > 50 and n_checked > 3500
+
+
+def test_write_image_large_payloads_vs_reference(orc, ref):
+    """Inline payloads of 1-70 MiB (copied by the writer's thread pool in
+    64 MiB pieces after its layout pass) and 1 MiB host pages: byte-identical
+    to the reference's write_image."""
+    from oracle_ctypes import ref_image
+    rng = np.random.default_rng(77)
+    sizes = [1 << 20, (1 << 20) - 1, 3 * (1 << 20) + 5, 70 * (1 << 20) + 3, 200]
+    recs, allocs, base = [], [], BASE
+    for h, size in zip([9, 2, 5, 7, 11], sizes):
+        allocs.append((h, base, size))
+        base += (size + 255) // 256 * 256
+        recs.append({"handle": h, "kind": 0, "seed": int(rng.integers(1, 1 << 30)), "len": size})
+    d = {"name": "large", "page_size": 1 << 20, "pages": [(3, 11), (0, 12)], "recs": recs, "allocs": allocs,
+         "streams": [1], "cursor": 5, "next_handle": 12, "next_base": base, "dag": ""}
+    assert pd.write_image(_image_from_desc(orc, d)) == ref_image(ref, d)
