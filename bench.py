@@ -1036,6 +1036,7 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
 
 
 def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> dict:
+    import ctypes as C
     """The streaming POSI writer (write_image, image.hpp:136-207; SURVEY 8(f)
     rank 1) on a prefix of the checkpoint image: Inline records straight from
     the pinned host image into a pre-touched output buffer (the payload
@@ -1056,8 +1057,16 @@ def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> d
         n = pd.write_image(ci, out=out)
         times.append(time.perf_counter() - t0)
     ms = min(times) * 1e3
+    # read_image's validation of the same bytes (image.hpp:209-361), zero-copy
+    off = C.c_uint64(0)
+    t0 = time.perf_counter()
+    rc = pd.lib().pos_image_check(out.ctypes.data, int(n), C.byref(off))
+    check_ms = (time.perf_counter() - t0) * 1e3
     del out
     return {"bytes": int(n), "records": len(recs), "ms": round(ms, 2), "gbps": round(n / (ms * 1e-3) / 1e9, 2),
+            "read_check": {"valid": rc == 0, "ms": round(check_ms, 3),
+                           "how": "pos_image_check: read_image's structural checks over the bytes in place "
+                                  "(zero-copy; the reference's read_image parses and copies every payload)"},
             "threads": min(16, os.cpu_count() or 1),
             "how": "pos_image_write of a POSI image of the first buffers' Inline records (from the pinned host "
                    "image) into a pre-touched buffer; byte-identity with the reference's write_image is "
