@@ -773,7 +773,7 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         np.array_equal(img, mem.download(b.size, offset=b.dev_ptr - mem.ptr)) for b, img in zip(bufs, host_image)))
     restore = (restore_measure(eng, pd, wl, bufs, host_image, mem, e)
                if (wl.name in ("c3", "c4", "c5") and direct) else None)
-    writer = image_writer_measure(pd, bufs, host_image) if (direct and wl.total > (4 << 30)) else None
+    writer = image_writer_measure(pd, eng, bufs, host_image) if (direct and wl.total > (4 << 30)) else None
     if restore is not None:
         ok = ok and restore["digests_match_checkpoint"] and restore["delta_replay"]["bit_exact"]
 
@@ -1035,7 +1035,7 @@ def restore_measure(eng, pd, wl, bufs, host_image, mem, e):
                                  int(np.count_nonzero(replay_dig != digests_ckpt)) <= pack_entries(writes))}}
 
 
-def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> dict:
+def image_writer_measure(pd, eng, bufs, host_image, sample_bytes: int = 8 << 30) -> dict:
     import ctypes as C
     """The streaming POSI writer (write_image, image.hpp:136-207; SURVEY 8(f)
     rank 1) on a prefix of the checkpoint image: Inline records straight from
@@ -1062,12 +1062,24 @@ def image_writer_measure(pd, bufs, host_image, sample_bytes: int = 8 << 30) -> d
     t0 = time.perf_counter()
     rc = pd.lib().pos_image_check(out.ctypes.data, int(n), C.byref(off))
     check_ms = (time.perf_counter() - t0) * 1e3
+    # ... and the image restored from those (pageable) bytes: the buffers get
+    # back what they hold (read_image + materialize, pos_image_restore)
+    loaded, recomp, coff = C.c_uint32(0), C.c_uint32(0), C.c_uint64(0)
+    s = pd.Stream()
+    t0 = time.perf_counter()
+    rrc = pd.lib().pos_image_restore(eng.ctx, out.ctypes.data, int(n), int(s), C.byref(coff), C.byref(loaded),
+                                     C.byref(recomp))
+    restore_ms = (time.perf_counter() - t0) * 1e3
     del out
     return {"bytes": int(n), "records": len(recs), "ms": round(ms, 2), "gbps": round(n / (ms * 1e-3) / 1e9, 2),
             "read_check": {"valid": rc == 0, "ms": round(check_ms, 3),
                            "how": "pos_image_check: read_image's structural checks over the bytes in place "
                                   "(zero-copy; the reference's read_image parses and copies every payload)"},
             "threads": min(16, os.cpu_count() or 1),
+            "restore_from_image": {"ok": rrc == 0, "records": int(loaded.value), "ms": round(restore_ms, 2),
+                                   "gbps": round(n / (restore_ms * 1e-3) / 1e9, 2),
+                                   "how": "pos_image_restore of the written image from pageable host memory "
+                                          "(checks, then one H2D per record)"},
             "how": "pos_image_write of a POSI image of the first buffers' Inline records (from the pinned host "
                    "image) into a pre-touched buffer; byte-identity with the reference's write_image is "
                    "tests/test_capi.py; the reference's own write_image: cpu_breakdown.write_image"}

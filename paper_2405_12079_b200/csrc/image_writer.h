@@ -62,9 +62,8 @@ struct PosiCursor {
   void u64(uint64_t v) { raw(&v, 8); }
 };
 
-// The deferred copies in 64 MiB pieces over up to 16 threads.
-inline void run_posi_copies(const std::vector<PosiCopy>& cps) {
-  constexpr uint64_t kPiece = 64ull << 20;
+// The deferred copies in kPiece pieces over up to 16 threads.
+inline void run_posi_copies(const std::vector<PosiCopy>& cps, uint64_t kPiece = 64ull << 20) {
   std::vector<PosiCopy> pieces;
   uint64_t total = 0;
   for (const PosiCopy& c : cps)
