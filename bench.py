@@ -467,9 +467,10 @@ def run_gpu(args, wl: Workload, world, rank, local, dist):
         # The checkpoint image itself is pinned + mapped: the copy engine moves
         # every shipped chunk to its place (chunk_copied, cr.hpp:499-501).
         img_offs, o = [], 0
+        align = args.image_align or 256
         for b in bufs:
             img_offs.append(o)
-            o += (b.size + 255) // 256 * 256
+            o += (b.size + align - 1) // align * align
         log(f"allocating the pinned host image ({o} B)")
         img_pin = pd.PinnedHost(max(o, 1), image=True)  # zero-filled huge pages, pinned + mapped
         huge_gb = anon_huge_gb()
@@ -1393,6 +1394,8 @@ def main():
                     help="SMs the hash may occupy (0 = all); the application's kernels get the rest")
     ap.add_argument("--drain-priority", type=int, default=-1, help="host-leg stream priority (default: as the dump)")
     ap.add_argument("--slice-mib", type=int, default=0, help="host-leg slice size (default: the engine's 16 MiB)")
+    ap.add_argument("--image-align", type=int, default=0,
+                    help="alignment of each buffer's range in the host image (default 256 B)")
     ap.add_argument("--o2-digest2", action="store_true",
                     help="a second, non-linear chunk digest beside CRC-32 in the O2 compare")
     ap.add_argument("--window", type=int, default=0, help="host-leg slices in flight (default: the engine's 3)")
