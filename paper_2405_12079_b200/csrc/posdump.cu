@@ -391,7 +391,8 @@ struct pos_ctx {
   uint64_t scan_seq = 0, slot_seq[kMaxWaves] = {};  // host-mirror sequence numbers
   // cache-cycled pre-copy (pos_precopy_stream): 2 cache regions, 2 pinned landing slots
   PinnedArray<uint8_t> h_land[2];
-  PinnedArray<uint8_t> h_bounce[2];           // pos_image_restore from pageable bytes
+  uint8_t* h_bounce = nullptr;                // pos_image_restore from pageable bytes: 2 slots
+                                              // (pos_host_image_alloc)
   cudaEvent_t ev_bounce[2] = {nullptr, nullptr};
   cudaEvent_t ev_d2h[2] = {}, ev_copied2[2] = {};
   bool pack_pending = false;
