@@ -1,6 +1,7 @@
 // kernels.cuh -- sm_100a kernels of the buffer-dump hot path.
 //
-//   k_hash_chunks<MODE>  O2 digest + dirty flags (kModeHash), digest + gather
+//   k_hash_chunks<MODE,D2> O2 digest + dirty flags (kModeHash; D2: plus the
+//                        opt-in second digest), digest + gather
 //                        into a POSD pack (kModeCopy: CoW staging), or digest
 //                        of chunks already gathered into a pack (kModeCached:
 //                        the STW delta is a pure bulk gather; its hashing
@@ -14,6 +15,7 @@
 //                        (handle, chunk)-ordered pack layout and its copy items
 //   k_copy_bulk          TMA bulk copies (cp.async.bulk) staged through smem
 //   k_copy_simt          16-B vector / byte copies (unaligned items)
+//   k_ship_runs          host leg, short runs: SM stores into the mapped image
 //   k_pack_items         restore: POSD entries -> scatter copy items
 //   k_stage_in           SM loads of the staged STW delta layout
 //   k_fill               fill_bytes(seed) (rng.hpp:43-54) into device memory
