@@ -36,4 +36,14 @@ for i in range(2):
     off, nb = eng.at_final_stop(stw_begin_slot=3, stw_end_slot=4)
     pd.device_synchronize()
     print("stw gather ms", round(eng.event_elapsed(3, 4), 4), "bytes", nb)
+# restore-side scatter (materialize, cr.hpp:1026-1084) of that delta pack back
+# into the buffers: k_pack_items + k_copy_bulk (the 3rd/4th k_copy_bulk launch)
+cache_ptr, _ = eng.cache()
+for i in range(2):
+    pd.check(pd.lib().pos_memset(flush.ptr, i, flush.nbytes, None))
+    pd.device_synchronize()
+    eng.materialize(cache_ptr + off, nb)
+    pd.device_synchronize()
+    print("scatter ms", round(eng.kernel_ms("scatter"), 4), "GB/s (2x payload)",
+          round(2 * 9 * SZ / eng.kernel_ms("scatter") / 1e6, 1))
 eng.close()
